@@ -1,0 +1,128 @@
+/*
+ * sk200.h -- C ABI of the B200-native matrix-free spectral/hp operator path.
+ *
+ * This is the drop-in boundary for the reference's per-block operator API
+ * (speckern/operators.py:551-776).  Every entry point below replaces one
+ * reference function; the reference file:line is cited beside it.  There
+ * are no torch (or any C++) types in these signatures: plain pointers,
+ * sizes and a cudaStream_t passed as void*.
+ *
+ * Conventions
+ *  - All field/payload pointers are DEVICE pointers owned by the caller.
+ *  - Fields use the reference's lane-major block layout
+ *    (speckern/field_block.py:205-214): for component c, element e and data
+ *    point n the double lives at ((c*G + e/W)*N + n)*W + e%W, with
+ *    W = interleave width, G = ceil(E/W) groups, N = n_modes or n_points.
+ *    W = 1 is plain element-major.  Padded lanes (e >= E) are written as 0.
+ *  - Mode order is lexicographic (p,q,r) with p slowest (shapes.py:142-179);
+ *    point order is l = (i*Q1 + j)*Q2 + k (shapes.py:482-487).
+ *  - Geometry enters as the reference's GeometricFactors
+ *    (geometry.py:94-116) and is packed once per block into a device
+ *    payload by sk_payload_pack (replaces Block.payload,
+ *    field_block.py:309-363); applies then stream the packed payload.
+ *  - Every call is stream-ordered and re-entrant.  The only shared state is
+ *    the immutable per-(shape, order) basis handle.
+ *  - Status: 0 ok; 1 bad state/shape; 2 unsupported (shape, order);
+ *    3 bad argument (lam < 0, E < 0, null pointer, W < 1);
+ *    4 CUDA error (see sk_last_error()).
+ */
+#ifndef SK200_H
+#define SK200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* shape ids = index in the reference's Shape enum (shapes.py:57-65) */
+enum { SK_SHAPE_QUAD = 0, SK_SHAPE_TRI = 1, SK_SHAPE_HEX = 2,
+       SK_SHAPE_PRISM = 3, SK_SHAPE_PYR = 4, SK_SHAPE_TET = 5 };
+/* GeometryClass (geometry.py:35-39) */
+enum { SK_GEO_REGULAR = 0, SK_GEO_DEFORMED = 1 };
+/* payload kinds: what Block.payload(...) feeds each operator family */
+enum { SK_PAYLOAD_HELMHOLTZ = 0,  /* lam + wj ("lam","wj"/"jac" keys)      */
+       SK_PAYLOAD_W = 1,          /* W diagonal ("wj" / "jac" keys)        */
+       SK_PAYLOAD_DERIV = 2 };    /* inverse Jacobian ("dxi" key)          */
+/* Helmholtz formulations (operators.py:702-721) */
+enum { SK_FORM_COLL = 0, SK_FORM_NONCOLL = 1 };
+enum { SK_OK = 0, SK_ERR_STATE = 1, SK_ERR_UNSUPPORTED = 2, SK_ERR_ARG = 3, SK_ERR_CUDA = 4 };
+
+typedef struct sk_basis sk_basis;
+
+/* ---- basis / constant tables -------------------------------------------
+ * Replaces build_shape_basis (shapes.py:521-541) + SumFacTables
+ * (shapes.py:444-456, 555-583): 1D rules (bases.py:235-270), modified
+ * bases (bases.py:277-354), collocation matrices (bases.py:468-477) and
+ * Duffy chain-rule factors (shapes.py:265-323), built natively in FP64.
+ * Host-only; device copies are made lazily per device on first use. */
+int sk_basis_create(int shape, int order, sk_basis** out);
+int sk_basis_destroy(sk_basis* b);
+/* counts: out[0..5] = Q0, Q1, Q2, n_points, n_modes, order */
+int sk_basis_counts(const sk_basis* b, int64_t out[6]);
+/* Read back a named host table (for tests and the host API): "z0".."z2",
+ * "w0".."w2", "D0".."D2", "a0".."a2", "da0".."da2", "b1_<p>", "db1_<p>",
+ * "c2_<p>", "dc2_<p>", "refw", "G", "modes".  Writes up to cap doubles,
+ * returns the table length via *len (0 when absent). */
+int sk_basis_table(const sk_basis* b, const char* name, double* out, int64_t cap, int64_t* len);
+
+/* ---- geometry -------------------------------------------------------------
+ * Payload size in doubles for E elements. */
+int sk_payload_size(const sk_basis* b, int geo_class, int kind, int64_t E, int64_t* n_doubles);
+/* Pack GeometricFactors (device, reference layout: dxi_dx (E,NQ,3,3) or
+ * (E,3,3); jac (E,NQ) or (E,)) into the kernel payload of `kind`.
+ * Replaces Block._build_payload (field_block.py:331-363). */
+int sk_payload_pack(const sk_basis* b, int geo_class, int kind, int64_t E,
+                    const double* dxi_dx, const double* jac, double* payload, void* stream);
+/* Device geometry builder (replaces make_synthetic_factors for DEFORMED,
+ * geometry.py:275-315 -> 161-212): per-element deformation parameters
+ * params[E][12] = amp[3], phase[3], perm[3] (as doubles), shift[3] ->
+ * dxi_dx (E,NQ,3,3) and jac = w|J| (E,NQ).  *n_bad receives the number of
+ * points with |J| <= 0 (DegenerateElementError, geometry.py:203-209). */
+int sk_geometry_deformed(const sk_basis* b, int64_t E, const double* params,
+                         double* dxi_dx, double* jac, int64_t* n_bad, void* stream);
+/* Device geometry builder straight into a kernel payload of `kind`
+ * (no dxi/jac materialised): the large-mesh path of the bench (H7). */
+int sk_payload_from_params(const sk_basis* b, int kind, int64_t E, const double* params,
+                           double* payload, int64_t* n_bad, void* stream);
+/* Iso-parametric factors from coordinates coords (E,NQ,3) (geometry.py:161-212). */
+int sk_geometry_from_coords(const sk_basis* b, int64_t E, const double* coords,
+                            double* dxi_dx, double* jac, int64_t* n_bad, void* stream);
+
+/* ---- operators (SUM_FAC_TOP: one CTA per element tile) -------------------- */
+/* bwd_trans (operators.py:551-561): coeff -> phys, per component */
+int sk_bwd_trans(const sk_basis* b, int64_t E, int W, int ncomp,
+                 const double* uhat, double* u, void* stream);
+/* iproduct_wrt_base (operators.py:564-574): phys -> coeff; payload kind W */
+int sk_iproduct_wrt_base(const sk_basis* b, int geo_class, int64_t E, int W, int ncomp,
+                         const double* u, const double* wpay, double* fhat, void* stream);
+/* phys_deriv (operators.py:577-596): 1 phys component -> 3; payload kind DERIV */
+int sk_phys_deriv(const sk_basis* b, int geo_class, int64_t E, int W,
+                  const double* u, const double* dpay, double* du, void* stream);
+/* iproduct_wrt_deriv_base (operators.py:599-619): 3 phys components -> 1 coeff; payload kind W */
+int sk_iproduct_wrt_deriv_base(const sk_basis* b, int geo_class, int64_t E, int W,
+                               const double* v, const double* wpay, double* fhat, void* stream);
+/* mass_apply (operators.py:622-633); payload kind W */
+int sk_mass_apply(const sk_basis* b, int geo_class, int64_t E, int W, int ncomp,
+                  const double* uhat, const double* wpay, double* out, void* stream);
+/* helmholtz_apply[_coll|_noncoll] (operators.py:636-721); payload kind
+ * HELMHOLTZ.  lam == 0 is the stiffness operator and skips the
+ * W stream. */
+int sk_helmholtz_apply(const sk_basis* b, int geo_class, int form, int64_t E, int W, int ncomp,
+                       const double* uhat, const double* hpay, double lam, double* out, void* stream);
+
+/* ---- diagnostics ------------------------------------------------------------ */
+/* Number of kernel launches this thread issued through the library. */
+int64_t sk_launch_count(void);
+/* Last error message of the calling thread ("" when none). */
+const char* sk_last_error(void);
+/* Kernel launch configuration chosen for an operator: out[0]=elements per
+ * CTA, out[1]=threads per CTA, out[2]=dynamic shared bytes. op: 0 helmholtz,
+ * 1 mass, 2 bwd, 3 iprod, 4 physderiv, 5 iprod_deriv. */
+int sk_launch_config(const sk_basis* b, int op, int64_t out[3]);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SK200_H */

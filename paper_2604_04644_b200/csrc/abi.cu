@@ -1,0 +1,323 @@
+// C ABI (include/sk200.h): argument checking, basis handles and dispatch to
+// the per-(shape, order) instantiations.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/sk200.h"
+#include "sk_opset.hpp"
+
+namespace sk {
+
+namespace {
+template <int S>
+const OpSet* by_order(int P) {
+  switch (P) {
+    case 1: return opset_impl<S, 1>();
+    case 2: return opset_impl<S, 2>();
+    case 3: return opset_impl<S, 3>();
+    case 4: return opset_impl<S, 4>();
+    case 5: return opset_impl<S, 5>();
+    case 6: return opset_impl<S, 6>();
+    case 7: return opset_impl<S, 7>();
+    case 8: return opset_impl<S, 8>();
+    case 9: return opset_impl<S, 9>();
+    case 10: return opset_impl<S, 10>();
+  }
+  return nullptr;
+}
+}  // namespace
+
+const OpSet* opset(int s, int P) {
+  switch (s) {
+    case HEX: return by_order<0>(P);
+    case PRISM: return by_order<1>(P);
+    case PYR: return by_order<2>(P);
+    case TET: return by_order<3>(P);
+  }
+  return nullptr;
+}
+
+}  // namespace sk
+
+struct sk_basis {
+  int shape_ref = 0;  // reference enum index
+  sk::HostBasis hb;
+  const sk::OpSet* ops = nullptr;
+  std::vector<unsigned char> fwd_vals, fwd_ders, dtab;
+  std::vector<double> gtab_host;
+  // device copies of gtab, one per device, created on first use
+  std::mutex mu;
+  std::vector<double*> gtab_dev;
+};
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<long long> g_launches{0};
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+int cuda_status(int e, const char* what) {
+  if (e == 0) return SK_OK;
+  return fail(SK_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(static_cast<cudaError_t>(e)));
+}
+
+const double* device_gtab(sk_basis* b, int* status) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) {
+    *status = cuda_status(e, "cudaGetDevice");
+    return nullptr;
+  }
+  std::lock_guard<std::mutex> lk(b->mu);
+  if ((int)b->gtab_dev.size() <= dev) b->gtab_dev.resize(dev + 1, nullptr);
+  if (!b->gtab_dev[dev]) {
+    double* p = nullptr;
+    e = cudaMalloc(&p, sizeof(double) * b->gtab_host.size());
+    if (e == cudaSuccess)
+      e = cudaMemcpy(p, b->gtab_host.data(), sizeof(double) * b->gtab_host.size(), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      *status = cuda_status(e, "device table upload");
+      return nullptr;
+    }
+    b->gtab_dev[dev] = p;
+  }
+  *status = SK_OK;
+  return b->gtab_dev[dev];
+}
+
+int check_layout(long long E, int W, int ncomp) {
+  if (E < 0) return fail(SK_ERR_ARG, "element count must be nonnegative");
+  if (W < 1) return fail(SK_ERR_ARG, "interleave width must be at least 1");
+  if (ncomp < 1) return fail(SK_ERR_ARG, "need at least one component");
+  return SK_OK;
+}
+
+long long padded(long long E, int W) { return ((E + W - 1) / W) * (long long)W; }
+
+int run(sk_basis* b, int op, int geo, long long E, int W, int ncomp, const double* in, double* out,
+        const double* pay, double lam, long long in_n, long long out_n, void* stream) {
+  int st = SK_OK;
+  const double* g = device_gtab(b, &st);
+  if (st) return st;
+  sk::LaunchReq r;
+  r.fwd = b->fwd_vals.data();
+  r.dtab = b->dtab.data();
+  r.in = in;
+  r.out = out;
+  r.pay = pay;
+  r.gtab = g;
+  r.E = E;
+  r.Epad = padded(E, W);
+  r.in_cs = r.Epad * in_n;
+  r.out_cs = r.Epad * out_n;
+  r.W = W;
+  r.ncomp = ncomp;
+  r.geo = geo;
+  r.lam = lam;
+  if (r.Epad == 0) return SK_OK;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cuda_status(b->ops->launch(op, r, stream), "kernel launch");
+}
+
+}  // namespace
+
+extern "C" {
+
+int sk_basis_create(int shape, int order, sk_basis** out) {
+  if (!out) return fail(SK_ERR_ARG, "null output handle");
+  *out = nullptr;
+  if (shape < SK_SHAPE_QUAD || shape > SK_SHAPE_TET) return fail(SK_ERR_STATE, "unknown shape id");
+  if (shape < SK_SHAPE_HEX) return fail(SK_ERR_UNSUPPORTED, "2D shapes are not on the device path");
+  if (order < 1) return fail(SK_ERR_ARG, "polynomial order must be at least 1");
+  const int s = shape - SK_SHAPE_HEX;
+  const sk::OpSet* ops = sk::opset(s, order);
+  if (!ops) return fail(SK_ERR_UNSUPPORTED, "order outside the compiled range 1..10");
+  std::unique_ptr<sk_basis> b(new sk_basis());
+  b->shape_ref = shape;
+  try {
+    if (!sk::build_host_basis(s, order, b->hb)) return fail(SK_ERR_UNSUPPORTED, "unsupported (shape, order)");
+  } catch (const std::exception& ex) {
+    return fail(SK_ERR_ARG, ex.what());
+  }
+  b->ops = ops;
+  b->fwd_vals.resize(ops->fwd_bytes);
+  b->fwd_ders.resize(ops->fwd_bytes);
+  b->dtab.resize(ops->dtab_bytes);
+  ops->fill(b->hb, b->fwd_vals.data(), b->fwd_ders.data(), b->dtab.data());
+  b->gtab_host.resize(ops->gtab_doubles);
+  ops->fill_gtab(b->hb, b->gtab_host.data());
+  *out = b.release();
+  return SK_OK;
+}
+
+int sk_basis_destroy(sk_basis* b) {
+  if (!b) return SK_OK;
+  for (double* p : b->gtab_dev)
+    if (p) cudaFree(p);
+  delete b;
+  return SK_OK;
+}
+
+int sk_basis_counts(const sk_basis* b, int64_t out[6]) {
+  if (!b || !out) return fail(SK_ERR_ARG, "null argument");
+  out[0] = b->hb.Q[0];
+  out[1] = b->hb.Q[1];
+  out[2] = b->hb.Q[2];
+  out[3] = b->hb.nq;
+  out[4] = b->hb.nm;
+  out[5] = b->hb.P;
+  return SK_OK;
+}
+
+int sk_basis_table(const sk_basis* b, const char* name, double* out, int64_t cap, int64_t* len) {
+  if (!b || !name || !len) return fail(SK_ERR_ARG, "null argument");
+  auto it = b->hb.named.find(name);
+  if (it == b->hb.named.end()) {
+    *len = 0;
+    return SK_OK;
+  }
+  *len = (int64_t)it->second.size();
+  if (out) std::memcpy(out, it->second.data(), sizeof(double) * std::min<int64_t>(cap, *len));
+  return SK_OK;
+}
+
+int sk_payload_size(const sk_basis* b, int geo_class, int kind, int64_t E, int64_t* n) {
+  if (!b || !n) return fail(SK_ERR_ARG, "null argument");
+  if (geo_class != SK_GEO_REGULAR && geo_class != SK_GEO_DEFORMED) return fail(SK_ERR_ARG, "bad geometry class");
+  if (kind < 0 || kind > 2) return fail(SK_ERR_ARG, "bad payload kind");
+  if (E < 0) return fail(SK_ERR_ARG, "element count must be nonnegative");
+  *n = b->ops->payload_doubles(kind, geo_class) * E;
+  return SK_OK;
+}
+
+int sk_payload_pack(const sk_basis* b, int geo_class, int kind, int64_t E, const double* dxi, const double* jac,
+                    double* pay, void* stream) {
+  if (!b || (E > 0 && (!dxi || !jac || !pay))) return fail(SK_ERR_ARG, "null argument");
+  if (geo_class != SK_GEO_REGULAR && geo_class != SK_GEO_DEFORMED) return fail(SK_ERR_ARG, "bad geometry class");
+  if (kind < 0 || kind > 2 || E < 0) return fail(SK_ERR_ARG, "bad payload kind or element count");
+  int st = SK_OK;
+  const double* g = device_gtab(const_cast<sk_basis*>(b), &st);
+  if (st) return st;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cuda_status(b->ops->pack(kind, geo_class, E, dxi, jac, pay, g, stream), "payload pack");
+}
+
+static int geometry_common(const sk_basis* b, int mode, int64_t E, const double* src, double* dxi, double* jac,
+                           int kind, double* pay, int64_t* n_bad, void* stream) {
+  if (!b || (E > 0 && !src)) return fail(SK_ERR_ARG, "null argument");
+  if (E < 0) return fail(SK_ERR_ARG, "element count must be nonnegative");
+  int st = SK_OK;
+  const double* g = device_gtab(const_cast<sk_basis*>(b), &st);
+  if (st) return st;
+  unsigned long long* d_bad = nullptr;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaMallocAsync(&d_bad, sizeof(unsigned long long), s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(d_bad, 0, sizeof(unsigned long long), s);
+  if (e != cudaSuccess) return cuda_status(e, "geometry scratch");
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  int r = b->ops->geometry(mode, E, src, dxi, jac, kind, pay, d_bad, g, stream);
+  if (r) {
+    cudaFreeAsync(d_bad, s);
+    return cuda_status(r, "geometry kernel");
+  }
+  unsigned long long h_bad = 0;
+  e = cudaMemcpyAsync(&h_bad, d_bad, sizeof(h_bad), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  cudaFreeAsync(d_bad, s);
+  if (e != cudaSuccess) return cuda_status(e, "geometry readback");
+  if (n_bad) *n_bad = (int64_t)h_bad;
+  return SK_OK;
+}
+
+int sk_geometry_deformed(const sk_basis* b, int64_t E, const double* params, double* dxi, double* jac,
+                         int64_t* n_bad, void* stream) {
+  return geometry_common(b, 1, E, params, dxi, jac, -1, nullptr, n_bad, stream);
+}
+
+int sk_geometry_from_coords(const sk_basis* b, int64_t E, const double* coords, double* dxi, double* jac,
+                            int64_t* n_bad, void* stream) {
+  return geometry_common(b, 0, E, coords, dxi, jac, -1, nullptr, n_bad, stream);
+}
+
+int sk_payload_from_params(const sk_basis* b, int kind, int64_t E, const double* params, double* pay,
+                           int64_t* n_bad, void* stream) {
+  if (kind < 0 || kind > 2) return fail(SK_ERR_ARG, "bad payload kind");
+  if (E > 0 && !pay) return fail(SK_ERR_ARG, "null payload");
+  return geometry_common(b, 1, E, params, nullptr, nullptr, kind, pay, n_bad, stream);
+}
+
+int sk_bwd_trans(const sk_basis* b, int64_t E, int W, int ncomp, const double* uhat, double* u, void* stream) {
+  if (!b || (E > 0 && (!uhat || !u))) return fail(SK_ERR_ARG, "null argument");
+  if (int st = check_layout(E, W, ncomp)) return st;
+  return run(const_cast<sk_basis*>(b), sk::OP_BWD, 0, E, W, ncomp, uhat, u, nullptr, 0.0, b->hb.nm, b->hb.nq,
+             stream);
+}
+
+int sk_iproduct_wrt_base(const sk_basis* b, int geo, int64_t E, int W, int ncomp, const double* u,
+                         const double* wpay, double* fhat, void* stream) {
+  if (!b || (E > 0 && (!u || !wpay || !fhat))) return fail(SK_ERR_ARG, "null argument");
+  if (geo != SK_GEO_REGULAR && geo != SK_GEO_DEFORMED) return fail(SK_ERR_ARG, "bad geometry class");
+  if (int st = check_layout(E, W, ncomp)) return st;
+  return run(const_cast<sk_basis*>(b), sk::OP_IPROD, geo, E, W, ncomp, u, fhat, wpay, 0.0, b->hb.nq, b->hb.nm,
+             stream);
+}
+
+int sk_phys_deriv(const sk_basis* b, int geo, int64_t E, int W, const double* u, const double* dpay, double* du,
+                  void* stream) {
+  if (!b || (E > 0 && (!u || !dpay || !du))) return fail(SK_ERR_ARG, "null argument");
+  if (geo != SK_GEO_REGULAR && geo != SK_GEO_DEFORMED) return fail(SK_ERR_ARG, "bad geometry class");
+  if (int st = check_layout(E, W, 1)) return st;
+  return run(const_cast<sk_basis*>(b), sk::OP_PDERIV, geo, E, W, 1, u, du, dpay, 0.0, b->hb.nq, b->hb.nq, stream);
+}
+
+int sk_iproduct_wrt_deriv_base(const sk_basis* b, int geo, int64_t E, int W, const double* v, const double* wpay,
+                               double* fhat, void* stream) {
+  if (!b || (E > 0 && (!v || !wpay || !fhat))) return fail(SK_ERR_ARG, "null argument");
+  if (geo != SK_GEO_REGULAR && geo != SK_GEO_DEFORMED) return fail(SK_ERR_ARG, "bad geometry class");
+  if (int st = check_layout(E, W, 1)) return st;
+  return run(const_cast<sk_basis*>(b), sk::OP_IPDERIV, geo, E, W, 1, v, fhat, wpay, 0.0, b->hb.nq, b->hb.nm,
+             stream);
+}
+
+int sk_mass_apply(const sk_basis* b, int geo, int64_t E, int W, int ncomp, const double* uhat, const double* wpay,
+                  double* out, void* stream) {
+  if (!b || (E > 0 && (!uhat || !wpay || !out))) return fail(SK_ERR_ARG, "null argument");
+  if (geo != SK_GEO_REGULAR && geo != SK_GEO_DEFORMED) return fail(SK_ERR_ARG, "bad geometry class");
+  if (int st = check_layout(E, W, ncomp)) return st;
+  return run(const_cast<sk_basis*>(b), sk::OP_MASS, geo, E, W, ncomp, uhat, out, wpay, 0.0, b->hb.nm, b->hb.nm,
+             stream);
+}
+
+int sk_helmholtz_apply(const sk_basis* b, int geo, int form, int64_t E, int W, int ncomp, const double* uhat,
+                       const double* hpay, double lam, double* out, void* stream) {
+  if (!b || (E > 0 && (!uhat || !hpay || !out))) return fail(SK_ERR_ARG, "null argument");
+  if (geo != SK_GEO_REGULAR && geo != SK_GEO_DEFORMED) return fail(SK_ERR_ARG, "bad geometry class");
+  if (!(lam >= 0.0)) return fail(SK_ERR_ARG, "reaction coefficient must be nonnegative");
+  if (form != SK_FORM_COLL && form != SK_FORM_NONCOLL) return fail(SK_ERR_ARG, "unknown Helmholtz form");
+  if (form == SK_FORM_NONCOLL) return fail(SK_ERR_UNSUPPORTED, "non-collocated form not built yet");
+  if (int st = check_layout(E, W, ncomp)) return st;
+  return run(const_cast<sk_basis*>(b), sk::OP_HELM, geo, E, W, ncomp, uhat, out, hpay, lam, b->hb.nm, b->hb.nm,
+             stream);
+}
+
+int64_t sk_launch_count(void) { return g_launches.load(); }
+
+const char* sk_last_error(void) { return g_err.c_str(); }
+
+int sk_launch_config(const sk_basis* b, int op, int64_t out[3]) {
+  if (!b || !out || op < 0 || op >= sk::OP_COUNT) return fail(SK_ERR_ARG, "bad argument");
+  b->ops->config(op, out);
+  return SK_OK;
+}
+
+}  // extern "C"

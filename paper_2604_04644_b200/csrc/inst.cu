@@ -1,0 +1,487 @@
+// One translation unit per (shape, order): compiled with -DSK_S=<0..3>
+// -DSK_P=<1..10>.  Instantiates every operator kernel for that pair, the
+// table fills, the geometry payload packers and the device geometry builder,
+// and exports them through sk::opset_impl<S,P>().
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <mutex>
+
+#include "sk_ops.cuh"
+#include "sk_opset.hpp"
+
+#ifndef SK_S
+#error "compile with -DSK_S=<shape> -DSK_P=<order>"
+#endif
+
+namespace sk {
+
+// ---------------------------------------------------------------------------
+// launch configuration: EB elements per CTA so that EB x (largest stage item
+// count) fills ~256 threads, capped by shared memory
+template <int S, int P, int OP>
+struct Cfg {
+  using Dm = Dims<S, P>;
+  static constexpr int planes = (OP == OP_HELM || OP == OP_PDERIV || OP == OP_IPDERIV) ? 3 : 2;
+  static constexpr int ES = planes * Dm::PLANE;
+  static constexpr int items =
+      cmax(cmax(cmax(Dm::Q1 * Dm::Q2, Dm::Q0 * Dm::Q2), cmax(Dm::Q0 * Dm::Q1, Dm::P1 * Dm::P1)), Dm::NPAIR);
+  static constexpr int eb_thr = cmax(1, (256 + items / 2) / items);
+  static constexpr int eb_smem = cmax(1, (96 * 1024) / (ES * 8));
+  static constexpr int EB = eb_thr < eb_smem ? eb_thr : eb_smem;
+  static constexpr int NT0 = ((EB * items + 31) / 32) * 32;
+  static constexpr int NT = NT0 > 1024 ? 1024 : NT0;
+  static constexpr int SMEM = EB * ES * 8;
+};
+
+// ---------------------------------------------------------------------------
+// host table fills
+template <int S, int P>
+void fill_fwd(const HostBasis& hb, FwdTab<S, P>& t, bool deriv) {
+  using Dm = Dims<S, P>;
+  std::memset(&t, 0, sizeof(t));
+  const std::vector<double>* a = deriv ? hb.da : hb.a;
+  std::memcpy(t.a0, a[0].data(), sizeof(double) * Dm::Q0 * Dm::P1);
+  if constexpr (S != TET) std::memcpy(t.a1, a[1].data(), sizeof(double) * Dm::Q1 * Dm::P1);
+  if constexpr (S == HEX) std::memcpy(t.a2, a[2].data(), sizeof(double) * Dm::Q2 * Dm::P1);
+  if constexpr (S == TET) {
+    const auto& fam = deriv ? hb.db1 : hb.b1;
+    for (int p = 0; p < Dm::P1; ++p)
+      std::memcpy(t.b1 + wfam_off(Dm::Q1, Dm::P1, p), fam[p].data(), sizeof(double) * fam[p].size());
+  }
+  if constexpr (S == PRISM) {
+    const auto& fam = deriv ? hb.dc2 : hb.c2;
+    for (int p = 0; p < Dm::P1; ++p)
+      std::memcpy(t.c2 + wfam_off(Dm::Q2, Dm::P1, p), fam[p].data(), sizeof(double) * fam[p].size());
+  }
+}
+
+template <int S, int P>
+void fill(const HostBasis& hb, void* fv, void* fd, void* dt) {
+  using Dm = Dims<S, P>;
+  fill_fwd<S, P>(hb, *static_cast<FwdTab<S, P>*>(fv), false);
+  fill_fwd<S, P>(hb, *static_cast<FwdTab<S, P>*>(fd), true);
+  auto& d = *static_cast<DTab<S, P>*>(dt);
+  std::memcpy(d.d0, hb.D[0].data(), sizeof(double) * Dm::Q0 * Dm::Q0);
+  std::memcpy(d.d1, hb.D[1].data(), sizeof(double) * Dm::Q1 * Dm::Q1);
+  std::memcpy(d.d2, hb.D[2].data(), sizeof(double) * Dm::Q2 * Dm::Q2);
+}
+
+// extra runtime-indexed tables (after GLayout<S,P>::SIZE)
+template <int S, int P>
+struct GExt {
+  using Dm = Dims<S, P>;
+  using L = GLayout<S, P>;
+  static constexpr int DM0 = L::SIZE;
+  static constexpr int DM1 = DM0 + Dm::Q0 * Dm::Q0;
+  static constexpr int DM2 = DM1 + Dm::Q1 * Dm::Q1;
+  static constexpr int Z0 = DM2 + Dm::Q2 * Dm::Q2;
+  static constexpr int Z1 = Z0 + Dm::Q0;
+  static constexpr int Z2 = Z1 + Dm::Q1;
+  static constexpr int GST = Z2 + Dm::Q2;  // [l][3][3] dense G, standard point order
+  static constexpr int SIZE = GST + 9 * Dm::NQ;
+};
+
+template <int S, int P>
+void fill_gtab(const HostBasis& hb, double* g) {
+  using Dm = Dims<S, P>;
+  using L = GLayout<S, P>;
+  using X = GExt<S, P>;
+  std::memset(g, 0, sizeof(double) * X::SIZE);
+  if constexpr (S != HEX) {
+    for (int m = 0; m < Dm::P1; ++m) {
+      std::memcpy(g + L::C2 + wfam_off(Dm::Q2, Dm::P1, m), hb.c2[m].data(), sizeof(double) * hb.c2[m].size());
+      std::memcpy(g + L::DC2 + wfam_off(Dm::Q2, Dm::P1, m), hb.dc2[m].data(), sizeof(double) * hb.dc2[m].size());
+    }
+  }
+  // (p, q) pairs of the ragged stages with their mode offset and run length
+  int* pr = reinterpret_cast<int*>(g + L::PAIRS);
+  int np = 0, off = 0;
+  for (int p = 0; p < Dm::P1; ++p) {
+    const int nq = (S == TET) ? Dm::P1 - p : Dm::P1;
+    for (int q = 0; q < nq; ++q) {
+      int nr = Dm::P1;
+      if (S == PRISM) nr = Dm::P1 - p;
+      if (S == PYR) nr = Dm::P1 - cmax(p, q);
+      if (S == TET) nr = Dm::P1 - p - q;
+      if (np < Dm::NPAIR && (S == PYR || S == TET)) {
+        pr[4 * np + 0] = p;
+        pr[4 * np + 1] = q;
+        pr[4 * np + 2] = off;
+        pr[4 * np + 3] = nr;
+        ++np;
+      }
+      off += nr;
+    }
+  }
+  for (int i = 0; i < Dm::Q0; ++i)
+    for (int j = 0; j < Dm::Q1; ++j)
+      for (int k = 0; k < Dm::Q2; ++k) {
+        const int l = (i * Dm::Q1 + j) * Dm::Q2 + k;
+        const int km = k * Dm::Q0 * Dm::Q1 + i * Dm::Q1 + j;
+        const double* G = &hb.G[9 * l];
+        g[L::REGK + 0 * Dm::NQ + km] = hb.refw[l];
+        g[L::REGK + 1 * Dm::NQ + km] = G[0];  // G00
+        g[L::REGK + 2 * Dm::NQ + km] = G[3];  // G10
+        g[L::REGK + 3 * Dm::NQ + km] = G[4];  // G11
+        g[L::REGK + 4 * Dm::NQ + km] = G[6];  // G20
+        g[L::REGK + 5 * Dm::NQ + km] = G[7];  // G21
+        g[L::REFW + l] = hb.refw[l];
+        for (int a = 0; a < 9; ++a) g[X::GST + 9 * l + a] = G[a];
+      }
+  std::memcpy(g + X::DM0, hb.D[0].data(), sizeof(double) * Dm::Q0 * Dm::Q0);
+  std::memcpy(g + X::DM1, hb.D[1].data(), sizeof(double) * Dm::Q1 * Dm::Q1);
+  std::memcpy(g + X::DM2, hb.D[2].data(), sizeof(double) * Dm::Q2 * Dm::Q2);
+  std::memcpy(g + X::Z0, hb.z[0].data(), sizeof(double) * Dm::Q0);
+  std::memcpy(g + X::Z1, hb.z[1].data(), sizeof(double) * Dm::Q1);
+  std::memcpy(g + X::Z2, hb.z[2].data(), sizeof(double) * Dm::Q2);
+}
+
+// ---------------------------------------------------------------------------
+// launches
+template <class K>
+static void ensure_smem(K kernel, int bytes) {
+  if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
+template <int S, int P, int OP, auto Kern>
+static int go(const OpArgs<S, P>& a, const LaunchReq& r, int gy, void* stream) {
+  using C = Cfg<S, P, OP>;
+  static std::once_flag once;  // one flag per kernel instantiation
+  std::call_once(once, [] { ensure_smem(Kern, C::SMEM); });
+  const long long tiles = (r.Epad + C::EB - 1) / C::EB;
+  if (tiles == 0) return 0;
+  dim3 grid((unsigned)tiles, (unsigned)gy);
+  Kern<<<grid, C::NT, C::SMEM, static_cast<cudaStream_t>(stream)>>>(a);
+  return (int)cudaGetLastError();
+}
+
+template <int S, int P>
+int launch(int op, const LaunchReq& r, void* stream) {
+  OpArgs<S, P> a;
+  std::memcpy(&a.B, r.fwd, sizeof(a.B));
+  std::memcpy(&a.D, r.dtab, sizeof(a.D));
+  a.in = r.in;
+  a.out = r.out;
+  a.pay = r.pay;
+  a.gtab = r.gtab;
+  a.E = r.E;
+  a.Epad = r.Epad;
+  a.in_cstride = r.in_cs;
+  a.out_cstride = r.out_cs;
+  a.W = r.W;
+  a.pad_ = 0;
+  a.lam = r.lam;
+  const bool def = r.geo == GEO_DEFORMED;
+  using namespace std;
+  switch (op) {
+    case OP_HELM: {
+      using C = Cfg<S, P, OP_HELM>;
+      if (def) {
+        if (r.lam != 0.0) return go<S, P, OP_HELM, k_helm<S, P, C::EB, C::NT, GEO_DEFORMED, true>>(a, r, r.ncomp, stream);
+        return go<S, P, OP_HELM, k_helm<S, P, C::EB, C::NT, GEO_DEFORMED, false>>(a, r, r.ncomp, stream);
+      }
+      if (r.lam != 0.0) return go<S, P, OP_HELM, k_helm<S, P, C::EB, C::NT, GEO_REGULAR, true>>(a, r, r.ncomp, stream);
+      return go<S, P, OP_HELM, k_helm<S, P, C::EB, C::NT, GEO_REGULAR, false>>(a, r, r.ncomp, stream);
+    }
+    case OP_MASS: {
+      using C = Cfg<S, P, OP_MASS>;
+      if (def) return go<S, P, OP_MASS, k_mass<S, P, C::EB, C::NT, GEO_DEFORMED>>(a, r, r.ncomp, stream);
+      return go<S, P, OP_MASS, k_mass<S, P, C::EB, C::NT, GEO_REGULAR>>(a, r, r.ncomp, stream);
+    }
+    case OP_BWD: {
+      using C = Cfg<S, P, OP_BWD>;
+      return go<S, P, OP_BWD, k_bwd<S, P, C::EB, C::NT>>(a, r, r.ncomp, stream);
+    }
+    case OP_IPROD: {
+      using C = Cfg<S, P, OP_IPROD>;
+      if (def) return go<S, P, OP_IPROD, k_iprod<S, P, C::EB, C::NT, GEO_DEFORMED>>(a, r, r.ncomp, stream);
+      return go<S, P, OP_IPROD, k_iprod<S, P, C::EB, C::NT, GEO_REGULAR>>(a, r, r.ncomp, stream);
+    }
+    case OP_PDERIV: {
+      using C = Cfg<S, P, OP_PDERIV>;
+      if (def) return go<S, P, OP_PDERIV, k_pderiv<S, P, C::EB, C::NT, GEO_DEFORMED>>(a, r, 1, stream);
+      return go<S, P, OP_PDERIV, k_pderiv<S, P, C::EB, C::NT, GEO_REGULAR>>(a, r, 1, stream);
+    }
+    case OP_IPDERIV: {
+      using C = Cfg<S, P, OP_IPDERIV>;
+      if (def) return go<S, P, OP_IPDERIV, k_ipderiv<S, P, C::EB, C::NT, GEO_DEFORMED>>(a, r, 1, stream);
+      return go<S, P, OP_IPDERIV, k_ipderiv<S, P, C::EB, C::NT, GEO_REGULAR>>(a, r, 1, stream);
+    }
+  }
+  return (int)cudaErrorInvalidValue;
+}
+
+template <int S, int P>
+void config(int op, int64_t out[3]) {
+  switch (op) {
+#define SK_CFG(OPV)                    \
+  case OPV:                            \
+    out[0] = Cfg<S, P, OPV>::EB;       \
+    out[1] = Cfg<S, P, OPV>::NT;       \
+    out[2] = Cfg<S, P, OPV>::SMEM;     \
+    return;
+    SK_CFG(OP_HELM)
+    SK_CFG(OP_MASS)
+    SK_CFG(OP_BWD)
+    SK_CFG(OP_IPROD)
+    SK_CFG(OP_PDERIV)
+    SK_CFG(OP_IPDERIV)
+#undef SK_CFG
+  }
+  out[0] = out[1] = out[2] = 0;
+}
+
+// ---------------------------------------------------------------------------
+// geometry payloads
+template <int S, int P>
+long long payload_doubles(int kind, int geo) {
+  constexpr long long NQ = Dims<S, P>::NQ;
+  if (geo == GEO_DEFORMED) return kind == 0 ? 7 * NQ : kind == 1 ? NQ : 9 * NQ;
+  return kind == 0 ? 8 : kind == 1 ? 1 : 9;
+}
+
+// write the payload entries of one deformed point from (dxi, w|J|)
+template <int S, int P>
+__device__ __forceinline__ void put_point(int kind, long long e, int l, const double (&dxi)[3][3], double wjac,
+                                          double* __restrict__ pay, const double* __restrict__ gtab) {
+  using Dm = Dims<S, P>;
+  constexpr int NQ = Dm::NQ;
+  const int k = l % Dm::Q2, ij = l / Dm::Q2;
+  const int km = k * Dm::Q0 * Dm::Q1 + ij;
+  if (kind == 1) {
+    pay[e * NQ + l] = wjac;
+    return;
+  }
+  double G[3][3];
+  const double* gs = gtab + GExt<S, P>::GST + 9 * l;
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b) G[a][b] = gs[3 * a + b];
+  if (kind == 0) {
+    // Lam_ab = (sum_k dxi[a][k] dxi[b][k]) * w|J|  (field_block.py:349-362)
+    double L[3][3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = a; b < 3; ++b) {
+        const double s = fma(dxi[a][2], dxi[b][2], fma(dxi[a][1], dxi[b][1], dxi[a][0] * dxi[b][0]));
+        L[a][b] = L[b][a] = s * wjac;
+      }
+    // Lam' = G^T Lam G: the chain rule of operators.py:471-490, 510-523 folded
+    double T[3][3];  // T = Lam G
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int n = 0; n < 3; ++n) T[a][n] = L[a][0] * G[0][n] + L[a][1] * G[1][n] + L[a][2] * G[2][n];
+    const int mi[6] = {0, 0, 0, 1, 1, 2}, ni[6] = {0, 1, 2, 1, 2, 2};
+    double* o = pay + e * (7LL * NQ) + km;
+#pragma unroll
+    for (int c = 0; c < 6; ++c) {
+      const int m = mi[c], n = ni[c];
+      o[c * NQ] = G[0][m] * T[0][n] + G[1][m] * T[1][n] + G[2][m] * T[2][n];
+    }
+    o[6 * NQ] = wjac;
+    return;
+  }
+  // DERIV: T[m][j] = sum_a G[a][m] dxi[a][j]
+  double* o = pay + e * (9LL * NQ) + km;
+#pragma unroll
+  for (int m = 0; m < 3; ++m)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) o[(m * 3 + j) * NQ] = G[0][m] * dxi[0][j] + G[1][m] * dxi[1][j] + G[2][m] * dxi[2][j];
+}
+
+template <int S, int P>
+__global__ void k_pack_deformed(int kind, long long E, const double* __restrict__ dxi, const double* __restrict__ jac,
+                                double* __restrict__ pay, const double* __restrict__ gtab) {
+  constexpr int NQ = Dims<S, P>::NQ;
+  const long long n = E * NQ;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
+    const long long e = t / NQ;
+    const int l = (int)(t - e * NQ);
+    double d[3][3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) d[a][b] = dxi[t * 9 + a * 3 + b];
+    put_point<S, P>(kind, e, l, d, jac[t], pay, gtab);
+  }
+}
+
+template <int S, int P>
+__global__ void k_pack_regular(int kind, long long E, const double* __restrict__ dxi, const double* __restrict__ jac,
+                               double* __restrict__ pay) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < E; e += (long long)gridDim.x * blockDim.x) {
+    const double* d = dxi + e * 9;
+    if (kind == 0) {
+      double* o = pay + e * 8;
+      const int mi[6] = {0, 0, 0, 1, 1, 2}, ni[6] = {0, 1, 2, 1, 2, 2};
+      for (int c = 0; c < 6; ++c) {
+        const int a = mi[c], b = ni[c];
+        const double s = fma(d[a * 3 + 2], d[b * 3 + 2], fma(d[a * 3 + 1], d[b * 3 + 1], d[a * 3] * d[b * 3]));
+        o[c] = s * jac[e];
+      }
+      o[6] = jac[e];
+      o[7] = 0.0;
+    } else if (kind == 1) {
+      pay[e] = jac[e];
+    } else {
+      for (int a = 0; a < 9; ++a) pay[e * 9 + a] = d[a];
+    }
+  }
+}
+
+static unsigned grid_for(long long n, int bs) {
+  long long g = (n + bs - 1) / bs;
+  if (g > 148LL * 64) g = 148LL * 64;
+  return (unsigned)(g < 1 ? 1 : g);
+}
+
+template <int S, int P>
+int pack(int kind, int geo, long long E, const double* dxi, const double* jac, double* pay, const double* gtab,
+         void* stream) {
+  if (E == 0) return 0;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (geo == GEO_DEFORMED)
+    k_pack_deformed<S, P><<<grid_for(E * Dims<S, P>::NQ, 256), 256, 0, s>>>(kind, E, dxi, jac, pay, gtab);
+  else
+    k_pack_regular<S, P><<<grid_for(E, 256), 256, 0, s>>>(kind, E, dxi, jac, pay);
+  return (int)cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// device geometry builder: iso-parametric metric of deformed elements
+// (geometry.py:161-212) from coordinates or from the seeded sinusoidal
+// deformation parameters (geometry.py:275-300)
+template <int S, int P, int MODE>
+__global__ void __launch_bounds__(128) k_geom(long long E, const double* __restrict__ src, double* __restrict__ dxi_out,
+                                              double* __restrict__ jac_out, int kind, double* __restrict__ pay,
+                                              unsigned long long* bad, const double* __restrict__ gtab) {
+  using Dm = Dims<S, P>;
+  using X = GExt<S, P>;
+  constexpr int NQ = Dm::NQ, Q0 = Dm::Q0, Q1 = Dm::Q1, Q2 = Dm::Q2;
+  __shared__ double x[3][NQ];
+  for (long long e = blockIdx.x; e < E; e += gridDim.x) {
+    __syncthreads();
+    for (int l = threadIdx.x; l < NQ; l += blockDim.x) {
+      if (MODE == 0) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) x[c][l] = src[(e * NQ + l) * 3 + c];
+      } else {
+        const int k = l % Q2, j = (l / Q2) % Q1, i = l / (Q1 * Q2);
+        const double e1 = gtab[X::Z0 + i], e2 = gtab[X::Z1 + j], e3 = gtab[X::Z2 + k];
+        // Duffy inverse (shapes.py:218-239)
+        double xi[3] = {e1, e2, e3};
+        if (S == PRISM) xi[0] = 0.5 * (1.0 + e1) * (1.0 - e3) - 1.0;
+        if (S == PYR) {
+          xi[0] = 0.5 * (1.0 + e1) * (1.0 - e3) - 1.0;
+          xi[1] = 0.5 * (1.0 + e2) * (1.0 - e3) - 1.0;
+        }
+        if (S == TET) {
+          xi[1] = 0.5 * (1.0 + e2) * (1.0 - e3) - 1.0;
+          xi[0] = 0.25 * (1.0 + e1) * (1.0 - e2) * (1.0 - e3) - 1.0;
+        }
+        const double* pr = src + e * 12;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const int perm = (int)pr[6 + c];
+          x[c][l] = (xi[c] + pr[9 + c]) + pr[c] * sin(M_PI * xi[perm] + pr[3 + c]);
+        }
+      }
+    }
+    __syncthreads();
+    for (int l = threadIdx.x; l < NQ; l += blockDim.x) {
+      const int k = l % Q2, j = (l / Q2) % Q1, i = l / (Q1 * Q2);
+      double dx[3][3];  // dx[c][m] = d x_c / d eta_m
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+        for (int a = 0; a < Q0; ++a) s0 = fma(gtab[X::DM0 + i * Q0 + a], x[c][(a * Q1 + j) * Q2 + k], s0);
+        for (int b = 0; b < Q1; ++b) s1 = fma(gtab[X::DM1 + j * Q1 + b], x[c][(i * Q1 + b) * Q2 + k], s1);
+        for (int d = 0; d < Q2; ++d) s2 = fma(gtab[X::DM2 + k * Q2 + d], x[c][(i * Q1 + j) * Q2 + d], s2);
+        dx[c][0] = s0;
+        dx[c][1] = s1;
+        dx[c][2] = s2;
+      }
+      // J[c][jj] = sum_m G[jj][m] dx[c][m]
+      const double* G = gtab + X::GST + 9 * l;
+      double J[3][3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int jj = 0; jj < 3; ++jj) {
+          if (S == HEX) {
+            J[c][jj] = dx[c][jj];
+          } else {
+            double s = 0.0;
+#pragma unroll
+            for (int m = 0; m < 3; ++m)
+              if (G[jj * 3 + m] != 0.0) s += (G[jj * 3 + m] == 1.0) ? dx[c][m] : dx[c][m] * G[jj * 3 + m];
+            J[c][jj] = s;
+          }
+        }
+      const double c00 = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+      const double c01 = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+      const double c02 = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+      const double det = J[0][0] * c00 + J[0][1] * c01 + J[0][2] * c02;
+      if (!(det > 0.0)) atomicAdd(bad, 1ULL);
+      const double id = 1.0 / det;
+      double inv[3][3];
+      inv[0][0] = c00 * id;
+      inv[1][0] = c01 * id;
+      inv[2][0] = c02 * id;
+      inv[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) * id;
+      inv[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) * id;
+      inv[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) * id;
+      inv[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) * id;
+      inv[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) * id;
+      inv[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) * id;
+      const double wjac = gtab[GLayout<S, P>::REFW + l] * det;
+      if (dxi_out) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+          for (int b = 0; b < 3; ++b) dxi_out[(e * NQ + l) * 9 + a * 3 + b] = inv[a][b];
+      }
+      if (jac_out) jac_out[e * NQ + l] = wjac;
+      if (kind >= 0) put_point<S, P>(kind, e, l, inv, wjac, pay, gtab);
+    }
+  }
+}
+
+template <int S, int P>
+int geometry(int mode, long long E, const double* src, double* dxi, double* jac, int kind, double* pay,
+             unsigned long long* bad, const double* gtab, void* stream) {
+  if (E == 0) return 0;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  long long g = E < 148LL * 32 ? E : 148LL * 32;
+  if (mode == 0)
+    k_geom<S, P, 0><<<(unsigned)g, 128, 0, s>>>(E, src, dxi, jac, kind, pay, bad, gtab);
+  else
+    k_geom<S, P, 1><<<(unsigned)g, 128, 0, s>>>(E, src, dxi, jac, kind, pay, bad, gtab);
+  return (int)cudaGetLastError();
+}
+
+template <int S, int P>
+const OpSet* opset_impl() {
+  static const OpSet ops = {S,
+                            P,
+                            sizeof(FwdTab<S, P>),
+                            sizeof(DTab<S, P>),
+                            GExt<S, P>::SIZE,
+                            &fill<S, P>,
+                            &fill_gtab<S, P>,
+                            &launch<S, P>,
+                            &config<S, P>,
+                            &payload_doubles<S, P>,
+                            &pack<S, P>,
+                            &geometry<S, P>};
+  return &ops;
+}
+
+template const OpSet* opset_impl<SK_S, SK_P>();
+
+}  // namespace sk

@@ -1,0 +1,102 @@
+// Compile-time dimensions, kernel-parameter tables and small device helpers
+// shared by every sm_100a operator kernel.
+#pragma once
+
+#include <cstdint>
+
+#include "sk_shapes.hpp"
+
+namespace sk {
+
+enum : int { GEO_REGULAR = 0, GEO_DEFORMED = 1 };
+
+__host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
+
+__host__ __device__ constexpr int n_modes(int S, int P) {
+  return S == HEX     ? (P + 1) * (P + 1) * (P + 1)
+         : S == PRISM ? (P + 1) * (P + 1) * (P + 2) / 2
+         : S == PYR   ? (P + 1) * (P + 2) * (2 * P + 3) / 6
+                      : (P + 1) * (P + 2) * (P + 3) / 6;
+}
+
+// Per-(shape, order) sizes.  Quadrature per direction: P+2 Gauss-Lobatto,
+// P+1 Gauss-Radau-Jacobi on collapsed directions (shapes.py:76-139).
+template <int S, int P>
+struct Dims {
+  static constexpr int P1 = P + 1;
+  static constexpr int Q0 = P + 2;
+  static constexpr int Q1 = (S == TET) ? P + 1 : P + 2;
+  static constexpr int Q2 = (S == HEX) ? P + 2 : P + 1;
+  static constexpr int NQ = Q0 * Q1 * Q2;
+  static constexpr int NM = n_modes(S, P);
+  static constexpr int NTRI = P1 * (P1 + 1) / 2;
+  // smem quad-point arrays are [i][j][k] with an odd k-row stride so that
+  // a line walk along any direction is bank-conflict free for doubles
+  static constexpr int S2 = Q2 | 1;
+  static constexpr int PLANE = Q0 * Q1 * S2;
+  // ragged first/last stages (pyr, tet) iterate over (p, q) pairs
+  static constexpr int NPAIR = (S == TET) ? NTRI : P1 * P1;
+};
+
+// offset of the leading-index-p slice in a packed warped family whose slice
+// p has (P1 - p) columns and Q rows
+__host__ __device__ constexpr int wfam_off(int Q, int P1, int p) {
+  return Q * (p * P1 - p * (p - 1) / 2);
+}
+
+// Basis tables consumed with compile-time indices: they live in the kernel
+// parameter space (constant bank) and enter DFMAs as uniform operands.
+// Filled either with values (B) or with derivatives (D_k B) per direction.
+template <int S, int P>
+struct FwdTab {
+  using Dm = Dims<S, P>;
+  double a0[Dm::Q0 * Dm::P1];                                // dir 0 [i][p]
+  double a1[(S != TET) ? Dm::Q1 * Dm::P1 : 1];               // dir 1 [j][q]
+  double a2[(S == HEX) ? Dm::Q2 * Dm::P1 : 1];               // dir 2 [k][r]
+  double b1[(S == TET) ? Dm::Q1 * Dm::NTRI : 1];             // tet dir 1, per p
+  double c2[(S == PRISM) ? Dm::Q2 * Dm::NTRI : 1];           // prism dir 2, per p
+};
+
+template <int S, int P>
+struct DTab {
+  using Dm = Dims<S, P>;
+  double d0[Dm::Q0 * Dm::Q0];
+  double d1[Dm::Q1 * Dm::Q1];
+  double d2[Dm::Q2 * Dm::Q2];
+};
+
+// Layout of the per-basis device table buffer ("gtab"), runtime indexed.
+template <int S, int P>
+struct GLayout {
+  using Dm = Dims<S, P>;
+  static constexpr int C2 = 0;                               // dir-2 family values
+  static constexpr int DC2 = C2 + Dm::Q2 * Dm::NTRI;         // dir-2 family derivatives
+  static constexpr int PAIRS = DC2 + Dm::Q2 * Dm::NTRI;      // NPAIR x 4 ints (as 2 doubles)
+  static constexpr int REGK = PAIRS + 2 * Dm::NPAIR;         // [6][k][i*Q1+j]: refw,g00,g10,g11,g20,g21
+  static constexpr int REFW = REGK + 6 * Dm::NQ;             // [i][j][k] refw
+  static constexpr int SIZE = REFW + Dm::NQ;
+};
+
+struct Ctx {
+  long long e0;    // first element of this CTA's tile
+  long long E;     // real elements (loads guarded by e < E)
+  long long Epad;  // padded elements = groups * W (stores guarded by e < Epad)
+  int W;           // interleave width of the field layout
+};
+
+// index of data point 0 of element e in a lane-major (G, N, W) component
+__device__ __forceinline__ long long lane_base(long long e, int N, int W) {
+  const long long g = e / W;
+  return g * (long long)N * W + (e - g * W);
+}
+
+template <int EB, int NPASS, int NT, class F>
+__device__ __forceinline__ void items(F&& f) {
+#pragma unroll 1
+  for (int w = threadIdx.x; w < EB * NPASS; w += NT) {
+    const int e = w / NPASS;
+    f(e, w - e * NPASS);
+  }
+}
+
+}  // namespace sk

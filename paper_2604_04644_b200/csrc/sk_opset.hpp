@@ -1,0 +1,51 @@
+// Type-erased per-(shape, order) entry points, implemented by the
+// explicit instantiations in inst.cu (one object file per (shape, order)).
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+
+#include "basis_host.hpp"
+
+namespace sk {
+
+enum OpId : int { OP_HELM = 0, OP_MASS = 1, OP_BWD = 2, OP_IPROD = 3, OP_PDERIV = 4, OP_IPDERIV = 5, OP_COUNT = 6 };
+
+struct LaunchReq {
+  const void* fwd;    // FwdTab<S,P> (host copy, values)
+  const void* dtab;   // DTab<S,P>   (host copy)
+  const double* in;
+  double* out;
+  const double* pay;
+  const double* gtab;  // device table buffer
+  long long E, Epad, in_cs, out_cs;
+  int W, ncomp, geo;
+  double lam;
+};
+
+struct OpSet {
+  int S, P;
+  size_t fwd_bytes, dtab_bytes;
+  int gtab_doubles;
+  void (*fill)(const HostBasis& hb, void* fwd_vals, void* fwd_ders, void* dtab);
+  void (*fill_gtab)(const HostBasis& hb, double* gtab_host);
+  // returns a cudaError_t value (0 = success)
+  int (*launch)(int op, const LaunchReq& r, void* stream);
+  void (*config)(int op, int64_t out[3]);
+  // payload kinds: 0 HELMHOLTZ, 1 W, 2 DERIV
+  long long (*payload_doubles)(int kind, int geo);  // per element
+  int (*pack)(int kind, int geo, long long E, const double* dxi, const double* jac, double* pay,
+              const double* gtab, void* stream);
+  // geometry builder: mode 0 from coords (E,NQ,3), mode 1 from params (E,12).
+  // Writes dxi/jac (either may be null) and/or the payload of `kind`
+  // (kind < 0: none).  Counts nonpositive-Jacobian points into *bad (device).
+  int (*geometry)(int mode, long long E, const double* src, double* dxi, double* jac, int kind,
+                  double* pay, unsigned long long* bad, const double* gtab, void* stream);
+};
+
+template <int S, int P>
+const OpSet* opset_impl();
+
+const OpSet* opset(int internal_shape, int P);
+
+}  // namespace sk

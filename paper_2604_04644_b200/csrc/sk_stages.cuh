@@ -1,0 +1,389 @@
+// Sum-factorisation stages of the SUM_FAC_TOP kernels.
+//
+// A CTA owns a tile of EB elements; each stage is one 1D contraction along
+// one tensor direction, parallel over (element, passive-index) items with
+// the contracted line held in registers.  Wherever the 1D table does not
+// depend on the item (all full families, and the warped families once the
+// selector index is unrolled inside the thread) the table entry is a
+// compile-time offset into kernel-parameter space, i.e. a uniform DFMA
+// operand.  The two ragged stages of pyr/tet (selector p+q or max(p,q)
+// varies per item) read their table from the L1-resident device buffer.
+//
+// Algorithm: reference sum-factorised kernels speckern/operators.py:149-391
+// (contraction order r -> q -> p forward, p -> q -> r transposed, the
+// collapsed-vertex rank-one corrections folded into the line passes).
+//
+// Per-element shared memory (doubles): three quad-point planes
+//   plane 0: U  [i][j][k]   (stride S2 per (i,j) row)   / TA [p][q][k] + Y row
+//   plane 1: V0 [i][j][k]
+//   plane 2: V1 [i][j][k]                                / TB [p][j][k]
+// TA and TB are live only between the sweeps that produce and consume them.
+#pragma once
+
+#include "sk_common.cuh"
+
+namespace sk {
+
+// ---- F1: r -> k.  TA[p][q][k] = sum_r C_(p,q)[k][r] uhat[p,q,r] ----------
+template <int S, int P, int EB, int NT, int ES, int TAo>
+__device__ __forceinline__ void stage_f1(const FwdTab<S, P>& B, const double* __restrict__ gtab,
+                                         const double* __restrict__ src, const Ctx& c,
+                                         double* sm) {
+  using Dm = Dims<S, P>;
+  constexpr int P1 = Dm::P1, Q2 = Dm::Q2, S2 = Dm::S2, NM = Dm::NM;
+  if constexpr (S == HEX) {
+    items<EB, P1 * P1, NT>([&](int e, int ps) {
+      const long long eg = c.e0 + e;
+      double x[P1];
+      const long long base = lane_base(eg, NM, c.W) + (long long)ps * P1 * c.W;
+#pragma unroll
+      for (int r = 0; r < P1; ++r) x[r] = eg < c.E ? __ldg(src + base + (long long)r * c.W) : 0.0;
+      double* ta = sm + e * ES + TAo + ps * S2;
+#pragma unroll
+      for (int k = 0; k < Q2; ++k) {
+        double s = B.a2[k * P1] * x[0];
+#pragma unroll
+        for (int r = 1; r < P1; ++r) s = fma(B.a2[k * P1 + r], x[r], s);
+        ta[k] = s;
+      }
+    });
+  } else if constexpr (S == PRISM) {
+    // item = (e, q); p unrolled so c2[p] is uniform (operators.py:275-295)
+    items<EB, P1, NT>([&](int e, int q) {
+      const long long eg = c.e0 + e;
+      const long long base = lane_base(eg, NM, c.W);
+      double* ta = sm + e * ES + TAo;
+      double u0q1 = 0.0;
+      int off = 0;
+#pragma unroll
+      for (int p = 0; p < P1; ++p) {
+        const int n = P1 - p;
+        double x[P1];
+#pragma unroll
+        for (int r = 0; r < P1; ++r)
+          x[r] = (r < n && eg < c.E) ? __ldg(src + base + (long long)(off + q * n + r) * c.W) : 0.0;
+        if (p == 0) u0q1 = x[1];  // mode (0, q, 1): collapsed-edge share
+        const int co = wfam_off(Q2, P1, p);
+#pragma unroll
+        for (int k = 0; k < Q2; ++k) {
+          double s = B.c2[co + k * n] * x[0];
+#pragma unroll
+          for (int r = 1; r < P1; ++r)
+            if (r < n) s = fma(B.c2[co + k * n + r], x[r], s);
+          if (p == 1) s = fma(u0q1, B.c2[k * P1 + 1], s);
+          ta[(p * P1 + q) * S2 + k] = s;
+        }
+        off += P1 * n;
+      }
+    });
+  } else {
+    // pyr / tet: item = (e, (p,q) pair); table c2[p+q] (tet) or c2[max(p,q)]
+    // (pyr) differs per item -> read from the device table buffer
+    const int4* pairs = reinterpret_cast<const int4*>(gtab + GLayout<S, P>::PAIRS);
+    items<EB, Dm::NPAIR, NT>([&](int e, int ps) {
+      const long long eg = c.e0 + e;
+      const int4 pr = __ldg(pairs + ps);  // p, q, mode offset, nr
+      const int m = (S == TET) ? pr.x + pr.y : cmax(pr.x, pr.y);
+      const int n = P1 - m;
+      const double* tab = gtab + GLayout<S, P>::C2 + wfam_off(Q2, P1, m);
+      const long long base = lane_base(eg, NM, c.W) + (long long)pr.z * c.W;
+      double x[P1];
+#pragma unroll
+      for (int r = 0; r < P1; ++r) x[r] = (r < pr.w && eg < c.E) ? __ldg(src + base + (long long)r * c.W) : 0.0;
+      double acc[Q2];
+#pragma unroll
+      for (int k = 0; k < Q2; ++k) {
+        double s = 0.0;
+#pragma unroll
+        for (int r = 0; r < P1; ++r)
+          if (r < pr.w) s = fma(__ldg(tab + k * n + r), x[r], s);
+        acc[k] = s;
+      }
+      double* ta = sm + e * ES + TAo;
+#pragma unroll
+      for (int k = 0; k < Q2; ++k) ta[(pr.x * P1 + pr.y) * S2 + k] = acc[k];
+      if (pr.x == 0 && pr.y == 0) {
+        // collapsed apex mode (0,0,1): Y[k] = c2[0][k][1] * uhat[0,0,1]
+        const double* t0 = gtab + GLayout<S, P>::C2;
+#pragma unroll
+        for (int k = 0; k < Q2; ++k) ta[P1 * P1 * S2 + k] = __ldg(t0 + k * P1 + 1) * x[1];
+      }
+    });
+  }
+}
+
+// ---- F2: q -> j.  TB[p][j][k] = sum_q B_p[j][q] TA[p][q][k] ---------------
+template <int S, int P, int EB, int NT, int ES, int TAo, int TBo>
+__device__ __forceinline__ void stage_f2(const FwdTab<S, P>& B, double* sm) {
+  using Dm = Dims<S, P>;
+  constexpr int P1 = Dm::P1, Q1 = Dm::Q1, Q2 = Dm::Q2, S2 = Dm::S2;
+  if constexpr (S != TET) {
+    items<EB, P1 * Q2, NT>([&](int e, int ps) {
+      const int p = ps / Q2, k = ps - p * Q2;
+      const double* ta = sm + e * ES + TAo;
+      double* tb = sm + e * ES + TBo;
+      double x[P1];
+#pragma unroll
+      for (int q = 0; q < P1; ++q) x[q] = ta[(p * P1 + q) * S2 + k];
+      double y = 0.0;
+      if constexpr (S == PYR) y = ta[P1 * P1 * S2 + k];
+#pragma unroll
+      for (int j = 0; j < Q1; ++j) {
+        double s = B.a1[j * P1] * x[0];
+#pragma unroll
+        for (int q = 1; q < P1; ++q) s = fma(B.a1[j * P1 + q], x[q], s);
+        if constexpr (S == PYR) {
+          // apex mode shares (operators.py:335-349)
+          if (p == 1) s += y;
+          if (p == 0) s = fma(B.a1[j * P1 + 1], y, s);
+        }
+        tb[(p * Q1 + j) * S2 + k] = s;
+      }
+    });
+  } else {
+    // tet: item = (e, k), p unrolled so b1[p] is uniform (operators.py:209-245)
+    items<EB, Q2, NT>([&](int e, int k) {
+      const double* ta = sm + e * ES + TAo;
+      double* tb = sm + e * ES + TBo;
+      const double y = ta[P1 * P1 * S2 + k];
+      const double x01 = ta[(0 * P1 + 1) * S2 + k];
+#pragma unroll
+      for (int p = 0; p < P1; ++p) {
+        const int n = P1 - p;
+        const int bo = wfam_off(Q1, P1, p);
+        double x[P1];
+#pragma unroll
+        for (int q = 0; q < P1; ++q)
+          if (q < n) x[q] = ta[(p * P1 + q) * S2 + k];
+#pragma unroll
+        for (int j = 0; j < Q1; ++j) {
+          double s = B.b1[bo + j * n] * x[0];
+#pragma unroll
+          for (int q = 1; q < P1; ++q)
+            if (q < n) s = fma(B.b1[bo + j * n + q], x[q], s);
+          if (p == 1) s = fma(B.b1[j * P1 + 1], x01, s) + y;  // edge (0,1,r) + apex shares
+          if (p == 0) s = fma(B.b1[j * P1 + 1], y, s);
+          tb[(p * Q1 + j) * S2 + k] = s;
+        }
+      }
+    });
+  }
+}
+
+// ---- F3 core: p -> i for one (j,k) line ------------------------------------
+template <int S, int P>
+__device__ __forceinline__ void line_a0(const FwdTab<S, P>& B, const double (&x)[P + 1],
+                                        double (&u)[Dims<S, P>::Q0]) {
+  using Dm = Dims<S, P>;
+#pragma unroll
+  for (int i = 0; i < Dm::Q0; ++i) {
+    double s = B.a0[i * Dm::P1] * x[0];
+#pragma unroll
+    for (int p = 1; p < Dm::P1; ++p) s = fma(B.a0[i * Dm::P1 + p], x[p], s);
+    u[i] = s;
+  }
+}
+
+// transposed p <- i for one (j,k) line
+template <int S, int P>
+__device__ __forceinline__ void line_a0t(const FwdTab<S, P>& B, const double (&r)[Dims<S, P>::Q0],
+                                         double (&t)[P + 1]) {
+  using Dm = Dims<S, P>;
+#pragma unroll
+  for (int p = 0; p < Dm::P1; ++p) {
+    double s = B.a0[p] * r[0];
+#pragma unroll
+    for (int i = 1; i < Dm::Q0; ++i) s = fma(B.a0[i * Dm::P1 + p], r[i], s);
+    t[p] = s;
+  }
+}
+
+// v = D u along a line of length Q (D row-major Q x Q)
+template <int Q>
+__device__ __forceinline__ void line_d(const double* D, const double (&u)[Q], double (&v)[Q]) {
+#pragma unroll
+  for (int a = 0; a < Q; ++a) {
+    double s = D[a * Q] * u[0];
+#pragma unroll
+    for (int b = 1; b < Q; ++b) s = fma(D[a * Q + b], u[b], s);
+    v[a] = s;
+  }
+}
+
+// r += D^T w along a line
+template <int Q>
+__device__ __forceinline__ void line_dt_acc(const double* D, const double (&w)[Q], double (&r)[Q]) {
+#pragma unroll
+  for (int a = 0; a < Q; ++a) {
+    double s = r[a];
+#pragma unroll
+    for (int b = 0; b < Q; ++b) s = fma(D[b * Q + a], w[b], s);
+    r[a] = s;
+  }
+}
+
+// ---- B2: j -> q.  TA[p][q][k] = sum_j B_p[j][q] TB[p][j][k] ---------------
+template <int S, int P, int EB, int NT, int ES, int TAo, int TBo>
+__device__ __forceinline__ void stage_b2(const FwdTab<S, P>& B, double* sm) {
+  using Dm = Dims<S, P>;
+  constexpr int P1 = Dm::P1, Q1 = Dm::Q1, Q2 = Dm::Q2, S2 = Dm::S2;
+  if constexpr (S != TET) {
+    items<EB, P1 * Q2, NT>([&](int e, int ps) {
+      const int p = ps / Q2, k = ps - p * Q2;
+      double* ta = sm + e * ES + TAo;
+      const double* tb = sm + e * ES + TBo;
+      double x[Q1];
+#pragma unroll
+      for (int j = 0; j < Q1; ++j) x[j] = tb[(p * Q1 + j) * S2 + k];
+#pragma unroll
+      for (int q = 0; q < P1; ++q) {
+        double s = B.a1[q] * x[0];
+#pragma unroll
+        for (int j = 1; j < Q1; ++j) s = fma(B.a1[j * P1 + q], x[j], s);
+        ta[(p * P1 + q) * S2 + k] = s;
+      }
+      if constexpr (S == PYR) {
+        if (p == 1) {  // Y[k] = sum_j TB[1][j][k] (apex share, operators.py:371)
+          double y = x[0];
+#pragma unroll
+          for (int j = 1; j < Q1; ++j) y += x[j];
+          ta[P1 * P1 * S2 + k] = y;
+        }
+      }
+    });
+  } else {
+    items<EB, Q2, NT>([&](int e, int k) {
+      double* ta = sm + e * ES + TAo;
+      const double* tb = sm + e * ES + TBo;
+      double t01 = 0.0;
+#pragma unroll
+      for (int p = 0; p < P1; ++p) {
+        const int n = P1 - p;
+        const int bo = wfam_off(Q1, P1, p);
+        double x[Q1];
+#pragma unroll
+        for (int j = 0; j < Q1; ++j) x[j] = tb[(p * Q1 + j) * S2 + k];
+#pragma unroll
+        for (int q = 0; q < P1; ++q) {
+          if (q < n) {
+            double s = B.b1[bo + q] * x[0];
+#pragma unroll
+            for (int j = 1; j < Q1; ++j) s = fma(B.b1[bo + j * n + q], x[j], s);
+            if (p == 0 && q == 1) t01 = s;
+            ta[(p * P1 + q) * S2 + k] = s;
+          }
+        }
+        if (p == 1) {
+          // edge (0,1,r) share s = sum_j b1[0][j][1] TB[1][j][k]; apex share
+          // Y[k] = sum_j TB[1][j][k] + sum_j b1[0][j][1] TB[0][j][k]
+          // (operators.py:263-271)
+          double s = B.b1[1] * x[0], y = x[0];
+#pragma unroll
+          for (int j = 1; j < Q1; ++j) {
+            s = fma(B.b1[j * P1 + 1], x[j], s);
+            y += x[j];
+          }
+          ta[(0 * P1 + 1) * S2 + k] = t01 + s;
+          ta[P1 * P1 * S2 + k] = y + t01;
+        }
+      }
+    });
+  }
+}
+
+// ---- B3: k -> r, write coefficients -----------------------------------------
+template <int S, int P, int EB, int NT, int ES, int TAo>
+__device__ __forceinline__ void stage_b3(const FwdTab<S, P>& B, const double* __restrict__ gtab,
+                                         double* __restrict__ dst, const Ctx& c, double* sm) {
+  using Dm = Dims<S, P>;
+  constexpr int P1 = Dm::P1, Q2 = Dm::Q2, S2 = Dm::S2, NM = Dm::NM;
+  if constexpr (S == HEX) {
+    items<EB, P1 * P1, NT>([&](int e, int ps) {
+      const long long eg = c.e0 + e;
+      const double* ta = sm + e * ES + TAo + ps * S2;
+      double x[Q2];
+#pragma unroll
+      for (int k = 0; k < Q2; ++k) x[k] = ta[k];
+      if (eg < c.Epad) {
+        const long long base = lane_base(eg, NM, c.W) + (long long)ps * P1 * c.W;
+#pragma unroll
+        for (int r = 0; r < P1; ++r) {
+          double s = B.a2[r] * x[0];
+#pragma unroll
+          for (int k = 1; k < Q2; ++k) s = fma(B.a2[k * P1 + r], x[k], s);
+          dst[base + (long long)r * c.W] = s;
+        }
+      }
+    });
+  } else if constexpr (S == PRISM) {
+    items<EB, P1, NT>([&](int e, int q) {
+      const long long eg = c.e0 + e;
+      const double* ta = sm + e * ES + TAo;
+      if (eg >= c.Epad) return;
+      const long long base = lane_base(eg, NM, c.W);
+      int off = 0;
+#pragma unroll
+      for (int p = 0; p < P1; ++p) {
+        const int n = P1 - p;
+        const int co = wfam_off(Q2, P1, p);
+        double x[Q2];
+#pragma unroll
+        for (int k = 0; k < Q2; ++k) x[k] = ta[(p * P1 + q) * S2 + k];
+#pragma unroll
+        for (int r = 0; r < P1; ++r) {
+          if (r < n) {
+            double s = B.c2[co + r] * x[0];
+#pragma unroll
+            for (int k = 1; k < Q2; ++k) s = fma(B.c2[co + k * n + r], x[k], s);
+            if (p == 0 && r == 1) {
+              // modes (0,q,1) += sum_k c2[0][k][1] TA[1][q][k] (operators.py:312-317)
+              double corr = 0.0;
+#pragma unroll
+              for (int k = 0; k < Q2; ++k) corr = fma(B.c2[k * P1 + 1], ta[(1 * P1 + q) * S2 + k], corr);
+              s += corr;
+            }
+            dst[base + (long long)(off + q * n + r) * c.W] = s;
+          }
+        }
+        off += P1 * n;
+      }
+    });
+  } else {
+    const int4* pairs = reinterpret_cast<const int4*>(gtab + GLayout<S, P>::PAIRS);
+    items<EB, Dm::NPAIR, NT>([&](int e, int ps) {
+      const long long eg = c.e0 + e;
+      const double* ta = sm + e * ES + TAo;
+      const int4 pr = __ldg(pairs + ps);
+      const int m = (S == TET) ? pr.x + pr.y : cmax(pr.x, pr.y);
+      const int n = P1 - m;
+      const double* tab = gtab + GLayout<S, P>::C2 + wfam_off(Q2, P1, m);
+      double x[Q2];
+#pragma unroll
+      for (int k = 0; k < Q2; ++k) x[k] = ta[(pr.x * P1 + pr.y) * S2 + k];
+      if (eg >= c.Epad) return;
+      const long long base = lane_base(eg, NM, c.W) + (long long)pr.z * c.W;
+      double apex = 0.0;
+      if (pr.x == 0 && pr.y == 0) {
+        const double* t0 = gtab + GLayout<S, P>::C2;
+#pragma unroll
+        for (int k = 0; k < Q2; ++k) {
+          double y = ta[P1 * P1 * S2 + k];
+          if constexpr (S == PYR) y += ta[(0 * P1 + 1) * S2 + k];
+          apex = fma(__ldg(t0 + k * P1 + 1), y, apex);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < P1; ++r) {
+        if (r < pr.w) {
+          double s = 0.0;
+#pragma unroll
+          for (int k = 0; k < Q2; ++k) s = fma(__ldg(tab + k * n + r), x[k], s);
+          if (r == 1) s += apex;
+          dst[base + (long long)r * c.W] = s;
+        }
+      }
+    });
+  }
+}
+
+}  // namespace sk

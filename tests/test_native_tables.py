@@ -1,0 +1,89 @@
+"""CPU tests of the native library: exported symbols match include/sk200.h,
+and the natively built constant tables equal the reference's (golden) ones.
+No device is needed: sk_basis_create is host-only."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+import oracle as O
+
+LIB = os.path.join(ROOT, "paper_2604_04644_b200", "libsk200.so")
+pytestmark = pytest.mark.skipif(not os.path.exists(LIB), reason="libsk200.so not built")
+
+SHAPES = ["hex", "prism", "pyr", "tet"]
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "sk200.h")).read()
+    return sorted(set(re.findall(r"\b(sk_[a-z_]+)\s*\(", src)))
+
+
+def test_exports_every_declared_symbol():
+    from paper_2604_04644_b200 import _lib
+
+    lib = _lib.load()
+    names = _declared()
+    assert len(names) >= 18
+    for n in names:
+        assert hasattr(lib, n), n
+    assert set(names) == set(_lib.SIGNATURES), set(names) ^ set(_lib.SIGNATURES)
+
+
+def test_status_codes_and_errors():
+    import paper_2604_04644_b200 as sk
+    from paper_2604_04644_b200 import _lib
+
+    lib = _lib.load()
+    h = ctypes.c_void_p()
+    assert lib.sk_basis_create(0, 3, ctypes.byref(h)) == _lib.SK_ERR_UNSUPPORTED  # quad
+    assert lib.sk_basis_create(9, 3, ctypes.byref(h)) == _lib.SK_ERR_STATE
+    assert lib.sk_basis_create(2, 0, ctypes.byref(h)) == _lib.SK_ERR_ARG
+    assert lib.sk_basis_create(2, 11, ctypes.byref(h)) == _lib.SK_ERR_UNSUPPORTED
+    with pytest.raises(sk.UnsupportedStrategyError):
+        sk.build_shape_basis(sk.Shape.QUAD, 2)
+    with pytest.raises(sk.UnsupportedStrategyError):
+        sk.build_shape_basis(sk.Shape.HEX, 2, qpoints=(5, 5, 5))
+    b = sk.build_shape_basis(sk.Shape.TET, 3)
+    # argument checks happen before any device work
+    assert lib.sk_helmholtz_apply(b.handle, 1, 0, 4, 1, 1, None, None, -1.0, None, None) == _lib.SK_ERR_ARG
+    assert lib.sk_mass_apply(b.handle, 1, -1, 1, 1, None, None, None, None) == _lib.SK_ERR_ARG
+    assert lib.sk_bwd_trans(b.handle, 4, 0, 1, None, None, None) == _lib.SK_ERR_ARG
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+@pytest.mark.parametrize("P", range(1, 11))
+def test_native_tables_match_reference(golden_tables, shape, P):
+    import paper_2604_04644_b200 as sk
+
+    g = golden_tables
+    k = f"{shape}_P{P}"
+    b = sk.build_shape_basis(sk.Shape(shape), P)
+    assert b.qcounts == O.qcounts(shape, P)
+    assert b.n_modes == O.mode_count(shape, P)
+    assert b.modes == tuple(O.mode_set(shape, P))
+
+    def close(a, ref, tol=1e-14):
+        a = np.asarray(a).reshape(ref.shape)
+        assert np.max(np.abs(a - ref)) <= tol * max(1.0, np.max(np.abs(ref))), (np.max(np.abs(a - ref)))
+
+    for d in range(3):
+        close(b.table(f"z{d}"), g[f"{k}_z{d}"])
+        close(b.table(f"w{d}"), g[f"{k}_w{d}"])
+        close(b.table(f"D{d}"), g[f"{k}_D{d}"], 1e-13)
+        if f"{k}_a{d}" in g:
+            close(b.table(f"a{d}"), g[f"{k}_a{d}"])
+            close(b.table(f"da{d}"), g[f"{k}_da{d}"], 1e-13)
+    for name, native in (("b2", "b1"), ("c3", "c2")):
+        p = 0
+        while f"{k}_{name}_{p}" in g:
+            close(b.table(f"{native}_{p}"), g[f"{k}_{name}_{p}"])
+            close(b.table(f"d{native}_{p}"), g[f"{k}_d{name}_{p}"], 1e-13)
+            p += 1
+    close(b.ref_weights, g[f"{k}_refw"])
+    close(b.gdense, g[f"{k}_G"], 1e-14)

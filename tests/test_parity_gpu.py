@@ -1,0 +1,160 @@
+"""Device parity: every operator of the device path against the reference's
+golden outputs and the CPU oracle, through the public API (C ABI underneath).
+
+Bar (BASELINE north star): max-normalised error <= 1e-12 in FP64
+(reference metric bench.py:192-194)."""
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = ["hex", "prism", "pyr", "tet"]
+TOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def sk():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2604_04644_b200 as sk
+
+    return sk
+
+
+def _block(sk, shape, P, deformed, n, seed, width, state=None, ncomp=1):
+    b = sk.build_shape_basis(sk.Shape(shape), P)
+    gcls = sk.GeometryClass.DEFORMED if deformed else sk.GeometryClass.REGULAR
+    fac = sk.make_synthetic_factors(b, gcls, n, seed=seed)
+    return sk.Block(b, fac, state or sk.FieldState.COEFF, ncomp, width)
+
+
+def _err(a, b):
+    return O.rel_diff(np.asarray(a), np.asarray(b))
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+@pytest.mark.parametrize("P", [1, 2, 3, 4, 5, 6, 8, 10])
+@pytest.mark.parametrize("geo", ["regular", "deformed"])
+def test_golden(sk, golden_ops, shape, P, geo):
+    """Against the real reference's outputs (tests/golden/make_golden.py)."""
+    g = golden_ops
+    k = f"{shape}_P{P}_{geo}"
+    blk = _block(sk, shape, P, geo == "deformed", 2, 3, 2)
+    blk.set_elements(g[f"{k}_x"][None])
+    for lam in (0.0, 1.0, 2.5):
+        got = sk.helmholtz_apply(blk, lam).get_elements()[0]
+        assert _err(got, g[f"{k}_helm_{lam}"]) <= TOL, (lam, _err(got, g[f"{k}_helm_{lam}"]))
+    assert _err(sk.mass_apply(blk).get_elements()[0], g[f"{k}_mass"]) <= TOL
+    assert _err(sk.bwd_trans(blk).get_elements()[0], g[f"{k}_bwd"]) <= TOL
+    pb = blk.like(sk.FieldState.PHYS)
+    pb.set_elements(g[f"{k}_y"][None])
+    assert _err(sk.iproduct_wrt_base(pb).get_elements()[0], g[f"{k}_iprod"]) <= TOL
+    assert _err(sk.phys_deriv(pb).get_elements(), g[f"{k}_dphys"]) <= TOL
+    vb = blk.like(sk.FieldState.PHYS, 3)
+    vb.set_elements(g[f"{k}_v"])
+    assert _err(sk.iproduct_wrt_deriv_base(vb).get_elements()[0], g[f"{k}_ipderiv"]) <= TOL
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+@pytest.mark.parametrize("P", [2, 4, 7, 9])
+@pytest.mark.parametrize("width", [1, 8])
+def test_oracle_ragged_tiles(sk, shape, P, width):
+    """Many elements (not a multiple of the CTA tile nor of the width)
+    against the oracle on the same seeded mesh."""
+    n = 157
+    el = O.element(shape, P)
+    for deformed in (False, True):
+        blk = _block(sk, shape, P, deformed, n, 5, width)
+        geo = O.synthetic_geometry(el, deformed, n, seed=5)
+        x = O.bench_coeffs(O.SHAPE_INDEX[shape], P, el.nm, n, seed=5)
+        blk.set_elements(x[None])
+        for lam in (0.0, 1.3):
+            got = sk.helmholtz_apply(blk, lam).get_elements()[0]
+            assert _err(got, O.helmholtz_coll(el, geo, x, lam)) <= TOL
+        assert _err(sk.mass_apply(blk).get_elements()[0], O.mass(el, geo, x)) <= TOL
+        y = np.random.default_rng(P).uniform(-1, 1, (el.nq, n))
+        pb = blk.like(sk.FieldState.PHYS)
+        pb.set_elements(y[None])
+        assert _err(sk.phys_deriv(pb).get_elements(), O.phys_deriv(el, geo, y)) <= TOL
+        assert _err(sk.iproduct_wrt_base(pb).get_elements()[0], O.iproduct_wrt_base(el, geo, y)) <= TOL
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+def test_padding_lanes_stay_zero(sk, shape):
+    """Padded lanes of the lane-major layout are written as zeros
+    (reference acceptance criterion 9)."""
+    n, w = 13, 8
+    blk = _block(sk, shape, 3, True, n, 1, w)
+    el = O.element(shape, 3)
+    blk.set_elements(O.bench_coeffs(O.SHAPE_INDEX[shape], 3, el.nm, n)[None])
+    out = blk.like(sk.FieldState.COEFF)
+    raw = out.host(sk.AccessQualifier.WRITE_ONLY)
+    raw[...] = 7.0  # poison, including the padded lanes
+    sk.helmholtz_apply(blk, 1.0, out=out)
+    flat = out.host()[0].transpose(1, 0, 2).reshape(el.nm, -1)
+    assert np.all(flat[:, n:] == 0.0)
+    assert np.all(np.isfinite(flat[:, :n]))
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+def test_device_geometry_builder(sk, shape):
+    """Device iso-parametric metric == oracle restatement of
+    deformed_factors_from_coords on the same seeded mesh."""
+    P, n = 4, 9
+    b = sk.build_shape_basis(sk.Shape(shape), P)
+    fac = sk.make_synthetic_factors(b, sk.GeometryClass.DEFORMED, n, seed=2)
+    geo = O.synthetic_geometry(O.element(shape, P), True, n, seed=2)
+    assert _err(fac.dxi_dx, geo.dxi) <= 1e-13
+    assert _err(fac.jac, geo.jac) <= 1e-13
+    # coords route
+    from oracle.geom import deformed_coords
+
+    coords = deformed_coords(O.element(shape, P), O.deformation_params(n, 2))
+    fac2 = sk.deformed_factors_from_coords(b, coords)
+    assert _err(fac2.dxi_dx, geo.dxi) <= 1e-13
+
+
+def test_memory_region_transfer_counting(sk):
+    """Repeated applies do not re-transfer (acceptance criterion 6)."""
+    blk = _block(sk, "hex", 2, True, 10, 0, 1)
+    el = O.element("hex", 2)
+    blk.set_elements(O.bench_coeffs(2, 2, el.nm, 10)[None])
+    out = blk.like(sk.FieldState.COEFF)
+    for _ in range(3):
+        sk.helmholtz_apply(blk, 1.0, out=out)
+    assert blk.region.transfer_count == 1
+    out.get_elements()
+    assert out.region.transfer_count == 1
+
+
+def test_large_block_properties(sk):
+    """At the bench size (2^20 tets, P=4): sampled elements match the oracle
+    exactly, and the operator is symmetric (u.Hv == v.Hu, size-independent)."""
+    import torch
+
+    n, P = 1 << 20, 4
+    el = O.element("tet", P)
+    b = sk.build_shape_basis(sk.Shape.TET, P)
+    fac = sk.make_synthetic_factors(b, sk.GeometryClass.DEFORMED, n, seed=0)
+    blk = sk.Block(b, fac, sk.FieldState.COEFF, 1, 1)
+    x = O.bench_coeffs(O.SHAPE_INDEX["tet"], P, el.nm, n, seed=0)
+    blk.set_elements(x[None])
+    hx = sk.helmholtz_apply(blk, 1.0).get_elements()[0]
+    idx = np.array([0, 1, 777, 65535, 65536, 999_999, n - 1])
+    params = np.concatenate([O.deformation_params(1, 0, first=int(e)) for e in idx])
+    from oracle.geom import deformed_coords
+
+    geo = O.deformed_geometry_from_coords(el, deformed_coords(el, params))
+    assert _err(hx[:, idx], O.helmholtz_coll(el, geo, x[:, idx], 1.0)) <= TOL
+    y = np.random.default_rng(1).uniform(-1, 1, x.shape)
+    blk2 = blk.like(sk.FieldState.COEFF)
+    blk2.set_elements(y[None])
+    hy = sk.helmholtz_apply(blk2, 1.0).get_elements()[0]
+    a, c = np.sum(x * hy), np.sum(y * hx)
+    assert abs(a - c) <= 1e-12 * np.sum(np.abs(x * hy))
+    del torch
