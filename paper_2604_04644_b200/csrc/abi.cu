@@ -196,7 +196,7 @@ int sk_payload_size(const sk_basis* b, int geo_class, int kind, int64_t E, int64
   if (geo_class != SK_GEO_REGULAR && geo_class != SK_GEO_DEFORMED) return fail(SK_ERR_ARG, "bad geometry class");
   if (kind < 0 || kind > 2) return fail(SK_ERR_ARG, "bad payload kind");
   if (E < 0) return fail(SK_ERR_ARG, "element count must be nonnegative");
-  *n = b->ops->payload_doubles(kind, geo_class) * E;
+  *n = b->ops->payload_doubles(kind, geo_class) * b->ops->payload_elements(E);
   return SK_OK;
 }
 

@@ -18,21 +18,33 @@
 namespace sk {
 
 // ---------------------------------------------------------------------------
-// launch configuration: EB elements per CTA so that EB x (largest stage item
-// count) fills ~256 threads, capped by shared memory
+// launch configuration.  Low orders (3 quad-point planes of 16 elements fit
+// in ~100 KB) use the interleaved 16-element tile (conflict-free shared
+// memory, 16-wide payload lanes); high orders use element-major tiles of EB
+// elements with EB x (largest stage item count) ~ 256 threads.
+template <int S, int P>
+struct Mode {
+  using Dm = Dims<S, P>;
+  static constexpr bool IL = 3 * Dm::NQ * 16 * 8 <= 100 * 1024;
+  static constexpr int PW = IL ? 16 : 1;  // payload lane width, shared by every op of (S, P)
+};
+
 template <int S, int P, int OP>
 struct Cfg {
   using Dm = Dims<S, P>;
+  static constexpr bool IL = Mode<S, P>::IL;
+  static constexpr int PW = Mode<S, P>::PW;
   static constexpr int planes = (OP == OP_HELM || OP == OP_PDERIV || OP == OP_IPDERIV) ? 3 : 2;
-  static constexpr int ES = planes * Dm::PLANE;
   static constexpr int items =
       cmax(cmax(cmax(Dm::Q1 * Dm::Q2, Dm::Q0 * Dm::Q2), cmax(Dm::Q0 * Dm::Q1, Dm::P1 * Dm::P1)), Dm::NPAIR);
+  static constexpr int ES_pe = planes * Dm::Q0 * Dm::Q1 * (Dm::Q2 | 1);
   static constexpr int eb_thr = cmax(1, (256 + items / 2) / items);
-  static constexpr int eb_smem = cmax(1, (96 * 1024) / (ES * 8));
-  static constexpr int EB = eb_thr < eb_smem ? eb_thr : eb_smem;
+  static constexpr int eb_smem = cmax(1, (96 * 1024) / (ES_pe * 8));
+  static constexpr int EB = IL ? 16 : (eb_thr < eb_smem ? eb_thr : eb_smem);
+  using L = Lay<S, P, planes, IL, EB>;
   static constexpr int NT0 = ((EB * items + 31) / 32) * 32;
-  static constexpr int NT = NT0 > 1024 ? 1024 : NT0;
-  static constexpr int SMEM = EB * ES * 8;
+  static constexpr int NT = NT0 > 512 ? 512 : NT0;
+  static constexpr int SMEM = L::SMEM_DOUBLES * 8;
 };
 
 // ---------------------------------------------------------------------------
@@ -145,15 +157,25 @@ static void ensure_smem(K kernel, int bytes) {
   if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
 
-template <int S, int P, int OP, auto Kern>
+template <int S, int P, int OP, class Op>
 static int go(const OpArgs<S, P>& a, const LaunchReq& r, int gy, void* stream) {
   using C = Cfg<S, P, OP>;
-  static std::once_flag once;  // one flag per kernel instantiation
-  std::call_once(once, [] { ensure_smem(Kern, C::SMEM); });
+  static_assert(!C::IL || C::EB == C::PW, "IL tiles must align with payload lanes");
+  static std::once_flag once;  // one per kernel instantiation
+  static int resident = 1;
+  std::call_once(once, [] {
+    ensure_smem(k_tile<Op, S, P>, C::SMEM);
+    int per_sm = 1, sms = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tile<Op, S, P>, Op::NT, C::SMEM);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    resident = (per_sm > 0 ? per_sm : 1) * sms;
+  });
   const long long tiles = (r.Epad + C::EB - 1) / C::EB;
   if (tiles == 0) return 0;
-  dim3 grid((unsigned)tiles, (unsigned)gy);
-  Kern<<<grid, C::NT, C::SMEM, static_cast<cudaStream_t>(stream)>>>(a);
+  OpArgs<S, P>& args = const_cast<OpArgs<S, P>&>(a);
+  args.pf_ahead = resident / (gy > 0 ? gy : 1);
+  k_tile<Op, S, P><<<dim3((unsigned)tiles, (unsigned)gy), Op::NT, C::SMEM, static_cast<cudaStream_t>(stream)>>>(args);
   return (int)cudaGetLastError();
 }
 
@@ -179,35 +201,35 @@ int launch(int op, const LaunchReq& r, void* stream) {
     case OP_HELM: {
       using C = Cfg<S, P, OP_HELM>;
       if (def) {
-        if (r.lam != 0.0) return go<S, P, OP_HELM, k_helm<S, P, C::EB, C::NT, GEO_DEFORMED, true>>(a, r, r.ncomp, stream);
-        return go<S, P, OP_HELM, k_helm<S, P, C::EB, C::NT, GEO_DEFORMED, false>>(a, r, r.ncomp, stream);
+        if (r.lam != 0.0) return go<S, P, OP_HELM, k_helm<S, P, typename C::L, C::NT, C::PW, GEO_DEFORMED, true>>(a, r, r.ncomp, stream);
+        return go<S, P, OP_HELM, k_helm<S, P, typename C::L, C::NT, C::PW, GEO_DEFORMED, false>>(a, r, r.ncomp, stream);
       }
-      if (r.lam != 0.0) return go<S, P, OP_HELM, k_helm<S, P, C::EB, C::NT, GEO_REGULAR, true>>(a, r, r.ncomp, stream);
-      return go<S, P, OP_HELM, k_helm<S, P, C::EB, C::NT, GEO_REGULAR, false>>(a, r, r.ncomp, stream);
+      if (r.lam != 0.0) return go<S, P, OP_HELM, k_helm<S, P, typename C::L, C::NT, C::PW, GEO_REGULAR, true>>(a, r, r.ncomp, stream);
+      return go<S, P, OP_HELM, k_helm<S, P, typename C::L, C::NT, C::PW, GEO_REGULAR, false>>(a, r, r.ncomp, stream);
     }
     case OP_MASS: {
       using C = Cfg<S, P, OP_MASS>;
-      if (def) return go<S, P, OP_MASS, k_mass<S, P, C::EB, C::NT, GEO_DEFORMED>>(a, r, r.ncomp, stream);
-      return go<S, P, OP_MASS, k_mass<S, P, C::EB, C::NT, GEO_REGULAR>>(a, r, r.ncomp, stream);
+      if (def) return go<S, P, OP_MASS, k_mass<S, P, typename C::L, C::NT, C::PW, GEO_DEFORMED>>(a, r, r.ncomp, stream);
+      return go<S, P, OP_MASS, k_mass<S, P, typename C::L, C::NT, C::PW, GEO_REGULAR>>(a, r, r.ncomp, stream);
     }
     case OP_BWD: {
       using C = Cfg<S, P, OP_BWD>;
-      return go<S, P, OP_BWD, k_bwd<S, P, C::EB, C::NT>>(a, r, r.ncomp, stream);
+      return go<S, P, OP_BWD, k_bwd<S, P, typename C::L, C::NT>>(a, r, r.ncomp, stream);
     }
     case OP_IPROD: {
       using C = Cfg<S, P, OP_IPROD>;
-      if (def) return go<S, P, OP_IPROD, k_iprod<S, P, C::EB, C::NT, GEO_DEFORMED>>(a, r, r.ncomp, stream);
-      return go<S, P, OP_IPROD, k_iprod<S, P, C::EB, C::NT, GEO_REGULAR>>(a, r, r.ncomp, stream);
+      if (def) return go<S, P, OP_IPROD, k_iprod<S, P, typename C::L, C::NT, C::PW, GEO_DEFORMED>>(a, r, r.ncomp, stream);
+      return go<S, P, OP_IPROD, k_iprod<S, P, typename C::L, C::NT, C::PW, GEO_REGULAR>>(a, r, r.ncomp, stream);
     }
     case OP_PDERIV: {
       using C = Cfg<S, P, OP_PDERIV>;
-      if (def) return go<S, P, OP_PDERIV, k_pderiv<S, P, C::EB, C::NT, GEO_DEFORMED>>(a, r, 1, stream);
-      return go<S, P, OP_PDERIV, k_pderiv<S, P, C::EB, C::NT, GEO_REGULAR>>(a, r, 1, stream);
+      if (def) return go<S, P, OP_PDERIV, k_pderiv<S, P, typename C::L, C::NT, C::PW, GEO_DEFORMED>>(a, r, 1, stream);
+      return go<S, P, OP_PDERIV, k_pderiv<S, P, typename C::L, C::NT, C::PW, GEO_REGULAR>>(a, r, 1, stream);
     }
     case OP_IPDERIV: {
       using C = Cfg<S, P, OP_IPDERIV>;
-      if (def) return go<S, P, OP_IPDERIV, k_ipderiv<S, P, C::EB, C::NT, GEO_DEFORMED>>(a, r, 1, stream);
-      return go<S, P, OP_IPDERIV, k_ipderiv<S, P, C::EB, C::NT, GEO_REGULAR>>(a, r, 1, stream);
+      if (def) return go<S, P, OP_IPDERIV, k_ipderiv<S, P, typename C::L, C::NT, C::PW, GEO_DEFORMED>>(a, r, 1, stream);
+      return go<S, P, OP_IPDERIV, k_ipderiv<S, P, typename C::L, C::NT, C::PW, GEO_REGULAR>>(a, r, 1, stream);
     }
   }
   return (int)cudaErrorInvalidValue;
@@ -242,16 +264,22 @@ long long payload_doubles(int kind, int geo) {
   return kind == 0 ? 8 : kind == 1 ? 1 : 9;
 }
 
+template <int S, int P>
+long long payload_elements(long long E) {
+  constexpr long long PW = Mode<S, P>::PW;
+  return (E + PW - 1) / PW * PW;
+}
+
 // write the payload entries of one deformed point from (dxi, w|J|)
 template <int S, int P>
 __device__ __forceinline__ void put_point(int kind, long long e, int l, const double (&dxi)[3][3], double wjac,
                                           double* __restrict__ pay, const double* __restrict__ gtab) {
   using Dm = Dims<S, P>;
-  constexpr int NQ = Dm::NQ;
+  constexpr int NQ = Dm::NQ, PW = Mode<S, P>::PW;
   const int k = l % Dm::Q2, ij = l / Dm::Q2;
-  const int km = k * Dm::Q0 * Dm::Q1 + ij;
+  const long long km = k * Dm::Q0 * Dm::Q1 + ij;
   if (kind == 1) {
-    pay[e * NQ + l] = wjac;
+    pay[pay_base<PW>(e, 1, NQ) + (long long)l * PW] = wjac;
     return;
   }
   double G[3][3];
@@ -277,21 +305,22 @@ __device__ __forceinline__ void put_point(int kind, long long e, int l, const do
 #pragma unroll
       for (int n = 0; n < 3; ++n) T[a][n] = L[a][0] * G[0][n] + L[a][1] * G[1][n] + L[a][2] * G[2][n];
     const int mi[6] = {0, 0, 0, 1, 1, 2}, ni[6] = {0, 1, 2, 1, 2, 2};
-    double* o = pay + e * (7LL * NQ) + km;
+    double* o = pay + pay_base<PW>(e, 7, NQ) + km * PW;
 #pragma unroll
     for (int c = 0; c < 6; ++c) {
       const int m = mi[c], n = ni[c];
-      o[c * NQ] = G[0][m] * T[0][n] + G[1][m] * T[1][n] + G[2][m] * T[2][n];
+      o[(long long)c * NQ * PW] = G[0][m] * T[0][n] + G[1][m] * T[1][n] + G[2][m] * T[2][n];
     }
-    o[6 * NQ] = wjac;
+    o[6LL * NQ * PW] = wjac;
     return;
   }
   // DERIV: T[m][j] = sum_a G[a][m] dxi[a][j]
-  double* o = pay + e * (9LL * NQ) + km;
+  double* o = pay + pay_base<PW>(e, 9, NQ) + km * PW;
 #pragma unroll
   for (int m = 0; m < 3; ++m)
 #pragma unroll
-    for (int j = 0; j < 3; ++j) o[(m * 3 + j) * NQ] = G[0][m] * dxi[0][j] + G[1][m] * dxi[1][j] + G[2][m] * dxi[2][j];
+    for (int j = 0; j < 3; ++j)
+      o[(long long)(m * 3 + j) * NQ * PW] = G[0][m] * dxi[0][j] + G[1][m] * dxi[1][j] + G[2][m] * dxi[2][j];
 }
 
 template <int S, int P>
@@ -314,22 +343,24 @@ __global__ void k_pack_deformed(int kind, long long E, const double* __restrict_
 template <int S, int P>
 __global__ void k_pack_regular(int kind, long long E, const double* __restrict__ dxi, const double* __restrict__ jac,
                                double* __restrict__ pay) {
+  constexpr int PW = Mode<S, P>::PW;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < E; e += (long long)gridDim.x * blockDim.x) {
     const double* d = dxi + e * 9;
     if (kind == 0) {
-      double* o = pay + e * 8;
+      double* o = pay + pay_base<PW>(e, 8, 1);
       const int mi[6] = {0, 0, 0, 1, 1, 2}, ni[6] = {0, 1, 2, 1, 2, 2};
       for (int c = 0; c < 6; ++c) {
         const int a = mi[c], b = ni[c];
         const double s = fma(d[a * 3 + 2], d[b * 3 + 2], fma(d[a * 3 + 1], d[b * 3 + 1], d[a * 3] * d[b * 3]));
-        o[c] = s * jac[e];
+        o[c * PW] = s * jac[e];
       }
-      o[6] = jac[e];
-      o[7] = 0.0;
+      o[6 * PW] = jac[e];
+      o[7 * PW] = 0.0;
     } else if (kind == 1) {
-      pay[e] = jac[e];
+      pay[pay_base<PW>(e, 1, 1)] = jac[e];
     } else {
-      for (int a = 0; a < 9; ++a) pay[e * 9 + a] = d[a];
+      double* o = pay + pay_base<PW>(e, 9, 1);
+      for (int a = 0; a < 9; ++a) o[a * PW] = d[a];
     }
   }
 }
@@ -477,6 +508,7 @@ const OpSet* opset_impl() {
                             &launch<S, P>,
                             &config<S, P>,
                             &payload_doubles<S, P>,
+                            &payload_elements<S, P>,
                             &pack<S, P>,
                             &geometry<S, P>};
   return &ops;

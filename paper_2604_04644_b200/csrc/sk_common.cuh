@@ -1,5 +1,5 @@
-// Compile-time dimensions, kernel-parameter tables and small device helpers
-// shared by every sm_100a operator kernel.
+// Compile-time dimensions, kernel-parameter tables, shared-memory layout
+// policies and small device helpers shared by every sm_100a kernel.
 #pragma once
 
 #include <cstdint>
@@ -11,6 +11,7 @@ namespace sk {
 enum : int { GEO_REGULAR = 0, GEO_DEFORMED = 1 };
 
 __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
+__host__ __device__ constexpr int cmin(int a, int b) { return a < b ? a : b; }
 
 __host__ __device__ constexpr int n_modes(int S, int P) {
   return S == HEX     ? (P + 1) * (P + 1) * (P + 1)
@@ -30,31 +31,56 @@ struct Dims {
   static constexpr int NQ = Q0 * Q1 * Q2;
   static constexpr int NM = n_modes(S, P);
   static constexpr int NTRI = P1 * (P1 + 1) / 2;
-  // smem quad-point arrays are [i][j][k] with an odd k-row stride so that
-  // a line walk along any direction is bank-conflict free for doubles
-  static constexpr int S2 = Q2 | 1;
-  static constexpr int PLANE = Q0 * Q1 * S2;
   // ragged first/last stages (pyr, tet) iterate over (p, q) pairs
   static constexpr int NPAIR = (S == TET) ? NTRI : P1 * P1;
 };
 
+// Shared-memory layout of the per-element work arrays.  Each element owns
+// NPL "planes" of quad-point-sized arrays, addressed by a plane-relative
+// index idx = plane*PLANE + (i*Q1 + j)*S2 + k (k-row stride S2).
+//
+//  IL (interleaved, low orders): the EB = 16 elements of a tile are the
+//    fastest smem dimension, sm[idx*16 + e], and work items map
+//    e = lane % 16.  Every half-warp then reads/writes 16 consecutive
+//    doubles whatever the sweep direction: bank-conflict free by
+//    construction (the shared-memory analogue of the reference's SIMD lane
+//    interleave, field_block.py:205-214).
+//  per-element (high orders, where 16 elements do not fit): element-major
+//    sm[e*ES + idx] with an odd k-row stride so that line walks are
+//    conflict free within an element.
+template <int S, int P, int NPL, bool IL_, int EB_>
+struct Lay {
+  using Dm = Dims<S, P>;
+  static constexpr bool IL = IL_;
+  static constexpr int EB = EB_;
+  static constexpr int S2 = IL ? Dm::Q2 : (Dm::Q2 | 1);
+  static constexpr int PLANE = Dm::Q0 * Dm::Q1 * S2;
+  static constexpr int ES = NPL * PLANE;
+  // tile staging area for coefficients (IL only): [mode][EB + 1]
+  static constexpr int XSTR = EB + 1;
+  static constexpr int SMEM_DOUBLES = EB * ES;
+  __device__ static __forceinline__ int at(int e, int idx) {
+    if constexpr (IL)
+      return idx * EB + e;
+    else
+      return e * ES + idx;
+  }
+};
+
 // offset of the leading-index-p slice in a packed warped family whose slice
 // p has (P1 - p) columns and Q rows
-__host__ __device__ constexpr int wfam_off(int Q, int P1, int p) {
-  return Q * (p * P1 - p * (p - 1) / 2);
-}
+__host__ __device__ constexpr int wfam_off(int Q, int P1, int p) { return Q * (p * P1 - p * (p - 1) / 2); }
 
 // Basis tables consumed with compile-time indices: they live in the kernel
 // parameter space (constant bank) and enter DFMAs as uniform operands.
-// Filled either with values (B) or with derivatives (D_k B) per direction.
 template <int S, int P>
 struct FwdTab {
   using Dm = Dims<S, P>;
-  double a0[Dm::Q0 * Dm::P1];                                // dir 0 [i][p]
-  double a1[(S != TET) ? Dm::Q1 * Dm::P1 : 1];               // dir 1 [j][q]
-  double a2[(S == HEX) ? Dm::Q2 * Dm::P1 : 1];               // dir 2 [k][r]
-  double b1[(S == TET) ? Dm::Q1 * Dm::NTRI : 1];             // tet dir 1, per p
-  double c2[(S == PRISM) ? Dm::Q2 * Dm::NTRI : 1];           // prism dir 2, per p
+  double a0[Dm::Q0 * Dm::P1];                       // dir 0 [i][p]
+  double a1[(S != TET) ? Dm::Q1 * Dm::P1 : 1];      // dir 1 [j][q]
+  double a2[(S == HEX) ? Dm::Q2 * Dm::P1 : 1];      // dir 2 [k][r]
+  double b1[(S == TET) ? Dm::Q1 * Dm::NTRI : 1];    // tet dir 1, per p
+  double c2[(S == PRISM) ? Dm::Q2 * Dm::NTRI : 1];  // prism dir 2, per p
 };
 
 template <int S, int P>
@@ -69,13 +95,25 @@ struct DTab {
 template <int S, int P>
 struct GLayout {
   using Dm = Dims<S, P>;
-  static constexpr int C2 = 0;                               // dir-2 family values
-  static constexpr int DC2 = C2 + Dm::Q2 * Dm::NTRI;         // dir-2 family derivatives
-  static constexpr int PAIRS = DC2 + Dm::Q2 * Dm::NTRI;      // NPAIR x 4 ints (as 2 doubles)
-  static constexpr int REGK = PAIRS + 2 * Dm::NPAIR;         // [6][k][i*Q1+j]: refw,g00,g10,g11,g20,g21
-  static constexpr int REFW = REGK + 6 * Dm::NQ;             // [i][j][k] refw
+  static constexpr int C2 = 0;                           // dir-2 family values
+  static constexpr int DC2 = C2 + Dm::Q2 * Dm::NTRI;     // dir-2 family derivatives
+  static constexpr int PAIRS = DC2 + Dm::Q2 * Dm::NTRI;  // NPAIR x 4 ints
+  static constexpr int REGK = PAIRS + 2 * Dm::NPAIR;     // [6][k][i*Q1+j]: refw,g00,g10,g11,g20,g21
+  static constexpr int REFW = REGK + 6 * Dm::NQ;         // [i][j][k] refw
   static constexpr int SIZE = REFW + Dm::NQ;
 };
+
+// Geometry payload addressing: [E/PW][C][NQ][PW], i.e. PW elements
+// interleaved innermost (PW = 16 for IL kernels: one 128-byte line per
+// point per half-warp), or plain [E][C][NQ] when PW = 1.
+template <int PW>
+__device__ __forceinline__ long long pay_base(long long e, int C, int N) {
+  if constexpr (PW == 1) {
+    return e * (long long)C * N;
+  } else {
+    return (e / PW) * (long long)C * N * PW + (e % PW);
+  }
+}
 
 struct Ctx {
   long long e0;    // first element of this CTA's tile
@@ -86,16 +124,22 @@ struct Ctx {
 
 // index of data point 0 of element e in a lane-major (G, N, W) component
 __device__ __forceinline__ long long lane_base(long long e, int N, int W) {
+  if (W == 1) return e * N;
   const long long g = e / W;
   return g * (long long)N * W + (e - g * W);
 }
 
-template <int EB, int NPASS, int NT, class F>
+template <class L, int NPASS, int NT, class F>
 __device__ __forceinline__ void items(F&& f) {
 #pragma unroll 1
-  for (int w = threadIdx.x; w < EB * NPASS; w += NT) {
-    const int e = w / NPASS;
-    f(e, w - e * NPASS);
+  for (int w = threadIdx.x; w < L::EB * NPASS; w += NT) {
+    if constexpr (L::IL) {
+      const int ps = w / L::EB;
+      f(w - ps * L::EB, ps);
+    } else {
+      const int e = w / NPASS;
+      f(e, w - e * NPASS);
+    }
   }
 }
 

