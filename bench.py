@@ -188,7 +188,7 @@ def run_reference(args, ws, rank):
     if rank != 0:
         return
     cores = os.cpu_count() or 1
-    ref = CpuReference(cores)
+    ref = CpuReference(cores, int(os.environ.get("SK_BENCH_CPU_PER_CORE", "4096")))
     step_s = max(0.3, min(3.0, 150.0 / max(1, args.steps + args.warmup)))
     reps = ref.calibrate(step_s)
     for _ in range(args.warmup):

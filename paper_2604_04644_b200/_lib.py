@@ -12,7 +12,8 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsk200.so")
+#: SK200_LIB selects an alternative in-tree build (tuning variants only)
+LIB_PATH = os.environ.get("SK200_LIB") or os.path.join(_HERE, "libsk200.so")
 
 SK_OK, SK_ERR_STATE, SK_ERR_UNSUPPORTED, SK_ERR_ARG, SK_ERR_CUDA = range(5)
 SK_GEO_REGULAR, SK_GEO_DEFORMED = 0, 1

@@ -10,6 +10,7 @@
 
 #include "sk_ops.cuh"
 #include "sk_opset.hpp"
+#include "sk_tune.h"
 
 #ifndef SK_S
 #error "compile with -DSK_S=<shape> -DSK_P=<order>"
@@ -18,33 +19,39 @@
 namespace sk {
 
 // ---------------------------------------------------------------------------
-// launch configuration.  Low orders (3 quad-point planes of 16 elements fit
-// in ~100 KB) use the interleaved 16-element tile (conflict-free shared
-// memory, 16-wide payload lanes); high orders use element-major tiles of EB
-// elements with EB x (largest stage item count) ~ 256 threads.
+// launch configuration.  EB = elements per CTA tile (a power of two, the smem
+// and payload lane width); chosen per (shape, order) from the B200 sweeps in
+// profiles/ (sk_tune.h), or forced with -DSK_EB_FIXED=<n> for tuning builds.
 template <int S, int P>
 struct Mode {
   using Dm = Dims<S, P>;
-  static constexpr bool IL = 3 * Dm::NQ * 16 * 8 <= 100 * 1024;
-  static constexpr int PW = IL ? 16 : 1;  // payload lane width, shared by every op of (S, P)
+  static constexpr int smem_bytes(int eb) {
+    return 3 * Dm::Q0 * Dm::Q1 * (eb >= 16 ? Dm::Q2 : (Dm::Q2 | 1)) * eb * 8;
+  }
+  static constexpr int fit(int eb, int budget) {
+    return (eb <= 1 || smem_bytes(eb) <= budget) ? eb : fit(eb / 2, budget);
+  }
+  static constexpr int EB = tuned_eb(S, P) > 0 ? fit(tuned_eb(S, P), 200 * 1024) : fit(16, 100 * 1024);
+  static constexpr int PW = EB;  // payload lane width, shared by every op of (S, P)
 };
 
 template <int S, int P, int OP>
 struct Cfg {
   using Dm = Dims<S, P>;
-  static constexpr bool IL = Mode<S, P>::IL;
+  static constexpr int EB = Mode<S, P>::EB;
   static constexpr int PW = Mode<S, P>::PW;
   static constexpr int planes = (OP == OP_HELM || OP == OP_PDERIV || OP == OP_IPDERIV) ? 3 : 2;
-  static constexpr int items =
-      cmax(cmax(cmax(Dm::Q1 * Dm::Q2, Dm::Q0 * Dm::Q2), cmax(Dm::Q0 * Dm::Q1, Dm::P1 * Dm::P1)), Dm::NPAIR);
-  static constexpr int ES_pe = planes * Dm::Q0 * Dm::Q1 * (Dm::Q2 | 1);
-  static constexpr int eb_thr = cmax(1, (256 + items / 2) / items);
-  static constexpr int eb_smem = cmax(1, (96 * 1024) / (ES_pe * 8));
-  static constexpr int EB = IL ? 16 : (eb_thr < eb_smem ? eb_thr : eb_smem);
-  using L = Lay<S, P, planes, IL, EB>;
-  static constexpr int NT0 = ((EB * items + 31) / 32) * 32;
-  static constexpr int NT = NT0 > 512 ? 512 : NT0;
+  static constexpr int items = cmax(cmax(cmax(Dm::Q1 * Dm::Q2, Dm::Q0 * Dm::Q2), cmax(Dm::Q0 * Dm::Q1, Dm::P1 * Dm::P1)),
+                                    cmax(Dm::NPAIR, Dm::P1 * Dm::Q2));
+  using L = Lay<S, P, planes, EB>;
+  static constexpr int NT0 = ((EB * items / tuned_nt_div(S, P) + 31) / 32) * 32;
+  static constexpr int NT = NT0 > 512 ? 512 : (NT0 < 64 ? 64 : NT0);
   static constexpr int SMEM = L::SMEM_DOUBLES * 8;
+  // __launch_bounds__ min blocks: 1, or the CTAs per SM that shared memory
+  // allows (forces ptxas to fit the registers; tuned, as it can spill)
+  static constexpr int MINB = (OP == OP_HELM && tuned_minb(S, P))
+                                  ? cmax(1, cmin(cmin(4, (220 * 1024) / (SMEM + 1024)), 2048 / NT))
+                                  : 1;
 };
 
 // ---------------------------------------------------------------------------
@@ -101,6 +108,12 @@ void fill_gtab(const HostBasis& hb, double* g) {
   using L = GLayout<S, P>;
   using X = GExt<S, P>;
   std::memset(g, 0, sizeof(double) * X::SIZE);
+  if constexpr (S == TET) {
+    for (int p = 0; p < Dm::P1; ++p) {
+      std::memcpy(g + L::B1 + wfam_off(Dm::Q1, Dm::P1, p), hb.b1[p].data(), sizeof(double) * hb.b1[p].size());
+      std::memcpy(g + L::DB1 + wfam_off(Dm::Q1, Dm::P1, p), hb.db1[p].data(), sizeof(double) * hb.db1[p].size());
+    }
+  }
   if constexpr (S != HEX) {
     for (int m = 0; m < Dm::P1; ++m) {
       std::memcpy(g + L::C2 + wfam_off(Dm::Q2, Dm::P1, m), hb.c2[m].data(), sizeof(double) * hb.c2[m].size());
@@ -160,7 +173,7 @@ static void ensure_smem(K kernel, int bytes) {
 template <int S, int P, int OP, class Op>
 static int go(const OpArgs<S, P>& a, const LaunchReq& r, int gy, void* stream) {
   using C = Cfg<S, P, OP>;
-  static_assert(!C::IL || C::EB == C::PW, "IL tiles must align with payload lanes");
+  static_assert(C::EB == C::PW, "tiles must align with payload lanes");
   static std::once_flag once;  // one per kernel instantiation
   static int resident = 1;
   std::call_once(once, [] {
@@ -201,36 +214,38 @@ int launch(int op, const LaunchReq& r, void* stream) {
     case OP_HELM: {
       using C = Cfg<S, P, OP_HELM>;
       if (def) {
-        if (r.lam != 0.0) return go<S, P, OP_HELM, k_helm<S, P, typename C::L, C::NT, C::PW, GEO_DEFORMED, true>>(a, r, r.ncomp, stream);
-        return go<S, P, OP_HELM, k_helm<S, P, typename C::L, C::NT, C::PW, GEO_DEFORMED, false>>(a, r, r.ncomp, stream);
+        if (r.lam != 0.0) return go<S, P, OP_HELM, k_helm<S, P, typename C::L, C::NT, C::PW, GEO_DEFORMED, true, C::MINB>>(a, r, r.ncomp, stream);
+        return go<S, P, OP_HELM, k_helm<S, P, typename C::L, C::NT, C::PW, GEO_DEFORMED, false, C::MINB>>(a, r, r.ncomp, stream);
       }
-      if (r.lam != 0.0) return go<S, P, OP_HELM, k_helm<S, P, typename C::L, C::NT, C::PW, GEO_REGULAR, true>>(a, r, r.ncomp, stream);
-      return go<S, P, OP_HELM, k_helm<S, P, typename C::L, C::NT, C::PW, GEO_REGULAR, false>>(a, r, r.ncomp, stream);
+      if (r.lam != 0.0) return go<S, P, OP_HELM, k_helm<S, P, typename C::L, C::NT, C::PW, GEO_REGULAR, true, C::MINB>>(a, r, r.ncomp, stream);
+      return go<S, P, OP_HELM, k_helm<S, P, typename C::L, C::NT, C::PW, GEO_REGULAR, false, C::MINB>>(a, r, r.ncomp, stream);
     }
+#ifndef SK_ONLY_HELM
     case OP_MASS: {
       using C = Cfg<S, P, OP_MASS>;
-      if (def) return go<S, P, OP_MASS, k_mass<S, P, typename C::L, C::NT, C::PW, GEO_DEFORMED>>(a, r, r.ncomp, stream);
-      return go<S, P, OP_MASS, k_mass<S, P, typename C::L, C::NT, C::PW, GEO_REGULAR>>(a, r, r.ncomp, stream);
+      if (def) return go<S, P, OP_MASS, k_mass<S, P, typename C::L, C::NT, C::PW, GEO_DEFORMED, C::MINB>>(a, r, r.ncomp, stream);
+      return go<S, P, OP_MASS, k_mass<S, P, typename C::L, C::NT, C::PW, GEO_REGULAR, C::MINB>>(a, r, r.ncomp, stream);
     }
     case OP_BWD: {
       using C = Cfg<S, P, OP_BWD>;
-      return go<S, P, OP_BWD, k_bwd<S, P, typename C::L, C::NT>>(a, r, r.ncomp, stream);
+      return go<S, P, OP_BWD, k_bwd<S, P, typename C::L, C::NT, C::MINB>>(a, r, r.ncomp, stream);
     }
     case OP_IPROD: {
       using C = Cfg<S, P, OP_IPROD>;
-      if (def) return go<S, P, OP_IPROD, k_iprod<S, P, typename C::L, C::NT, C::PW, GEO_DEFORMED>>(a, r, r.ncomp, stream);
-      return go<S, P, OP_IPROD, k_iprod<S, P, typename C::L, C::NT, C::PW, GEO_REGULAR>>(a, r, r.ncomp, stream);
+      if (def) return go<S, P, OP_IPROD, k_iprod<S, P, typename C::L, C::NT, C::PW, GEO_DEFORMED, C::MINB>>(a, r, r.ncomp, stream);
+      return go<S, P, OP_IPROD, k_iprod<S, P, typename C::L, C::NT, C::PW, GEO_REGULAR, C::MINB>>(a, r, r.ncomp, stream);
     }
     case OP_PDERIV: {
       using C = Cfg<S, P, OP_PDERIV>;
-      if (def) return go<S, P, OP_PDERIV, k_pderiv<S, P, typename C::L, C::NT, C::PW, GEO_DEFORMED>>(a, r, 1, stream);
-      return go<S, P, OP_PDERIV, k_pderiv<S, P, typename C::L, C::NT, C::PW, GEO_REGULAR>>(a, r, 1, stream);
+      if (def) return go<S, P, OP_PDERIV, k_pderiv<S, P, typename C::L, C::NT, C::PW, GEO_DEFORMED, C::MINB>>(a, r, 1, stream);
+      return go<S, P, OP_PDERIV, k_pderiv<S, P, typename C::L, C::NT, C::PW, GEO_REGULAR, C::MINB>>(a, r, 1, stream);
     }
     case OP_IPDERIV: {
       using C = Cfg<S, P, OP_IPDERIV>;
-      if (def) return go<S, P, OP_IPDERIV, k_ipderiv<S, P, typename C::L, C::NT, C::PW, GEO_DEFORMED>>(a, r, 1, stream);
-      return go<S, P, OP_IPDERIV, k_ipderiv<S, P, typename C::L, C::NT, C::PW, GEO_REGULAR>>(a, r, 1, stream);
+      if (def) return go<S, P, OP_IPDERIV, k_ipderiv<S, P, typename C::L, C::NT, C::PW, GEO_DEFORMED, C::MINB>>(a, r, 1, stream);
+      return go<S, P, OP_IPDERIV, k_ipderiv<S, P, typename C::L, C::NT, C::PW, GEO_REGULAR, C::MINB>>(a, r, 1, stream);
     }
+#endif
   }
   return (int)cudaErrorInvalidValue;
 }

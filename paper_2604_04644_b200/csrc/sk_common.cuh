@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cstdint>
+#include <type_traits>
 
 #include "sk_shapes.hpp"
 
@@ -37,34 +38,27 @@ struct Dims {
 
 // Shared-memory layout of the per-element work arrays.  Each element owns
 // NPL "planes" of quad-point-sized arrays, addressed by a plane-relative
-// index idx = plane*PLANE + (i*Q1 + j)*S2 + k (k-row stride S2).
-//
-//  IL (interleaved, low orders): the EB = 16 elements of a tile are the
-//    fastest smem dimension, sm[idx*16 + e], and work items map
-//    e = lane % 16.  Every half-warp then reads/writes 16 consecutive
-//    doubles whatever the sweep direction: bank-conflict free by
-//    construction (the shared-memory analogue of the reference's SIMD lane
-//    interleave, field_block.py:205-214).
-//  per-element (high orders, where 16 elements do not fit): element-major
-//    sm[e*ES + idx] with an odd k-row stride so that line walks are
-//    conflict free within an element.
-template <int S, int P, int NPL, bool IL_, int EB_>
+// index idx = plane*PLANE + (i*Q1 + j)*S2 + k (k-row stride S2).  The EB
+// elements of a tile are the fastest smem dimension, sm[idx*EB + e], and work
+// items map e = item % EB (the shared-memory analogue of the reference's
+// SIMD lane interleave, field_block.py:205-214).  A half-warp then covers
+// 16/EB consecutive passive indices at the same EB lanes: with EB = 16 it
+// reads 16 consecutive doubles whatever the sweep direction, and for
+// EB < 16 an odd row stride S2 keeps consecutive passive indices in
+// distinct bank groups, so every sweep is (nearly) bank-conflict free.
+template <int S, int P, int NPL, int EB_>
 struct Lay {
   using Dm = Dims<S, P>;
-  static constexpr bool IL = IL_;
   static constexpr int EB = EB_;
-  static constexpr int S2 = IL ? Dm::Q2 : (Dm::Q2 | 1);
+  static constexpr int S2 = EB >= 16 ? Dm::Q2 : (Dm::Q2 | 1);
   static constexpr int PLANE = Dm::Q0 * Dm::Q1 * S2;
-  static constexpr int ES = NPL * PLANE;
-  // tile staging area for coefficients (IL only): [mode][EB + 1]
-  static constexpr int XSTR = EB + 1;
-  static constexpr int SMEM_DOUBLES = EB * ES;
-  __device__ static __forceinline__ int at(int e, int idx) {
-    if constexpr (IL)
-      return idx * EB + e;
-    else
-      return e * ES + idx;
-  }
+  // tile staging area for coefficients, [mode][XSTR] from the start of plane
+  // 1: an odd stride keeps the transposing copy conflict free; it must fit
+  // in the planes that are dead while it is live (plane 1 on, >= 2 planes)
+  static constexpr int XSTR = EB >= 8 ? EB + 1 : EB;
+  static constexpr int SMEM_DOUBLES = NPL * PLANE * EB;
+  static_assert(Dm::NM * XSTR <= (NPL - 1) * PLANE * EB, "coefficient staging does not fit");
+  __device__ static __forceinline__ int at(int e, int idx) { return idx * EB + e; }
 };
 
 // offset of the leading-index-p slice in a packed warped family whose slice
@@ -100,12 +94,14 @@ struct GLayout {
   static constexpr int PAIRS = DC2 + Dm::Q2 * Dm::NTRI;  // NPAIR x 4 ints
   static constexpr int REGK = PAIRS + 2 * Dm::NPAIR;     // [6][k][i*Q1+j]: refw,g00,g10,g11,g20,g21
   static constexpr int REFW = REGK + 6 * Dm::NQ;         // [i][j][k] refw
-  static constexpr int SIZE = REFW + Dm::NQ;
+  static constexpr int B1 = REFW + Dm::NQ;               // tet dir-1 family values
+  static constexpr int DB1 = B1 + Dm::Q1 * Dm::NTRI;     // tet dir-1 family derivatives
+  static constexpr int SIZE = DB1 + Dm::Q1 * Dm::NTRI;
 };
 
-// Geometry payload addressing: [E/PW][C][NQ][PW], i.e. PW elements
-// interleaved innermost (PW = 16 for IL kernels: one 128-byte line per
-// point per half-warp), or plain [E][C][NQ] when PW = 1.
+// Geometry payload addressing: [E/PW][C][NQ][PW], i.e. PW = EB elements
+// interleaved innermost, so a half-warp's EB lanes read consecutive
+// doubles; plain [E][C][NQ] when PW = 1.
 template <int PW>
 __device__ __forceinline__ long long pay_base(long long e, int C, int N) {
   if constexpr (PW == 1) {
@@ -129,17 +125,26 @@ __device__ __forceinline__ long long lane_base(long long e, int N, int W) {
   return g * (long long)N * W + (e - g * W);
 }
 
+// call f(std::integral_constant<int, v>) for the runtime value v in [0, N):
+// lets a per-item selector (a warped-family slice index) become a
+// compile-time constant, so its table entries stay uniform DFMA operands
+template <int I, int N, class F>
+__device__ __forceinline__ void dispatch(int v, F&& f) {
+  if constexpr (I < N) {
+    if (v == I) {
+      f(std::integral_constant<int, I>{});
+    } else {
+      dispatch<I + 1, N>(v, f);
+    }
+  }
+}
+
 template <class L, int NPASS, int NT, class F>
 __device__ __forceinline__ void items(F&& f) {
 #pragma unroll 1
   for (int w = threadIdx.x; w < L::EB * NPASS; w += NT) {
-    if constexpr (L::IL) {
-      const int ps = w / L::EB;
-      f(w - ps * L::EB, ps);
-    } else {
-      const int e = w / NPASS;
-      f(e, w - e * NPASS);
-    }
+    const int ps = w / L::EB;
+    f(w - ps * L::EB, ps);
   }
 }
 

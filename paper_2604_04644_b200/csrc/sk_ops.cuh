@@ -103,7 +103,7 @@ __device__ __forceinline__ void prefetch_field(const double* in, long long cstri
 // (consumed mid-tile, by the metric sweep) and the input field of the tile
 // one resident wave ahead (A.pf_ahead tiles), which a later CTA will load.
 template <class Op, int S, int P>
-__global__ void __launch_bounds__(Op::NT) k_tile(const __grid_constant__ OpArgs<S, P> A) {
+__global__ void __launch_bounds__(Op::NT, Op::MINB) k_tile(const __grid_constant__ OpArgs<S, P> A) {
   extern __shared__ double sm[];
   const long long t = blockIdx.x;
   if (threadIdx.x < 32) {
@@ -115,11 +115,12 @@ __global__ void __launch_bounds__(Op::NT) k_tile(const __grid_constant__ OpArgs<
 }
 
 // ---------------------------------------------------------------------------
-// Helmholtz, collocated: 9 sweeps, 8 CTA barriers (+2 for IL staging)
-template <int S, int P, class L, int NT_, int PW, int GEO, bool LAMW>
+// Helmholtz, collocated: 9 sweeps + coefficient tile staging, 10 CTA barriers
+template <int S, int P, class L, int NT_, int PW, int GEO, bool LAMW, int MINB_>
 struct k_helm {
   static constexpr int NT = NT_;
   static constexpr int EB = L::EB;
+  static constexpr int MINB = MINB_;
   __device__ static void prefetch_geo(const OpArgs<S, P>& A, long long t) {
     const long long e0 = t * EB;
     const long long n = A.E - e0 < EB ? A.E - e0 : EB;
@@ -140,15 +141,13 @@ struct k_helm {
   const Ctx c = make_ctx<L::EB>(tile, A.E, A.Epad, A.W);
   const double* src = A.in + blockIdx.y * A.in_cstride;
   double* dst = A.out + blockIdx.y * A.out_cstride;
-  double* xs = sm + L::EB * PL;  // plane 1: coefficient staging (IL)
+  double* xs = sm + L::EB * PL;  // plane 1: coefficient tile staging
 
-  if constexpr (L::IL) {
-    load_tile<L, NM, NT>(src, c, xs);
-    __syncthreads();
-  }
-  stage_f1<S, P, L, NT, TAo>(A.B, A.gtab, CoefIn<L, NM>{src, xs, &c}, sm);
+  load_tile<L, NM, NT>(src, c, xs);
   __syncthreads();
-  stage_f2<S, P, L, NT, TAo, TBo>(A.B, sm);
+  stage_f1<S, P, L, NT, TAo>(A.B, A.gtab, CoefIn<L, NM>{xs}, sm);
+  __syncthreads();
+  stage_f2<S, P, L, NT, TAo, TBo>(A.B, A.gtab, sm);
   __syncthreads();
   // F3 + D0: u along i, v0 = D0 u
   items<L, Q1 * Q2, NT>([&](int e, int ps) {
@@ -282,13 +281,11 @@ struct k_helm {
     for (int p = 0; p < P1; ++p) sm[L::at(e, TBo + (p * Q1 + j) * S2 + k)] = t[p];
   });
   __syncthreads();
-  stage_b2<S, P, L, NT, TAo, TBo>(A.B, sm);
+  stage_b2<S, P, L, NT, TAo, TBo>(A.B, A.gtab, sm);
   __syncthreads();
-  stage_b3<S, P, L, NT, TAo>(A.B, A.gtab, CoefOut<L, NM>{dst, xs, &c}, sm);
-  if constexpr (L::IL) {
-    __syncthreads();
-    store_tile<L, NM, NT>(dst, c, xs);
-  }
+  stage_b3<S, P, L, NT, TAo>(A.B, A.gtab, CoefOut<L, NM>{xs}, sm);
+  __syncthreads();
+  store_tile<L, NM, NT>(dst, c, xs);
   }
 };
 
@@ -305,10 +302,11 @@ __device__ __forceinline__ double w_at(const OpArgs<S, P>& A, long long eg, bool
 
 // ---------------------------------------------------------------------------
 // Mass: F1, F2, fused (B, W, B^T) along dir 0, B2, B3
-template <int S, int P, class L, int NT_, int PW, int GEO>
+template <int S, int P, class L, int NT_, int PW, int GEO, int MINB_>
 struct k_mass {
   static constexpr int NT = NT_;
   static constexpr int EB = L::EB;
+  static constexpr int MINB = MINB_;
   __device__ static void prefetch_geo(const OpArgs<S, P>& A, long long t) {
     const long long e0 = t * EB;
     const long long n = A.E - e0 < EB ? A.E - e0 : EB;
@@ -329,13 +327,11 @@ struct k_mass {
   const double* src = A.in + blockIdx.y * A.in_cstride;
   double* dst = A.out + blockIdx.y * A.out_cstride;
   double* xs = sm + L::EB * PL;  // plane 1 (TB): staging before F2 and after B2
-  if constexpr (L::IL) {
-    load_tile<L, NM, NT>(src, c, xs);
-    __syncthreads();
-  }
-  stage_f1<S, P, L, NT, TAo>(A.B, A.gtab, CoefIn<L, NM>{src, xs, &c}, sm);
+  load_tile<L, NM, NT>(src, c, xs);
   __syncthreads();
-  stage_f2<S, P, L, NT, TAo, TBo>(A.B, sm);
+  stage_f1<S, P, L, NT, TAo>(A.B, A.gtab, CoefIn<L, NM>{xs}, sm);
+  __syncthreads();
+  stage_f2<S, P, L, NT, TAo, TBo>(A.B, A.gtab, sm);
   __syncthreads();
   items<L, Q1 * Q2, NT>([&](int e, int ps) {
     const int j = ps / Q2, k = ps - j * Q2;
@@ -352,22 +348,21 @@ struct k_mass {
     for (int p = 0; p < P1; ++p) sm[L::at(e, TBo + (p * Q1 + j) * S2 + k)] = x[p];
   });
   __syncthreads();
-  stage_b2<S, P, L, NT, TAo, TBo>(A.B, sm);
+  stage_b2<S, P, L, NT, TAo, TBo>(A.B, A.gtab, sm);
   __syncthreads();
-  stage_b3<S, P, L, NT, TAo>(A.B, A.gtab, CoefOut<L, NM>{dst, xs, &c}, sm);
-  if constexpr (L::IL) {
-    __syncthreads();
-    store_tile<L, NM, NT>(dst, c, xs);
-  }
+  stage_b3<S, P, L, NT, TAo>(A.B, A.gtab, CoefOut<L, NM>{xs}, sm);
+  __syncthreads();
+  store_tile<L, NM, NT>(dst, c, xs);
   }
 };
 
 // ---------------------------------------------------------------------------
 // BwdTrans: coefficients -> quadrature values
-template <int S, int P, class L, int NT_>
+template <int S, int P, class L, int NT_, int MINB_>
 struct k_bwd {
   static constexpr int NT = NT_;
   static constexpr int EB = L::EB;
+  static constexpr int MINB = MINB_;
   __device__ static void prefetch_geo(const OpArgs<S, P>& A, long long t) {
     const long long e0 = t * EB;
     const long long n = A.E - e0 < EB ? A.E - e0 : EB;
@@ -388,13 +383,11 @@ struct k_bwd {
   const double* src = A.in + blockIdx.y * A.in_cstride;
   double* dst = A.out + blockIdx.y * A.out_cstride;
   double* xs = sm + L::EB * PL;
-  if constexpr (L::IL) {
-    load_tile<L, NM, NT>(src, c, xs);
-    __syncthreads();
-  }
-  stage_f1<S, P, L, NT, TAo>(A.B, A.gtab, CoefIn<L, NM>{src, xs, &c}, sm);
+  load_tile<L, NM, NT>(src, c, xs);
   __syncthreads();
-  stage_f2<S, P, L, NT, TAo, TBo>(A.B, sm);
+  stage_f1<S, P, L, NT, TAo>(A.B, A.gtab, CoefIn<L, NM>{xs}, sm);
+  __syncthreads();
+  stage_f2<S, P, L, NT, TAo, TBo>(A.B, A.gtab, sm);
   __syncthreads();
   items<L, Q1 * Q2, NT>([&](int e, int ps) {
     const int j = ps / Q2, k = ps - j * Q2;
@@ -414,10 +407,11 @@ struct k_bwd {
 
 // ---------------------------------------------------------------------------
 // IProductWRTBase: quadrature values -> coefficients, B^T W u
-template <int S, int P, class L, int NT_, int PW, int GEO>
+template <int S, int P, class L, int NT_, int PW, int GEO, int MINB_>
 struct k_iprod {
   static constexpr int NT = NT_;
   static constexpr int EB = L::EB;
+  static constexpr int MINB = MINB_;
   __device__ static void prefetch_geo(const OpArgs<S, P>& A, long long t) {
     const long long e0 = t * EB;
     const long long n = A.E - e0 < EB ? A.E - e0 : EB;
@@ -454,22 +448,21 @@ struct k_iprod {
     for (int p = 0; p < P1; ++p) sm[L::at(e, TBo + (p * Q1 + j) * S2 + k)] = t[p];
   });
   __syncthreads();
-  stage_b2<S, P, L, NT, TAo, TBo>(A.B, sm);
+  stage_b2<S, P, L, NT, TAo, TBo>(A.B, A.gtab, sm);
   __syncthreads();
-  stage_b3<S, P, L, NT, TAo>(A.B, A.gtab, CoefOut<L, NM>{dst, xs, &c}, sm);
-  if constexpr (L::IL) {
-    __syncthreads();
-    store_tile<L, NM, NT>(dst, c, xs);
-  }
+  stage_b3<S, P, L, NT, TAo>(A.B, A.gtab, CoefOut<L, NM>{xs}, sm);
+  __syncthreads();
+  store_tile<L, NM, NT>(dst, c, xs);
   }
 };
 
 // ---------------------------------------------------------------------------
 // PhysDeriv: u (1 component) -> du/dx_j (3 components)
-template <int S, int P, class L, int NT_, int PW, int GEO>
+template <int S, int P, class L, int NT_, int PW, int GEO, int MINB_>
 struct k_pderiv {
   static constexpr int NT = NT_;
   static constexpr int EB = L::EB;
+  static constexpr int MINB = MINB_;
   __device__ static void prefetch_geo(const OpArgs<S, P>& A, long long t) {
     const long long e0 = t * EB;
     const long long n = A.E - e0 < EB ? A.E - e0 : EB;
@@ -563,10 +556,11 @@ struct k_pderiv {
 
 // ---------------------------------------------------------------------------
 // IProductWRTDerivBase: 3 phys components -> 1 coefficient component
-template <int S, int P, class L, int NT_, int PW, int GEO>
+template <int S, int P, class L, int NT_, int PW, int GEO, int MINB_>
 struct k_ipderiv {
   static constexpr int NT = NT_;
   static constexpr int EB = L::EB;
+  static constexpr int MINB = MINB_;
   __device__ static void prefetch_geo(const OpArgs<S, P>& A, long long t) {
     const long long e0 = t * EB;
     const long long n = A.E - e0 < EB ? A.E - e0 : EB;
@@ -634,13 +628,11 @@ struct k_ipderiv {
     for (int p = 0; p < P1; ++p) sm[L::at(e, TBo + (p * Q1 + j) * S2 + k)] = t[p];
   });
   __syncthreads();
-  stage_b2<S, P, L, NT, TAo, TBo>(A.B, sm);
+  stage_b2<S, P, L, NT, TAo, TBo>(A.B, A.gtab, sm);
   __syncthreads();
-  stage_b3<S, P, L, NT, TAo>(A.B, A.gtab, CoefOut<L, NM>{A.out, xs, &c}, sm);
-  if constexpr (L::IL) {
-    __syncthreads();
-    store_tile<L, NM, NT>(A.out, c, xs);
-  }
+  stage_b3<S, P, L, NT, TAo>(A.B, A.gtab, CoefOut<L, NM>{xs}, sm);
+  __syncthreads();
+  store_tile<L, NM, NT>(A.out, c, xs);
   }
 };
 

@@ -14,8 +14,8 @@
 // collapsed-vertex rank-one corrections folded into the line passes).
 //
 // Per-element work arrays, plane-relative index (see Lay in sk_common.cuh):
-//   plane 0: U  [i][j][k]                       / TA [p][q][k], Y row
-//   plane 1: V0 [i][j][k]  (IL: coefficient staging [mode][EB+1])
+//   plane 0: U  [i][j][k]                       / TA [p][q][k], Y and S rows
+//   plane 1: V0 [i][j][k]   / coefficient tile staging [mode][XSTR]
 //   plane 2: V1 [i][j][k]                       / TB [p][j][k]
 // TA/TB are live only between the sweeps that produce and consume them.
 #pragma once
@@ -24,7 +24,7 @@
 
 namespace sk {
 
-// ---- coefficient tile staging (IL layouts) ---------------------------------
+// ---- coefficient tile staging ----------------------------------------------
 // xs[m * XSTR + e] <-> field value of mode m of element e0 + e; iteration order
 // follows the field layout so that consecutive threads touch consecutive
 // global addresses.
@@ -68,35 +68,17 @@ __device__ __forceinline__ void store_tile(double* __restrict__ dst, const Ctx& 
   }
 }
 
-// coefficient m of tile element e: staged (IL) or straight from the field
+// coefficient m of tile element e from / to the staged tile
 template <class L, int NM>
 struct CoefIn {
-  const double* __restrict__ src;
   const double* xs;
-  const Ctx* c;
-  __device__ __forceinline__ double operator()(int e, int m) const {
-    if constexpr (L::IL) {
-      return xs[m * L::XSTR + e];
-    } else {
-      const long long eg = c->e0 + e;
-      return eg < c->E ? __ldg(src + lane_base(eg, NM, c->W) + (long long)m * c->W) : 0.0;
-    }
-  }
+  __device__ __forceinline__ double operator()(int e, int m) const { return xs[m * L::XSTR + e]; }
 };
 
 template <class L, int NM>
 struct CoefOut {
-  double* __restrict__ dst;
   double* xs;
-  const Ctx* c;
-  __device__ __forceinline__ void operator()(int e, int m, double v) const {
-    if constexpr (L::IL) {
-      xs[m * L::XSTR + e] = v;
-    } else {
-      const long long eg = c->e0 + e;
-      if (eg < c->Epad) dst[lane_base(eg, NM, c->W) + (long long)m * c->W] = v;
-    }
-  }
+  __device__ __forceinline__ void operator()(int e, int m, double v) const { xs[m * L::XSTR + e] = v; }
 };
 
 // ---- F1: r -> k.  TA[p][q][k] = sum_r C_(p,q)[k][r] uhat[p,q,r] ----------
@@ -175,7 +157,7 @@ __device__ __forceinline__ void stage_f1(const FwdTab<S, P>& B, const double* __
 
 // ---- F2: q -> j.  TB[p][j][k] = sum_q B_p[j][q] TA[p][q][k] ---------------
 template <int S, int P, class L, int NT, int TAo, int TBo>
-__device__ __forceinline__ void stage_f2(const FwdTab<S, P>& B, double* sm) {
+__device__ __forceinline__ void stage_f2(const FwdTab<S, P>& B, const double* __restrict__ gtab, double* sm) {
   using Dm = Dims<S, P>;
   constexpr int P1 = Dm::P1, Q1 = Dm::Q1, Q2 = Dm::Q2, S2 = L::S2;
   if constexpr (S != TET) {
@@ -200,28 +182,33 @@ __device__ __forceinline__ void stage_f2(const FwdTab<S, P>& B, double* sm) {
       }
     });
   } else {
-    // tet: item = (e, k), p unrolled so b1[p] is uniform (operators.py:209-245)
-    items<L, Q2, NT>([&](int e, int k) {
-      const double y = sm[L::at(e, TAo + P1 * P1 * S2 + k)];
-      const double x01 = sm[L::at(e, TAo + (0 * P1 + 1) * S2 + k)];
+    // tet: item = (e, k, p) so that all P1 slices run in parallel; the slice
+    // index is dispatched to a compile-time constant so b1[p] stays a
+    // uniform operand (operators.py:209-245)
+    items<L, Q2 * P1, NT>([&](int e, int ps) {
+      const int pr = ps / Q2, k = ps - pr * Q2;
+      dispatch<0, P1>(pr, [&](auto pc) {
+        constexpr int p = decltype(pc)::value;
+        constexpr int n = P1 - p;
+        constexpr int bo = wfam_off(Q1, P1, p);
+        double x[n];
 #pragma unroll
-      for (int p = 0; p < P1; ++p) {
-        const int n = P1 - p;
-        const int bo = wfam_off(Q1, P1, p);
-        double x[P1];
-#pragma unroll
-        for (int q = 0; q < P1; ++q) x[q] = q < n ? sm[L::at(e, TAo + (p * P1 + q) * S2 + k)] : 0.0;
+        for (int q = 0; q < n; ++q) x[q] = sm[L::at(e, TAo + (p * P1 + q) * S2 + k)];
+        double y = 0.0, x01 = 0.0;
+        if constexpr (p <= 1) {
+          y = sm[L::at(e, TAo + P1 * P1 * S2 + k)];
+          x01 = sm[L::at(e, TAo + (0 * P1 + 1) * S2 + k)];
+        }
 #pragma unroll
         for (int j = 0; j < Q1; ++j) {
           double s = B.b1[bo + j * n] * x[0];
 #pragma unroll
-          for (int q = 1; q < P1; ++q)
-            if (q < n) s = fma(B.b1[bo + j * n + q], x[q], s);
-          if (p == 1) s = fma(B.b1[j * P1 + 1], x01, s) + y;  // edge (0,1,r) + apex shares
-          if (p == 0) s = fma(B.b1[j * P1 + 1], y, s);
+          for (int q = 1; q < n; ++q) s = fma(B.b1[bo + j * n + q], x[q], s);
+          if constexpr (p == 1) s = fma(B.b1[j * P1 + 1], x01, s) + y;  // edge (0,1,r) + apex shares
+          if constexpr (p == 0) s = fma(B.b1[j * P1 + 1], y, s);
           sm[L::at(e, TBo + (p * Q1 + j) * S2 + k)] = s;
         }
-      }
+      });
     });
   }
 }
@@ -280,7 +267,7 @@ __device__ __forceinline__ void line_dt_acc(const double* D, const double (&w)[Q
 
 // ---- B2: j -> q.  TA[p][q][k] = sum_j B_p[j][q] TB[p][j][k] ---------------
 template <int S, int P, class L, int NT, int TAo, int TBo>
-__device__ __forceinline__ void stage_b2(const FwdTab<S, P>& B, double* sm) {
+__device__ __forceinline__ void stage_b2(const FwdTab<S, P>& B, const double* __restrict__ gtab, double* sm) {
   using Dm = Dims<S, P>;
   constexpr int P1 = Dm::P1, Q1 = Dm::Q1, Q2 = Dm::Q2, S2 = L::S2;
   if constexpr (S != TET) {
@@ -306,39 +293,37 @@ __device__ __forceinline__ void stage_b2(const FwdTab<S, P>& B, double* sm) {
       }
     });
   } else {
-    items<L, Q2, NT>([&](int e, int k) {
-      double t01 = 0.0;
-#pragma unroll
-      for (int p = 0; p < P1; ++p) {
-        const int n = P1 - p;
-        const int bo = wfam_off(Q1, P1, p);
+    // tet: item = (e, k, p), p dispatched to a compile-time constant.  The
+    // collapsed-edge share S[k] = sum_j b1[0][j][1] TB[1][j][k] and the apex
+    // share Y[k] = sum_j TB[1][j][k] go to two spare rows; B3 adds them to
+    // modes (0,1,r) and (0,0,1) (operators.py:263-271).
+    items<L, Q2 * P1, NT>([&](int e, int ps) {
+      const int pr = ps / Q2, k = ps - pr * Q2;
+      dispatch<0, P1>(pr, [&](auto pc) {
+        constexpr int p = decltype(pc)::value;
+        constexpr int n = P1 - p;
+        constexpr int bo = wfam_off(Q1, P1, p);
         double x[Q1];
 #pragma unroll
         for (int j = 0; j < Q1; ++j) x[j] = sm[L::at(e, TBo + (p * Q1 + j) * S2 + k)];
 #pragma unroll
-        for (int q = 0; q < P1; ++q) {
-          if (q < n) {
-            double s = B.b1[bo + q] * x[0];
+        for (int q = 0; q < n; ++q) {
+          double s = B.b1[bo + q] * x[0];
 #pragma unroll
-            for (int j = 1; j < Q1; ++j) s = fma(B.b1[bo + j * n + q], x[j], s);
-            if (p == 0 && q == 1) t01 = s;
-            sm[L::at(e, TAo + (p * P1 + q) * S2 + k)] = s;
-          }
+          for (int j = 1; j < Q1; ++j) s = fma(B.b1[bo + j * n + q], x[j], s);
+          sm[L::at(e, TAo + (p * P1 + q) * S2 + k)] = s;
         }
-        if (p == 1) {
-          // edge (0,1,r) share s = sum_j b1[0][j][1] TB[1][j][k]; apex share
-          // Y[k] = sum_j TB[1][j][k] + sum_j b1[0][j][1] TB[0][j][k]
-          // (operators.py:263-271)
+        if constexpr (p == 1) {
           double s = B.b1[1] * x[0], y = x[0];
 #pragma unroll
           for (int j = 1; j < Q1; ++j) {
             s = fma(B.b1[j * P1 + 1], x[j], s);
             y += x[j];
           }
-          sm[L::at(e, TAo + (0 * P1 + 1) * S2 + k)] = t01 + s;
-          sm[L::at(e, TAo + P1 * P1 * S2 + k)] = y + t01;
+          sm[L::at(e, TAo + P1 * P1 * S2 + k)] = y;
+          sm[L::at(e, TAo + (P1 * P1 + 1) * S2 + k)] = s;
         }
-      }
+      });
     });
   }
 }
@@ -402,13 +387,18 @@ __device__ __forceinline__ void stage_b3(const FwdTab<S, P>& B, const double* __
       double x[Q2];
 #pragma unroll
       for (int k = 0; k < Q2; ++k) x[k] = sm[L::at(e, TAo + (pr.x * P1 + pr.y) * S2 + k)];
+      if constexpr (S == TET) {
+        if (pr.x == 0 && pr.y == 1) {
+#pragma unroll
+          for (int k = 0; k < Q2; ++k) x[k] += sm[L::at(e, TAo + (P1 * P1 + 1) * S2 + k)];
+        }
+      }
       double apex = 0.0;
       if (pr.x == 0 && pr.y == 0) {
         const double* t0 = gtab + GLayout<S, P>::C2;
 #pragma unroll
         for (int k = 0; k < Q2; ++k) {
-          double y = sm[L::at(e, TAo + P1 * P1 * S2 + k)];
-          if constexpr (S == PYR) y += sm[L::at(e, TAo + (0 * P1 + 1) * S2 + k)];
+          const double y = sm[L::at(e, TAo + P1 * P1 * S2 + k)] + sm[L::at(e, TAo + (0 * P1 + 1) * S2 + k)];
           apex = fma(__ldg(t0 + k * P1 + 1), y, apex);
         }
       }
