@@ -42,9 +42,10 @@ enum { SK_SHAPE_QUAD = 0, SK_SHAPE_TRI = 1, SK_SHAPE_HEX = 2,
 /* GeometryClass (geometry.py:35-39) */
 enum { SK_GEO_REGULAR = 0, SK_GEO_DEFORMED = 1 };
 /* payload kinds: what Block.payload(...) feeds each operator family */
-enum { SK_PAYLOAD_HELMHOLTZ = 0,  /* lam + wj ("lam","wj"/"jac" keys)      */
-       SK_PAYLOAD_W = 1,          /* W diagonal ("wj" / "jac" keys)        */
-       SK_PAYLOAD_DERIV = 2 };    /* inverse Jacobian ("dxi" key)          */
+enum { SK_PAYLOAD_HELMHOLTZ = 0,      /* lam + wj ("lam","wj"/"jac" keys), collocated form */
+       SK_PAYLOAD_W = 1,              /* W diagonal ("wj" / "jac" keys)                    */
+       SK_PAYLOAD_DERIV = 2,          /* inverse Jacobian ("dxi" key)                      */
+       SK_PAYLOAD_HELMHOLTZ_NC = 3 }; /* lam + wj, point order of the non-collocated form  */
 /* Helmholtz formulations (operators.py:702-721) */
 enum { SK_FORM_COLL = 0, SK_FORM_NONCOLL = 1 };
 enum { SK_OK = 0, SK_ERR_STATE = 1, SK_ERR_UNSUPPORTED = 2, SK_ERR_ARG = 3, SK_ERR_CUDA = 4 };
@@ -107,8 +108,8 @@ int sk_iproduct_wrt_deriv_base(const sk_basis* b, int geo_class, int64_t E, int 
 int sk_mass_apply(const sk_basis* b, int geo_class, int64_t E, int W, int ncomp,
                   const double* uhat, const double* wpay, double* out, void* stream);
 /* helmholtz_apply[_coll|_noncoll] (operators.py:636-721); payload kind
- * HELMHOLTZ.  lam == 0 is the stiffness operator and skips the
- * W stream. */
+ * HELMHOLTZ for SK_FORM_COLL, HELMHOLTZ_NC for SK_FORM_NONCOLL.  lam == 0 is
+ * the stiffness operator and skips the W stream. */
 int sk_helmholtz_apply(const sk_basis* b, int geo_class, int form, int64_t E, int W, int ncomp,
                        const double* uhat, const double* hpay, double lam, double* out, void* stream);
 
@@ -119,7 +120,7 @@ int64_t sk_launch_count(void);
 const char* sk_last_error(void);
 /* Kernel launch configuration chosen for an operator: out[0]=elements per
  * CTA, out[1]=threads per CTA, out[2]=dynamic shared bytes. op: 0 helmholtz,
- * 1 mass, 2 bwd, 3 iprod, 4 physderiv, 5 iprod_deriv. */
+ * 1 mass, 2 bwd, 3 iprod, 4 physderiv, 5 iprod_deriv, 6 helmholtz noncoll. */
 int sk_launch_config(const sk_basis* b, int op, int64_t out[3]);
 
 #ifdef __cplusplus

@@ -17,7 +17,7 @@ LIB_PATH = os.environ.get("SK200_LIB") or os.path.join(_HERE, "libsk200.so")
 
 SK_OK, SK_ERR_STATE, SK_ERR_UNSUPPORTED, SK_ERR_ARG, SK_ERR_CUDA = range(5)
 SK_GEO_REGULAR, SK_GEO_DEFORMED = 0, 1
-SK_PAYLOAD_HELMHOLTZ, SK_PAYLOAD_W, SK_PAYLOAD_DERIV = 0, 1, 2
+SK_PAYLOAD_HELMHOLTZ, SK_PAYLOAD_W, SK_PAYLOAD_DERIV, SK_PAYLOAD_HELMHOLTZ_NC = 0, 1, 2, 3
 SK_FORM_COLL, SK_FORM_NONCOLL = 0, 1
 
 #: every exported symbol and its (restype, argtypes)

@@ -111,6 +111,7 @@ int run(sk_basis* b, int op, int geo, long long E, int W, int ncomp, const doubl
   if (st) return st;
   sk::LaunchReq r;
   r.fwd = b->fwd_vals.data();
+  r.fwd_d = b->fwd_ders.data();
   r.dtab = b->dtab.data();
   r.in = in;
   r.out = out;
@@ -194,7 +195,7 @@ int sk_basis_table(const sk_basis* b, const char* name, double* out, int64_t cap
 int sk_payload_size(const sk_basis* b, int geo_class, int kind, int64_t E, int64_t* n) {
   if (!b || !n) return fail(SK_ERR_ARG, "null argument");
   if (geo_class != SK_GEO_REGULAR && geo_class != SK_GEO_DEFORMED) return fail(SK_ERR_ARG, "bad geometry class");
-  if (kind < 0 || kind > 2) return fail(SK_ERR_ARG, "bad payload kind");
+  if (kind < 0 || kind > 3) return fail(SK_ERR_ARG, "bad payload kind");
   if (E < 0) return fail(SK_ERR_ARG, "element count must be nonnegative");
   *n = b->ops->payload_doubles(kind, geo_class) * b->ops->payload_elements(E);
   return SK_OK;
@@ -204,7 +205,7 @@ int sk_payload_pack(const sk_basis* b, int geo_class, int kind, int64_t E, const
                     double* pay, void* stream) {
   if (!b || (E > 0 && (!dxi || !jac || !pay))) return fail(SK_ERR_ARG, "null argument");
   if (geo_class != SK_GEO_REGULAR && geo_class != SK_GEO_DEFORMED) return fail(SK_ERR_ARG, "bad geometry class");
-  if (kind < 0 || kind > 2 || E < 0) return fail(SK_ERR_ARG, "bad payload kind or element count");
+  if (kind < 0 || kind > 3 || E < 0) return fail(SK_ERR_ARG, "bad payload kind or element count");
   int st = SK_OK;
   const double* g = device_gtab(const_cast<sk_basis*>(b), &st);
   if (st) return st;
@@ -251,7 +252,7 @@ int sk_geometry_from_coords(const sk_basis* b, int64_t E, const double* coords, 
 
 int sk_payload_from_params(const sk_basis* b, int kind, int64_t E, const double* params, double* pay,
                            int64_t* n_bad, void* stream) {
-  if (kind < 0 || kind > 2) return fail(SK_ERR_ARG, "bad payload kind");
+  if (kind < 0 || kind > 3) return fail(SK_ERR_ARG, "bad payload kind");
   if (E > 0 && !pay) return fail(SK_ERR_ARG, "null payload");
   return geometry_common(b, 1, E, params, nullptr, nullptr, kind, pay, n_bad, stream);
 }
@@ -304,10 +305,9 @@ int sk_helmholtz_apply(const sk_basis* b, int geo, int form, int64_t E, int W, i
   if (geo != SK_GEO_REGULAR && geo != SK_GEO_DEFORMED) return fail(SK_ERR_ARG, "bad geometry class");
   if (!(lam >= 0.0)) return fail(SK_ERR_ARG, "reaction coefficient must be nonnegative");
   if (form != SK_FORM_COLL && form != SK_FORM_NONCOLL) return fail(SK_ERR_ARG, "unknown Helmholtz form");
-  if (form == SK_FORM_NONCOLL) return fail(SK_ERR_UNSUPPORTED, "non-collocated form not built yet");
   if (int st = check_layout(E, W, ncomp)) return st;
-  return run(const_cast<sk_basis*>(b), sk::OP_HELM, geo, E, W, ncomp, uhat, out, hpay, lam, b->hb.nm, b->hb.nm,
-             stream);
+  return run(const_cast<sk_basis*>(b), form == SK_FORM_NONCOLL ? sk::OP_HELM_NC : sk::OP_HELM, geo, E, W, ncomp, uhat,
+             out, hpay, lam, b->hb.nm, b->hb.nm, stream);
 }
 
 int64_t sk_launch_count(void) { return g_launches.load(); }

@@ -40,7 +40,7 @@ struct Cfg {
   using Dm = Dims<S, P>;
   static constexpr int EB = Mode<S, P>::EB;
   static constexpr int PW = Mode<S, P>::PW;
-  static constexpr int planes = (OP == OP_HELM || OP == OP_PDERIV || OP == OP_IPDERIV) ? 3 : 2;
+  static constexpr int planes = OP == OP_HELM_NC ? 5 : (OP == OP_HELM || OP == OP_PDERIV || OP == OP_IPDERIV) ? 3 : 2;
   static constexpr int items = cmax(cmax(cmax(Dm::Q1 * Dm::Q2, Dm::Q0 * Dm::Q2), cmax(Dm::Q0 * Dm::Q1, Dm::P1 * Dm::P1)),
                                     cmax(Dm::NPAIR, Dm::P1 * Dm::Q2));
   using L = Lay<S, P, planes, EB>;
@@ -170,26 +170,52 @@ static void ensure_smem(K kernel, int bytes) {
   if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
 
-template <int S, int P, int OP, class Op>
-static int go(const OpArgs<S, P>& a, const LaunchReq& r, int gy, void* stream) {
+template <int S, int P, int OP, class Op, class Args>
+static int go(const Args& a, const LaunchReq& r, int gy, void* stream) {
   using C = Cfg<S, P, OP>;
   static_assert(C::EB == C::PW, "tiles must align with payload lanes");
   static std::once_flag once;  // one per kernel instantiation
   static int resident = 1;
   std::call_once(once, [] {
-    ensure_smem(k_tile<Op, S, P>, C::SMEM);
+    ensure_smem(k_tile<Op, Args>, C::SMEM);
     int per_sm = 1, sms = 148, dev = 0;
     cudaGetDevice(&dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tile<Op, S, P>, Op::NT, C::SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tile<Op, Args>, Op::NT, C::SMEM);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     resident = (per_sm > 0 ? per_sm : 1) * sms;
   });
   const long long tiles = (r.Epad + C::EB - 1) / C::EB;
   if (tiles == 0) return 0;
-  OpArgs<S, P>& args = const_cast<OpArgs<S, P>&>(a);
+  Args& args = const_cast<Args&>(a);
   args.pf_ahead = resident / (gy > 0 ? gy : 1);
-  k_tile<Op, S, P><<<dim3((unsigned)tiles, (unsigned)gy), Op::NT, C::SMEM, static_cast<cudaStream_t>(stream)>>>(args);
+  k_tile<Op, Args><<<dim3((unsigned)tiles, (unsigned)gy), Op::NT, C::SMEM, static_cast<cudaStream_t>(stream)>>>(args);
   return (int)cudaGetLastError();
+}
+
+template <int S, int P>
+int launch_nc(const LaunchReq& r, void* stream) {
+  NcArgs<S, P> a;
+  std::memcpy(&a.B, r.fwd, sizeof(a.B));
+  std::memcpy(&a.DB, r.fwd_d, sizeof(a.DB));
+  a.in = r.in;
+  a.out = r.out;
+  a.pay = r.pay;
+  a.gtab = r.gtab;
+  a.E = r.E;
+  a.Epad = r.Epad;
+  a.in_cstride = r.in_cs;
+  a.out_cstride = r.out_cs;
+  a.W = r.W;
+  a.pad_ = 0;
+  a.lam = r.lam;
+  using C = Cfg<S, P, OP_HELM_NC>;
+  using L = typename C::L;
+  if (r.geo == GEO_DEFORMED) {
+    if (r.lam != 0.0) return go<S, P, OP_HELM_NC, k_helm_nc<S, P, L, C::NT, C::PW, GEO_DEFORMED, true, 1>>(a, r, r.ncomp, stream);
+    return go<S, P, OP_HELM_NC, k_helm_nc<S, P, L, C::NT, C::PW, GEO_DEFORMED, false, 1>>(a, r, r.ncomp, stream);
+  }
+  if (r.lam != 0.0) return go<S, P, OP_HELM_NC, k_helm_nc<S, P, L, C::NT, C::PW, GEO_REGULAR, true, 1>>(a, r, r.ncomp, stream);
+  return go<S, P, OP_HELM_NC, k_helm_nc<S, P, L, C::NT, C::PW, GEO_REGULAR, false, 1>>(a, r, r.ncomp, stream);
 }
 
 template <int S, int P>
@@ -211,6 +237,10 @@ int launch(int op, const LaunchReq& r, void* stream) {
   const bool def = r.geo == GEO_DEFORMED;
   using namespace std;
   switch (op) {
+#ifndef SK_ONLY_HELM
+    case OP_HELM_NC:
+      return launch_nc<S, P>(r, stream);
+#endif
     case OP_HELM: {
       using C = Cfg<S, P, OP_HELM>;
       if (def) {
@@ -265,6 +295,7 @@ void config(int op, int64_t out[3]) {
     SK_CFG(OP_IPROD)
     SK_CFG(OP_PDERIV)
     SK_CFG(OP_IPDERIV)
+    SK_CFG(OP_HELM_NC)
 #undef SK_CFG
   }
   out[0] = out[1] = out[2] = 0;
@@ -275,8 +306,8 @@ void config(int op, int64_t out[3]) {
 template <int S, int P>
 long long payload_doubles(int kind, int geo) {
   constexpr long long NQ = Dims<S, P>::NQ;
-  if (geo == GEO_DEFORMED) return kind == 0 ? 7 * NQ : kind == 1 ? NQ : 9 * NQ;
-  return kind == 0 ? 8 : kind == 1 ? 1 : 9;
+  if (geo == GEO_DEFORMED) return (kind == 0 || kind == 3) ? 7 * NQ : kind == 1 ? NQ : 9 * NQ;
+  return (kind == 0 || kind == 3) ? 8 : kind == 1 ? 1 : 9;
 }
 
 template <int S, int P>
@@ -303,7 +334,7 @@ __device__ __forceinline__ void put_point(int kind, long long e, int l, const do
   for (int a = 0; a < 3; ++a)
 #pragma unroll
     for (int b = 0; b < 3; ++b) G[a][b] = gs[3 * a + b];
-  if (kind == 0) {
+  if (kind == 0 || kind == 3) {
     // Lam_ab = (sum_k dxi[a][k] dxi[b][k]) * w|J|  (field_block.py:349-362)
     double L[3][3];
 #pragma unroll
@@ -320,7 +351,7 @@ __device__ __forceinline__ void put_point(int kind, long long e, int l, const do
 #pragma unroll
       for (int n = 0; n < 3; ++n) T[a][n] = L[a][0] * G[0][n] + L[a][1] * G[1][n] + L[a][2] * G[2][n];
     const int mi[6] = {0, 0, 0, 1, 1, 2}, ni[6] = {0, 1, 2, 1, 2, 2};
-    double* o = pay + pay_base<PW>(e, 7, NQ) + km * PW;
+    double* o = pay + pay_base<PW>(e, 7, NQ) + (kind == 3 ? (long long)l : km) * PW;
 #pragma unroll
     for (int c = 0; c < 6; ++c) {
       const int m = mi[c], n = ni[c];
@@ -361,7 +392,7 @@ __global__ void k_pack_regular(int kind, long long E, const double* __restrict__
   constexpr int PW = Mode<S, P>::PW;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < E; e += (long long)gridDim.x * blockDim.x) {
     const double* d = dxi + e * 9;
-    if (kind == 0) {
+    if (kind == 0 || kind == 3) {
       double* o = pay + pay_base<PW>(e, 8, 1);
       const int mi[6] = {0, 0, 0, 1, 1, 2}, ni[6] = {0, 1, 2, 1, 2, 2};
       for (int c = 0; c < 6; ++c) {

@@ -42,6 +42,23 @@ struct OpArgs {
   double lam;
 };
 
+// arguments of the non-collocated Helmholtz: value and derivative tables
+template <int S, int P>
+struct NcArgs {
+  FwdTab<S, P> B;   // psi values
+  FwdTab<S, P> DB;  // psi derivatives (reference dmode tables, shapes.py:555-583)
+  const double* __restrict__ in;
+  double* __restrict__ out;
+  const double* __restrict__ pay;
+  const double* __restrict__ gtab;
+  long long E, Epad;
+  long long in_cstride, out_cstride;
+  long long pf_ahead;
+  int W;
+  int pad_;
+  double lam;
+};
+
 template <int EB>
 __device__ __forceinline__ Ctx make_ctx(long long tile, long long E, long long Epad, int W) {
   Ctx c;
@@ -102,8 +119,8 @@ __device__ __forceinline__ void prefetch_field(const double* in, long long cstri
 // high order).  Warp 0 first prefetches into L2 the tile's geometry payload
 // (consumed mid-tile, by the metric sweep) and the input field of the tile
 // one resident wave ahead (A.pf_ahead tiles), which a later CTA will load.
-template <class Op, int S, int P>
-__global__ void __launch_bounds__(Op::NT, Op::MINB) k_tile(const __grid_constant__ OpArgs<S, P> A) {
+template <class Op, class Args>
+__global__ void __launch_bounds__(Op::NT, Op::MINB) k_tile(const __grid_constant__ Args A) {
   extern __shared__ double sm[];
   const long long t = blockIdx.x;
   if (threadIdx.x < 32) {
@@ -633,6 +650,154 @@ struct k_ipderiv {
   stage_b3<S, P, L, NT, TAo>(A.B, A.gtab, CoefOut<L, NM>{xs}, sm);
   __syncthreads();
   store_tile<L, NM, NT>(A.out, c, xs);
+  }
+};
+
+
+// ---------------------------------------------------------------------------
+// Helmholtz, non-collocated (Alg. 5, operators.py:636-667):
+//   u = B uhat, v_m = (D_m B) uhat by sum factorisation with the derivative
+//   1D tables (dmode), pointwise metric, then
+//   out = sum_m (D_m B)^T w_m + lam B^T W u.
+// Smem planes: 0 TA (F1 values, later R1), 1 TA' (F1 dir-2 derivative,
+// later R2), 2 TB (F2 on TA, later S_A), 3 TB' (F2 dir-1 derivative on TA,
+// later S_B), 4 TB'' (F2 on TA', later S_C); plane 2 doubles as the
+// coefficient staging.  The middle sweep evaluates u, v0, v1, v2, the
+// metric and the three transposed dir-0 contractions in registers, so
+// quadrature-point arrays never touch shared memory.  Deformed geometry uses
+// the standard-point-order payload (kind 3).
+template <int S, int P, class L, int NT_, int PW, int GEO, bool LAMW, int MINB_>
+struct k_helm_nc {
+  static constexpr int NT = NT_;
+  static constexpr int EB = L::EB;
+  static constexpr int MINB = MINB_;
+  using A_t = NcArgs<S, P>;
+  __device__ static void prefetch_geo(const A_t& A, long long t) {
+    const long long e0 = t * EB;
+    const long long n = A.E - e0 < EB ? A.E - e0 : EB;
+    if constexpr (GEO == GEO_DEFORMED) prefetch_payload<PW>(A.pay, e0, n, A.E, LAMW ? 7 : 6, Dims<S, P>::NQ);
+  }
+  __device__ static void prefetch_in(const A_t& A, long long t) {
+    const long long e0 = t * EB;
+    const long long n = A.Epad - e0 < EB ? A.Epad - e0 : EB;
+    prefetch_field<Dims<S, P>::NM>(A.in, A.in_cstride, gridDim.y, e0, n, A.Epad, A.W);
+  }
+  __device__ static void run(const A_t& A, long long tile, double* sm) {
+    using Dm = Dims<S, P>;
+    constexpr int P1 = Dm::P1, Q0 = Dm::Q0, Q1 = Dm::Q1, Q2 = Dm::Q2, S2 = L::S2;
+    constexpr int NQ = Dm::NQ, NM = Dm::NM, PL = L::PLANE;
+    constexpr int TA = 0, TA2 = PL, TB = 2 * PL, TB1 = 3 * PL, TB2 = 4 * PL;
+    const Ctx c = make_ctx<L::EB>(tile, A.E, A.Epad, A.W);
+    const double* src = A.in + blockIdx.y * A.in_cstride;
+    double* dst = A.out + blockIdx.y * A.out_cstride;
+    double* xs = sm + L::EB * 2 * PL;  // plane 2: coefficient staging
+
+    load_tile<L, NM, NT>(src, c, xs);
+    __syncthreads();
+    stage_f1<S, P, L, NT, TA>(A.B, A.gtab, CoefIn<L, NM>{xs}, sm);
+    stage_f1<S, P, L, NT, TA2, CoefIn<L, NM>, true>(A.DB, A.gtab, CoefIn<L, NM>{xs}, sm);
+    __syncthreads();
+    stage_f2<S, P, L, NT, TA, TB>(A.B, A.gtab, sm);
+    stage_f2<S, P, L, NT, TA, TB1, true>(A.DB, A.gtab, sm);
+    stage_f2<S, P, L, NT, TA2, TB2>(A.B, A.gtab, sm);
+    __syncthreads();
+    items<L, Q1 * Q2, NT>([&](int e, int ps) {
+      const int j = ps / Q2, k = ps - j * Q2;
+      const long long eg = c.e0 + e;
+      const bool live = eg < c.E;
+      double xv[P1], x1[P1], x2[P1];
+#pragma unroll
+      for (int p = 0; p < P1; ++p) {
+        xv[p] = sm[L::at(e, TB + (p * Q1 + j) * S2 + k)];
+        x1[p] = sm[L::at(e, TB1 + (p * Q1 + j) * S2 + k)];
+        x2[p] = sm[L::at(e, TB2 + (p * Q1 + j) * S2 + k)];
+      }
+      double u[Q0], v0[Q0], v1[Q0], v2[Q0];
+      line_a0<S, P>(A.B, xv, u);
+      line_a0<S, P>(A.DB, xv, v0);
+      line_a0<S, P>(A.B, x1, v1);
+      line_a0<S, P>(A.B, x2, v2);
+#pragma unroll
+      for (int i = 0; i < Q0; ++i) {
+        const int l = (i * Q1 + j) * Q2 + k;
+        double w0, w1, w2, z;
+        if constexpr (GEO == GEO_DEFORMED) {
+          const double* g = A.pay + pay_base<PW>(live ? eg : 0, 7, NQ) + (long long)l * PW;
+          const double l00 = live ? __ldcs(g + 0LL * NQ * PW) : 0.0, l01 = live ? __ldcs(g + 1LL * NQ * PW) : 0.0,
+                       l02 = live ? __ldcs(g + 2LL * NQ * PW) : 0.0, l11 = live ? __ldcs(g + 3LL * NQ * PW) : 0.0,
+                       l12 = live ? __ldcs(g + 4LL * NQ * PW) : 0.0, l22 = live ? __ldcs(g + 5LL * NQ * PW) : 0.0;
+          w0 = fma(l02, v2[i], fma(l01, v1[i], l00 * v0[i]));
+          w1 = fma(l12, v2[i], fma(l11, v1[i], l01 * v0[i]));
+          w2 = fma(l22, v2[i], fma(l12, v1[i], l02 * v0[i]));
+          z = 0.0;
+          if constexpr (LAMW) z = live ? (A.lam * __ldcs(g + 6LL * NQ * PW)) * u[i] : 0.0;
+        } else {
+          const double* ge = A.pay + pay_base<PW>(live ? eg : 0, 8, 1);
+          const double* rp = A.gtab + GLayout<S, P>::REGK + k * (Q0 * Q1) + i * Q1 + j;
+          const double rw = __ldg(rp);
+          const double L00 = __ldg(ge + 0 * PW), L01 = __ldg(ge + 1 * PW), L02 = __ldg(ge + 2 * PW),
+                       L11 = __ldg(ge + 3 * PW), L12 = __ldg(ge + 4 * PW), L22 = __ldg(ge + 5 * PW);
+          double t0 = v0[i], t1 = v1[i], t2 = v2[i];
+          double g00 = 1.0, g10 = 0.0, g11 = 1.0, g20 = 0.0, g21 = 0.0;
+          if constexpr (S != HEX) {
+            g00 = __ldg(rp + 1 * NQ);
+            g10 = __ldg(rp + 2 * NQ);
+            g11 = __ldg(rp + 3 * NQ);
+            g20 = __ldg(rp + 4 * NQ);
+            g21 = __ldg(rp + 5 * NQ);
+            t0 = g00 * v0[i];
+            t1 = fma(g11, v1[i], g10 * v0[i]);
+            t2 = fma(g21, v1[i], fma(g20, v0[i], v2[i]));
+          }
+          const double s0 = rw * fma(L02, t2, fma(L01, t1, L00 * t0));
+          const double s1 = rw * fma(L12, t2, fma(L11, t1, L01 * t0));
+          const double s2 = rw * fma(L22, t2, fma(L12, t1, L02 * t0));
+          w0 = s0;
+          w1 = s1;
+          w2 = s2;
+          if constexpr (S != HEX) {
+            w0 = fma(g20, s2, fma(g10, s1, g00 * s0));
+            w1 = fma(g21, s2, g11 * s1);
+          }
+          w0 = live ? w0 : 0.0;
+          w1 = live ? w1 : 0.0;
+          w2 = live ? w2 : 0.0;
+          z = 0.0;
+          if constexpr (LAMW) z = live ? A.lam * ((u[i] * rw) * __ldg(ge + 6 * PW)) : 0.0;
+        }
+        u[i] = z;  // lam W u
+        v0[i] = w0;
+        v1[i] = w1;
+        v2[i] = w2;
+      }
+      double sa[P1], sb[P1], sc[P1], t[P1];
+      line_a0t<S, P>(A.B, u, sa);
+      line_a0t<S, P>(A.DB, v0, t);
+#pragma unroll
+      for (int p = 0; p < P1; ++p) sa[p] += t[p];
+      line_a0t<S, P>(A.B, v1, sb);
+      line_a0t<S, P>(A.B, v2, sc);
+#pragma unroll
+      for (int p = 0; p < P1; ++p) {
+        sm[L::at(e, TB + (p * Q1 + j) * S2 + k)] = sa[p];
+        sm[L::at(e, TB1 + (p * Q1 + j) * S2 + k)] = sb[p];
+        sm[L::at(e, TB2 + (p * Q1 + j) * S2 + k)] = sc[p];
+      }
+    });
+    __syncthreads();
+    // R1 = B1^T S_A + (D B1)^T S_B (both continue with dir-2 values),
+    // R2 = B1^T S_C (continues with the dir-2 derivative)
+    stage_b2<S, P, L, NT, TA, TB>(A.B, A.gtab, sm);
+    stage_b2<S, P, L, NT, TA2, TB2>(A.B, A.gtab, sm);
+    __syncthreads();
+    stage_b2<S, P, L, NT, TA, TB1, true, true>(A.DB, A.gtab, sm);
+    __syncthreads();
+    double* ys = sm + L::EB * 2 * PL;  // plane 2: output staging (S_A dead)
+    stage_b3<S, P, L, NT, TA>(A.B, A.gtab, CoefOut<L, NM>{ys}, sm);
+    __syncthreads();
+    stage_b3<S, P, L, NT, TA2, CoefOut<L, NM, true>, true>(A.DB, A.gtab, CoefOut<L, NM, true>{ys}, sm);
+    __syncthreads();
+    store_tile<L, NM, NT>(dst, c, ys);
   }
 };
 

@@ -9,10 +9,11 @@
 
 namespace sk {
 
-enum OpId : int { OP_HELM = 0, OP_MASS = 1, OP_BWD = 2, OP_IPROD = 3, OP_PDERIV = 4, OP_IPDERIV = 5, OP_COUNT = 6 };
+enum OpId : int { OP_HELM = 0, OP_MASS = 1, OP_BWD = 2, OP_IPROD = 3, OP_PDERIV = 4, OP_IPDERIV = 5, OP_HELM_NC = 6, OP_COUNT = 7 };
 
 struct LaunchReq {
   const void* fwd;    // FwdTab<S,P> (host copy, values)
+  const void* fwd_d;  // FwdTab<S,P> (host copy, derivatives)
   const void* dtab;   // DTab<S,P>   (host copy)
   const double* in;
   double* out;
@@ -32,7 +33,7 @@ struct OpSet {
   // returns a cudaError_t value (0 = success)
   int (*launch)(int op, const LaunchReq& r, void* stream);
   void (*config)(int op, int64_t out[3]);
-  // payload kinds: 0 HELMHOLTZ, 1 W, 2 DERIV
+  // payload kinds: 0 HELMHOLTZ (k-major), 1 W, 2 DERIV, 3 HELMHOLTZ (standard order)
   long long (*payload_doubles)(int kind, int geo);  // per element
   long long (*payload_elements)(long long E);       // elements incl. lane padding
   int (*pack)(int kind, int geo, long long E, const double* dxi, const double* jac, double* pay,

@@ -75,14 +75,22 @@ struct CoefIn {
   __device__ __forceinline__ double operator()(int e, int m) const { return xs[m * L::XSTR + e]; }
 };
 
-template <class L, int NM>
+template <class L, int NM, bool ACC = false>
 struct CoefOut {
   double* xs;
-  __device__ __forceinline__ void operator()(int e, int m, double v) const { xs[m * L::XSTR + e] = v; }
+  __device__ __forceinline__ void operator()(int e, int m, double v) const {
+    if constexpr (ACC)
+      xs[m * L::XSTR + e] += v;
+    else
+      xs[m * L::XSTR + e] = v;
+  }
 };
 
 // ---- F1: r -> k.  TA[p][q][k] = sum_r C_(p,q)[k][r] uhat[p,q,r] ----------
-template <int S, int P, class L, int NT, int TAo, class In>
+// DER2: the dir-2 family is the derivative one (reference dmode == 2; the
+// caller passes the derivative FwdTab for hex/prism, the device buffer's DC2
+// slices are used for pyr/tet)
+template <int S, int P, class L, int NT, int TAo, class In, bool DER2 = false>
 __device__ __forceinline__ void stage_f1(const FwdTab<S, P>& B, const double* __restrict__ gtab, const In& xin,
                                          double* sm) {
   using Dm = Dims<S, P>;
@@ -133,7 +141,8 @@ __device__ __forceinline__ void stage_f1(const FwdTab<S, P>& B, const double* __
       const int4 pr = __ldg(pairs + ps);  // p, q, mode offset, nr
       const int m = (S == TET) ? pr.x + pr.y : cmax(pr.x, pr.y);
       const int n = P1 - m;
-      const double* tab = gtab + GLayout<S, P>::C2 + wfam_off(Q2, P1, m);
+      const double* fam = gtab + (DER2 ? GLayout<S, P>::DC2 : GLayout<S, P>::C2);
+      const double* tab = fam + wfam_off(Q2, P1, m);
       double x[P1];
 #pragma unroll
       for (int r = 0; r < P1; ++r) x[r] = r < pr.w ? xin(e, pr.z + r) : 0.0;
@@ -147,16 +156,18 @@ __device__ __forceinline__ void stage_f1(const FwdTab<S, P>& B, const double* __
       }
       if (pr.x == 0 && pr.y == 0) {
         // collapsed apex mode (0,0,1): Y[k] = c2[0][k][1] * uhat[0,0,1]
-        const double* t0 = gtab + GLayout<S, P>::C2;
 #pragma unroll
-        for (int k = 0; k < Q2; ++k) sm[L::at(e, TAo + P1 * P1 * S2 + k)] = __ldg(t0 + k * P1 + 1) * x[1];
+        for (int k = 0; k < Q2; ++k) sm[L::at(e, TAo + P1 * P1 * S2 + k)] = __ldg(fam + k * P1 + 1) * x[1];
       }
     });
   }
 }
 
 // ---- F2: q -> j.  TB[p][j][k] = sum_q B_p[j][q] TA[p][q][k] ---------------
-template <int S, int P, class L, int NT, int TAo, int TBo>
+// DER1: the dir-1 family is the derivative one (reference dmode == 1): the
+// caller passes the derivative FwdTab and the apex share's constant eta_2
+// factor differentiates to zero ("ones2", operators.py:233-235)
+template <int S, int P, class L, int NT, int TAo, int TBo, bool DER1 = false>
 __device__ __forceinline__ void stage_f2(const FwdTab<S, P>& B, const double* __restrict__ gtab, double* sm) {
   using Dm = Dims<S, P>;
   constexpr int P1 = Dm::P1, Q1 = Dm::Q1, Q2 = Dm::Q2, S2 = L::S2;
@@ -175,7 +186,7 @@ __device__ __forceinline__ void stage_f2(const FwdTab<S, P>& B, const double* __
         for (int q = 1; q < P1; ++q) s = fma(B.a1[j * P1 + q], x[q], s);
         if constexpr (S == PYR) {
           // apex mode shares (operators.py:335-349)
-          if (p == 1) s += y;
+          if (!DER1 && p == 1) s += y;
           if (p == 0) s = fma(B.a1[j * P1 + 1], y, s);
         }
         sm[L::at(e, TBo + (p * Q1 + j) * S2 + k)] = s;
@@ -204,7 +215,10 @@ __device__ __forceinline__ void stage_f2(const FwdTab<S, P>& B, const double* __
           double s = B.b1[bo + j * n] * x[0];
 #pragma unroll
           for (int q = 1; q < n; ++q) s = fma(B.b1[bo + j * n + q], x[q], s);
-          if constexpr (p == 1) s = fma(B.b1[j * P1 + 1], x01, s) + y;  // edge (0,1,r) + apex shares
+          if constexpr (p == 1) {  // edge (0,1,r) + apex shares
+            s = fma(B.b1[j * P1 + 1], x01, s);
+            if constexpr (!DER1) s += y;
+          }
           if constexpr (p == 0) s = fma(B.b1[j * P1 + 1], y, s);
           sm[L::at(e, TBo + (p * Q1 + j) * S2 + k)] = s;
         }
@@ -266,7 +280,9 @@ __device__ __forceinline__ void line_dt_acc(const double* D, const double (&w)[Q
 }
 
 // ---- B2: j -> q.  TA[p][q][k] = sum_j B_p[j][q] TB[p][j][k] ---------------
-template <int S, int P, class L, int NT, int TAo, int TBo>
+// DER1: derivative dir-1 family (transposed dmode == 1, apex "ones" share
+// vanishes); ACC: add into TA and the spare rows instead of overwriting
+template <int S, int P, class L, int NT, int TAo, int TBo, bool DER1 = false, bool ACC = false>
 __device__ __forceinline__ void stage_b2(const FwdTab<S, P>& B, const double* __restrict__ gtab, double* sm) {
   using Dm = Dims<S, P>;
   constexpr int P1 = Dm::P1, Q1 = Dm::Q1, Q2 = Dm::Q2, S2 = L::S2;
@@ -281,14 +297,19 @@ __device__ __forceinline__ void stage_b2(const FwdTab<S, P>& B, const double* __
         double s = B.a1[q] * x[0];
 #pragma unroll
         for (int j = 1; j < Q1; ++j) s = fma(B.a1[j * P1 + q], x[j], s);
-        sm[L::at(e, TAo + (p * P1 + q) * S2 + k)] = s;
+        double& t = sm[L::at(e, TAo + (p * P1 + q) * S2 + k)];
+        t = ACC ? t + s : s;
       }
       if constexpr (S == PYR) {
         if (p == 1) {  // Y[k] = sum_j TB[1][j][k] (apex share, operators.py:371)
-          double y = x[0];
+          double y = 0.0;
+          if constexpr (!DER1) {
+            y = x[0];
 #pragma unroll
-          for (int j = 1; j < Q1; ++j) y += x[j];
-          sm[L::at(e, TAo + P1 * P1 * S2 + k)] = y;
+            for (int j = 1; j < Q1; ++j) y += x[j];
+          }
+          double& t = sm[L::at(e, TAo + P1 * P1 * S2 + k)];
+          t = ACC ? t + y : y;
         }
       }
     });
@@ -311,17 +332,20 @@ __device__ __forceinline__ void stage_b2(const FwdTab<S, P>& B, const double* __
           double s = B.b1[bo + q] * x[0];
 #pragma unroll
           for (int j = 1; j < Q1; ++j) s = fma(B.b1[bo + j * n + q], x[j], s);
-          sm[L::at(e, TAo + (p * P1 + q) * S2 + k)] = s;
+          double& t = sm[L::at(e, TAo + (p * P1 + q) * S2 + k)];
+          t = ACC ? t + s : s;
         }
         if constexpr (p == 1) {
-          double s = B.b1[1] * x[0], y = x[0];
+          double s = B.b1[1] * x[0], y = DER1 ? 0.0 : x[0];
 #pragma unroll
           for (int j = 1; j < Q1; ++j) {
             s = fma(B.b1[j * P1 + 1], x[j], s);
-            y += x[j];
+            if constexpr (!DER1) y += x[j];
           }
-          sm[L::at(e, TAo + P1 * P1 * S2 + k)] = y;
-          sm[L::at(e, TAo + (P1 * P1 + 1) * S2 + k)] = s;
+          double& ty = sm[L::at(e, TAo + P1 * P1 * S2 + k)];
+          double& ts = sm[L::at(e, TAo + (P1 * P1 + 1) * S2 + k)];
+          ty = ACC ? ty + y : y;
+          ts = ACC ? ts + s : s;
         }
       });
     });
@@ -329,7 +353,9 @@ __device__ __forceinline__ void stage_b2(const FwdTab<S, P>& B, const double* __
 }
 
 // ---- B3: k -> r, produce coefficients ----------------------------------------
-template <int S, int P, class L, int NT, int TAo, class Out>
+// DER2: derivative dir-2 family (transposed dmode == 2); accumulation into
+// the output is the Out functor's business
+template <int S, int P, class L, int NT, int TAo, class Out, bool DER2 = false>
 __device__ __forceinline__ void stage_b3(const FwdTab<S, P>& B, const double* __restrict__ gtab, const Out& out,
                                          const double* sm) {
   using Dm = Dims<S, P>;
@@ -383,7 +409,8 @@ __device__ __forceinline__ void stage_b3(const FwdTab<S, P>& B, const double* __
       const int4 pr = __ldg(pairs + ps);
       const int m = (S == TET) ? pr.x + pr.y : cmax(pr.x, pr.y);
       const int n = P1 - m;
-      const double* tab = gtab + GLayout<S, P>::C2 + wfam_off(Q2, P1, m);
+      const double* fam = gtab + (DER2 ? GLayout<S, P>::DC2 : GLayout<S, P>::C2);
+      const double* tab = fam + wfam_off(Q2, P1, m);
       double x[Q2];
 #pragma unroll
       for (int k = 0; k < Q2; ++k) x[k] = sm[L::at(e, TAo + (pr.x * P1 + pr.y) * S2 + k)];
@@ -395,11 +422,10 @@ __device__ __forceinline__ void stage_b3(const FwdTab<S, P>& B, const double* __
       }
       double apex = 0.0;
       if (pr.x == 0 && pr.y == 0) {
-        const double* t0 = gtab + GLayout<S, P>::C2;
 #pragma unroll
         for (int k = 0; k < Q2; ++k) {
           const double y = sm[L::at(e, TAo + P1 * P1 * S2 + k)] + sm[L::at(e, TAo + (0 * P1 + 1) * S2 + k)];
-          apex = fma(__ldg(t0 + k * P1 + 1), y, apex);
+          apex = fma(__ldg(fam + k * P1 + 1), y, apex);
         }
       }
 #pragma unroll

@@ -205,7 +205,7 @@ def _helmholtz(block: Block, lam: float, form: int, out: Block | None, name: str
     if lam < 0.0:
         raise ValueError(f"reaction coefficient must be nonnegative, got {lam}")
     out = _out_block(block, out, FieldState.COEFF, block.n_components)
-    pay = block.payload(_lib.SK_PAYLOAD_HELMHOLTZ)
+    pay = block.payload(_lib.SK_PAYLOAD_HELMHOLTZ if form == _lib.SK_FORM_COLL else _lib.SK_PAYLOAD_HELMHOLTZ_NC)
     xin = block.device(AccessQualifier.READ_ONLY)
     xout = out.device(AccessQualifier.WRITE_ONLY)
     _lib.check(

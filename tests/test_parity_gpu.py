@@ -60,6 +60,8 @@ def test_golden(sk, golden_ops, shape, P, gname):
         assert _err(got, g[f"{k}_helm_{lam}"]) <= TOL, (lam, _err(got, g[f"{k}_helm_{lam}"]))
     assert _err(sk.mass_apply(blk).get_elements()[0], g[f"{k}_mass"]) <= TOL
     assert _err(sk.bwd_trans(blk).get_elements()[0], g[f"{k}_bwd"]) <= TOL
+    got = sk.helmholtz_apply(blk, 1.0, form="noncoll").get_elements()[0]
+    assert _err(got, g[f"{k}_helmnc_1.0"]) <= TOL
     pb = blk.like(sk.FieldState.PHYS)
     pb.set_elements(g[f"{k}_y"][None])
     assert _err(sk.iproduct_wrt_base(pb).get_elements()[0], g[f"{k}_iprod"]) <= TOL
@@ -93,6 +95,8 @@ def test_oracle_ragged_tiles(sk, shape, P, width):
         for lam in (0.0, 1.3):
             got = sk.helmholtz_apply(blk, lam).get_elements()[0]
             assert _err(got, O.helmholtz_coll(el, geo, x, lam)) <= TOL
+            got = sk.helmholtz_apply_noncoll(blk, lam).get_elements()[0]
+            assert _err(got, O.helmholtz_noncoll(el, geo, x, lam)) <= TOL
         assert _err(sk.mass_apply(blk).get_elements()[0], O.mass(el, geo, x)) <= TOL
         y = np.random.default_rng(P).uniform(-1, 1, (el.nq, n))
         pb = blk.like(sk.FieldState.PHYS)

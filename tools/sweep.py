@@ -53,7 +53,7 @@ def main():
             fp64 = 34.2
     deformed = a.geo == "deformed"
     kinds = {"helm": (sk.OperatorKind.HELMHOLTZ_COLL, 1.0), "stiff": (sk.OperatorKind.HELMHOLTZ_COLL, 0.0),
-             "mass": (sk.OperatorKind.MASS, 1.0)}
+             "mass": (sk.OperatorKind.MASS, 1.0), "helmnc": (sk.OperatorKind.HELMHOLTZ_NONCOLL, 1.0)}
     cases = []
     emax = 1
     for op in a.ops.split(","):
@@ -74,7 +74,12 @@ def main():
         blk = sk.Block(b, fac, sk.FieldState.COEFF, 1, 1)
         blk.set_elements(np.random.default_rng(P).uniform(-1, 1, (1, b.n_modes, E)))
         out = blk.like(sk.FieldState.COEFF)
-        fn = (lambda: sk.mass_apply(blk, out=out)) if op == "mass" else (lambda: sk.helmholtz_apply(blk, lam, out=out))
+        if op == "mass":
+            fn = lambda: sk.mass_apply(blk, out=out)  # noqa: E731
+        elif op == "helmnc":
+            fn = lambda: sk.helmholtz_apply_noncoll(blk, lam, out=out)  # noqa: E731
+        else:
+            fn = lambda: sk.helmholtz_apply(blk, lam, out=out)  # noqa: E731
         for _ in range(3):
             fn()
         torch.cuda.synchronize()
@@ -87,7 +92,7 @@ def main():
         sec = t0.elapsed_time(t1) / 1e3 / a.reps
         gdof = b.n_modes * E / sec / 1e9
         flops = sk.operator_flops(kind, sk.Shape(s), P) * E
-        cfg = b.launch_config(_lib.load() and (1 if op == "mass" else 0))
+        cfg = b.launch_config({"mass": 1, "helmnc": 6}.get(op, 0))
         rec = {
             "op": op, "shape": s, "P": P, "geo": a.geo, "elements": E, "ms": sec * 1e3, "gdof_s": gdof,
             "hbm_gbs": bel * E / sec / 1e9, "hbm_frac": bel * E / sec / 1e9 / hbm,
