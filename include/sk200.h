@@ -113,6 +113,20 @@ int sk_mass_apply(const sk_basis* b, int geo_class, int64_t E, int W, int ncomp,
 int sk_helmholtz_apply(const sk_basis* b, int geo_class, int form, int64_t E, int W, int ncomp,
                        const double* uhat, const double* hpay, double lam, double* out, void* stream);
 
+/* ---- assembled C0 variant (hex, conforming, axis-aligned) --------
+ * No reference counterpart (global assembly is outside speckern, SPEC.md:8,
+ * 452).  Mesh nx x ny x nz_local element slab, e = (ez*ny + ey)*nx + ex; the
+ * slab's DOF vector covers gz in [0, nz_local*order] with
+ * g = (gz*(ny*order+1) + gy)*(nx*order+1) + gx.  gather: local(e, mode) =
+ * x[l2g(e, mode)] in the lane-major field layout of width W; scatter:
+ * y[g] = sum of the <= 8 element contributions (deterministic, no atomics).
+ * The end layers gz = 0 and gz = nz_local*order are shared with the
+ * neighbouring slabs and summed by the caller (NCCL exchange). */
+int sk_c0_gather(int order, int nx, int ny, int64_t nz_local, const double* x, int W, double* local,
+                 void* stream);
+int sk_c0_scatter(int order, int nx, int ny, int64_t nz_local, const double* local, int W, double* y,
+                  void* stream);
+
 /* ---- diagnostics ------------------------------------------------------------ */
 /* Number of kernel launches this thread issued through the library. */
 int64_t sk_launch_count(void);

@@ -43,6 +43,8 @@ SIGNATURES = {
     "sk_iproduct_wrt_deriv_base": (_I, [_P, _I, _L, _I, _P, _P, _P, _P]),
     "sk_mass_apply": (_I, [_P, _I, _L, _I, _I, _P, _P, _P, _P]),
     "sk_helmholtz_apply": (_I, [_P, _I, _I, _L, _I, _I, _P, _P, _D, _P, _P]),
+    "sk_c0_gather": (_I, [_I, _I, _I, _L, _P, _I, _P, _P]),
+    "sk_c0_scatter": (_I, [_I, _I, _I, _L, _P, _I, _P, _P]),
     "sk_launch_count": (_L, []),
     "sk_last_error": (ctypes.c_char_p, []),
     "sk_launch_config": (_I, [_P, _I, _PL]),

@@ -312,6 +312,14 @@ int sk_helmholtz_apply(const sk_basis* b, int geo, int form, int64_t E, int W, i
 
 int64_t sk_launch_count(void) { return g_launches.load(); }
 
+}  // extern "C"
+
+namespace sk {
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+}  // namespace sk
+
+extern "C" {
+
 const char* sk_last_error(void) { return g_err.c_str(); }
 
 int sk_launch_config(const sk_basis* b, int op, int64_t out[3]) {

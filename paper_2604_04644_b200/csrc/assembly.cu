@@ -1,0 +1,124 @@
+// Assembled C0 variant on a conforming, axis-aligned hex mesh (SURVEY §8f
+// rank 2): global <-> element-local maps for the modal basis.
+//
+// Mesh nx x ny x nz, element e = (ez*ny + ey)*nx + ex.  Along each axis the
+// modal index p of element ex maps to the 1D C0 DOF ex*P + (0, P, p-1 for
+// p = 0, 1, >= 2): vertex modes psi_0 / psi_1 are shared with the
+// neighbours, bubbles are private.  A rank owns the element slab
+// ez in [z0, z0 + nzl) and the DOF layers gz in [z0*P, (z0+nzl)*P]; the two
+// end layers are shared with the neighbouring ranks (summed by the caller's
+// NCCL exchange).  Both kernels are deterministic: the scatter is a gather
+// over the <= 8 element contributions of each DOF (no atomics).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "../../include/sk200.h"
+
+namespace sk {
+void count_launch();
+}
+
+namespace {
+
+__device__ __forceinline__ int mode_dof(int e, int p, int P) { return e * P + (p == 0 ? 0 : p == 1 ? P : p - 1); }
+
+__device__ __forceinline__ long long lane_idx(long long e, int n, int N, int W) {
+  const long long g = e / W;
+  return (g * N + n) * (long long)W + (e - g * W);
+}
+
+__global__ void k_c0_gather(int P, int nx, int ny, long long nzl, const double* __restrict__ x, int W,
+                            double* __restrict__ local) {
+  const int P1 = P + 1, NM = P1 * P1 * P1;
+  const long long Nx = (long long)nx * P + 1, Ny = (long long)ny * P + 1;
+  const long long E = (long long)nx * ny * nzl;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < E * NM; t += (long long)gridDim.x * blockDim.x) {
+    const long long e = t / NM;
+    const int m = (int)(t - e * NM);
+    const int r = m % P1, q = (m / P1) % P1, p = m / (P1 * P1);
+    const int ex = (int)(e % nx);
+    const int ey = (int)((e / nx) % ny);
+    const long long ez = e / ((long long)nx * ny);  // slab-relative
+    const long long g = ((long long)mode_dof((int)ez, r, P) * Ny + mode_dof(ey, q, P)) * Nx + mode_dof(ex, p, P);
+    local[lane_idx(e, m, NM, W)] = x[g];
+  }
+}
+
+// contributions of 1D DOF g: (element, mode) pairs, at most two
+__device__ __forceinline__ int dof_owners(long long g, int P, long long ne, long long* el, int* md) {
+  int n = 0;
+  const long long e = g / P;
+  const int o = (int)(g - e * P);
+  if (o == 0) {
+    if (e >= 1) {
+      el[n] = e - 1;
+      md[n++] = 1;
+    }
+    if (e < ne) {
+      el[n] = e;
+      md[n++] = 0;
+    }
+  } else {
+    el[n] = e;
+    md[n++] = o + 1;
+  }
+  return n;
+}
+
+__global__ void k_c0_scatter(int P, int nx, int ny, long long nzl, const double* __restrict__ local, int W,
+                             double* __restrict__ y) {
+  const int P1 = P + 1, NM = P1 * P1 * P1;
+  const long long Nx = (long long)nx * P + 1, Ny = (long long)ny * P + 1, Nz = nzl * P + 1;
+  const long long N = Nx * Ny * Nz;
+  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < N; g += (long long)gridDim.x * blockDim.x) {
+    const long long gx = g % Nx, gy = (g / Nx) % Ny, gz = g / (Nx * Ny);
+    long long ex[2], ey[2], ez[2];
+    int px[2], py[2], pz[2];
+    const int nxo = dof_owners(gx, P, nx, ex, px);
+    const int nyo = dof_owners(gy, P, ny, ey, py);
+    const int nzo = dof_owners(gz, P, nzl, ez, pz);
+    double s = 0.0;
+    for (int c = 0; c < nzo; ++c)
+      for (int b = 0; b < nyo; ++b)
+        for (int a = 0; a < nxo; ++a) {
+          const long long e = (ez[c] * ny + ey[b]) * nx + ex[a];
+          const int m = (px[a] * P1 + py[b]) * P1 + pz[c];
+          s += local[lane_idx(e, m, NM, W)];
+        }
+    y[g] = s;
+  }
+}
+
+unsigned grid_for(long long n) {
+  long long g = (n + 255) / 256;
+  if (g > 148LL * 32) g = 148LL * 32;
+  return (unsigned)(g < 1 ? 1 : g);
+}
+
+}  // namespace
+
+extern "C" {
+
+int sk_c0_gather(int order, int nx, int ny, int64_t nz_local, const double* x, int W, double* local, void* stream) {
+  if (order < 1 || order > 10 || nx < 1 || ny < 1 || nz_local < 0 || W < 1) return SK_ERR_ARG;
+  if (nz_local == 0) return SK_OK;
+  if (!x || !local) return SK_ERR_ARG;
+  const long long E = (long long)nx * ny * nz_local;
+  const long long NM = (long long)(order + 1) * (order + 1) * (order + 1);
+  sk::count_launch();
+  k_c0_gather<<<grid_for(E * NM), 256, 0, static_cast<cudaStream_t>(stream)>>>(order, nx, ny, nz_local, x, W, local);
+  return cudaGetLastError() == cudaSuccess ? SK_OK : SK_ERR_CUDA;
+}
+
+int sk_c0_scatter(int order, int nx, int ny, int64_t nz_local, const double* local, int W, double* y, void* stream) {
+  if (order < 1 || order > 10 || nx < 1 || ny < 1 || nz_local < 0 || W < 1) return SK_ERR_ARG;
+  if (nz_local == 0) return SK_OK;
+  if (!y || !local) return SK_ERR_ARG;
+  const long long N = ((long long)nx * order + 1) * ((long long)ny * order + 1) * (nz_local * order + 1);
+  sk::count_launch();
+  k_c0_scatter<<<grid_for(N), 256, 0, static_cast<cudaStream_t>(stream)>>>(order, nx, ny, nz_local, local, W, y);
+  return cudaGetLastError() == cudaSuccess ? SK_OK : SK_ERR_CUDA;
+}
+
+}  // extern "C"

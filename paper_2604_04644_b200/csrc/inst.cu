@@ -130,7 +130,7 @@ void fill_gtab(const HostBasis& hb, double* g) {
       if (S == PRISM) nr = Dm::P1 - p;
       if (S == PYR) nr = Dm::P1 - cmax(p, q);
       if (S == TET) nr = Dm::P1 - p - q;
-      if (np < Dm::NPAIR && (S == PYR || S == TET)) {
+      if (np < Dm::NPAIR && S != HEX) {
         pr[4 * np + 0] = p;
         pr[4 * np + 1] = q;
         pr[4 * np + 2] = off;

@@ -203,8 +203,12 @@ struct k_helm {
     line_d<Q2>(A.D.d2, u, w2);  // w2 holds v2 until overwritten per point
     if constexpr (GEO == GEO_DEFORMED) {
       const double* g = A.pay + pay_base<PW>(live ? eg : 0, 7, NQ) + (long long)ps * PW;
+      // points in chunks of CH: a compiler fence between chunks keeps ptxas
+      // from hoisting all 7*Q2 geometry loads (register pressure at high P)
+      constexpr int CH = Q2 <= 6 ? Q2 : 4;
 #pragma unroll
       for (int k = 0; k < Q2; ++k) {
+        if (k > 0 && k % CH == 0) asm volatile("" ::: "memory");
         const double* gk = g + (long long)k * (Q0 * Q1) * PW;
         const double l00 = live ? __ldcs(gk + 0LL * NQ * PW) : 0.0, l01 = live ? __ldcs(gk + 1LL * NQ * PW) : 0.0,
                      l02 = live ? __ldcs(gk + 2LL * NQ * PW) : 0.0, l11 = live ? __ldcs(gk + 3LL * NQ * PW) : 0.0,

@@ -24,6 +24,14 @@
 
 namespace sk {
 
+// Code-size / parallelism switches (measured, profiles/r01): tet q <-> j
+// sweeps use compile-time slice dispatch up to this order and a compact
+// L1-table loop above it (instruction-cache footprint); prism r <-> k sweeps
+// run one thread per (element, q) with uniform slice tables up to
+// kPrismUniformMaxP and one per (element, p, q) pair above it.
+constexpr int kTetDispatchMaxP = 9;
+constexpr int kPrismUniformMaxP = 8;
+
 // ---- coefficient tile staging ----------------------------------------------
 // xs[m * XSTR + e] <-> field value of mode m of element e0 + e; iteration order
 // follows the field layout so that consecutive threads touch consecutive
@@ -108,7 +116,7 @@ __device__ __forceinline__ void stage_f1(const FwdTab<S, P>& B, const double* __
         sm[L::at(e, TAo + ps * S2 + k)] = s;
       }
     });
-  } else if constexpr (S == PRISM) {
+  } else if constexpr (S == PRISM && P <= kPrismUniformMaxP) {
     // item = (e, q); p unrolled so c2[p] is uniform (operators.py:275-295)
     items<L, P1, NT>([&](int e, int q) {
       double u0q1 = 0.0;
@@ -134,27 +142,33 @@ __device__ __forceinline__ void stage_f1(const FwdTab<S, P>& B, const double* __
       }
     });
   } else {
-    // pyr / tet: item = (e, (p,q) pair); table c2[p+q] (tet) or c2[max(p,q)]
-    // (pyr) differs per item -> read from the device table buffer
+    // prism / pyr / tet: item = (e, (p,q) pair); the dir-2 slice c2[p]
+    // (prism), c2[max(p,q)] (pyr) or c2[p+q] (tet) differs per item -> read
+    // from the device table buffer through L1 (operators.py:209-351)
     const int4* pairs = reinterpret_cast<const int4*>(gtab + GLayout<S, P>::PAIRS);
     items<L, Dm::NPAIR, NT>([&](int e, int ps) {
       const int4 pr = __ldg(pairs + ps);  // p, q, mode offset, nr
-      const int m = (S == TET) ? pr.x + pr.y : cmax(pr.x, pr.y);
+      const int m = (S == TET) ? pr.x + pr.y : (S == PRISM) ? pr.x : cmax(pr.x, pr.y);
       const int n = P1 - m;
       const double* fam = gtab + (DER2 ? GLayout<S, P>::DC2 : GLayout<S, P>::C2);
       const double* tab = fam + wfam_off(Q2, P1, m);
       double x[P1];
 #pragma unroll
       for (int r = 0; r < P1; ++r) x[r] = r < pr.w ? xin(e, pr.z + r) : 0.0;
+      // prism collapsed-edge share of mode (0, q, 1) (operators.py:288-293)
+      const double u0q1 = (S == PRISM && pr.x == 1) ? xin(e, pr.y * P1 + 1) : 0.0;
 #pragma unroll
       for (int k = 0; k < Q2; ++k) {
         double s = 0.0;
 #pragma unroll
         for (int r = 0; r < P1; ++r)
           if (r < pr.w) s = fma(__ldg(tab + k * n + r), x[r], s);
+        if constexpr (S == PRISM) {
+          if (pr.x == 1) s = fma(u0q1, __ldg(fam + k * P1 + 1), s);
+        }
         sm[L::at(e, TAo + (pr.x * P1 + pr.y) * S2 + k)] = s;
       }
-      if (pr.x == 0 && pr.y == 0) {
+      if (S != PRISM && pr.x == 0 && pr.y == 0) {
         // collapsed apex mode (0,0,1): Y[k] = c2[0][k][1] * uhat[0,0,1]
 #pragma unroll
         for (int k = 0; k < Q2; ++k) sm[L::at(e, TAo + P1 * P1 * S2 + k)] = __ldg(fam + k * P1 + 1) * x[1];
@@ -196,6 +210,35 @@ __device__ __forceinline__ void stage_f2(const FwdTab<S, P>& B, const double* __
     // tet: item = (e, k, p) so that all P1 slices run in parallel; the slice
     // index is dispatched to a compile-time constant so b1[p] stays a
     // uniform operand (operators.py:209-245)
+    if constexpr (P > kTetDispatchMaxP) {
+      // high order: one compact loop, slice table through L1 (keeps the
+      // kernel inside the instruction cache)
+      const double* fam = gtab + (DER1 ? GLayout<S, P>::DB1 : GLayout<S, P>::B1);
+      items<L, Q2 * P1, NT>([&](int e, int ps) {
+        const int p = ps / Q2, k = ps - p * Q2;
+        const int n = P1 - p;
+        const double* tab = fam + wfam_off(Q1, P1, p);
+        double x[P1];
+#pragma unroll
+        for (int q = 0; q < P1; ++q) x[q] = q < n ? sm[L::at(e, TAo + (p * P1 + q) * S2 + k)] : 0.0;
+        const double y = p <= 1 ? sm[L::at(e, TAo + P1 * P1 * S2 + k)] : 0.0;
+        const double x01 = p == 1 ? sm[L::at(e, TAo + (0 * P1 + 1) * S2 + k)] : 0.0;
+#pragma unroll
+        for (int j = 0; j < Q1; ++j) {
+          double s = 0.0;
+#pragma unroll
+          for (int q = 0; q < P1; ++q)
+            if (q < n) s = fma(__ldg(tab + j * n + q), x[q], s);
+          if (p == 1) {
+            s = fma(B.b1[j * P1 + 1], x01, s);
+            if constexpr (!DER1) s += y;
+          }
+          if (p == 0) s = fma(B.b1[j * P1 + 1], y, s);
+          sm[L::at(e, TBo + (p * Q1 + j) * S2 + k)] = s;
+        }
+      });
+      return;
+    }
     items<L, Q2 * P1, NT>([&](int e, int ps) {
       const int pr = ps / Q2, k = ps - pr * Q2;
       dispatch<0, P1>(pr, [&](auto pc) {
@@ -318,6 +361,40 @@ __device__ __forceinline__ void stage_b2(const FwdTab<S, P>& B, const double* __
     // collapsed-edge share S[k] = sum_j b1[0][j][1] TB[1][j][k] and the apex
     // share Y[k] = sum_j TB[1][j][k] go to two spare rows; B3 adds them to
     // modes (0,1,r) and (0,0,1) (operators.py:263-271).
+    if constexpr (P > kTetDispatchMaxP) {
+      const double* fam = gtab + (DER1 ? GLayout<S, P>::DB1 : GLayout<S, P>::B1);
+      items<L, Q2 * P1, NT>([&](int e, int ps) {
+        const int p = ps / Q2, k = ps - p * Q2;
+        const int n = P1 - p;
+        const double* tab = fam + wfam_off(Q1, P1, p);
+        double x[Q1];
+#pragma unroll
+        for (int j = 0; j < Q1; ++j) x[j] = sm[L::at(e, TBo + (p * Q1 + j) * S2 + k)];
+#pragma unroll
+        for (int q = 0; q < P1; ++q) {
+          if (q < n) {
+            double s = 0.0;
+#pragma unroll
+            for (int j = 0; j < Q1; ++j) s = fma(__ldg(tab + j * n + q), x[j], s);
+            double& t = sm[L::at(e, TAo + (p * P1 + q) * S2 + k)];
+            t = ACC ? t + s : s;
+          }
+        }
+        if (p == 1) {
+          double s = B.b1[1] * x[0], y = DER1 ? 0.0 : x[0];
+#pragma unroll
+          for (int j = 1; j < Q1; ++j) {
+            s = fma(B.b1[j * P1 + 1], x[j], s);
+            if constexpr (!DER1) y += x[j];
+          }
+          double& ty = sm[L::at(e, TAo + P1 * P1 * S2 + k)];
+          double& ts = sm[L::at(e, TAo + (P1 * P1 + 1) * S2 + k)];
+          ty = ACC ? ty + y : y;
+          ts = ACC ? ts + s : s;
+        }
+      });
+      return;
+    }
     items<L, Q2 * P1, NT>([&](int e, int ps) {
       const int pr = ps / Q2, k = ps - pr * Q2;
       dispatch<0, P1>(pr, [&](auto pc) {
@@ -373,7 +450,7 @@ __device__ __forceinline__ void stage_b3(const FwdTab<S, P>& B, const double* __
         out(e, ps * P1 + r, s);
       }
     });
-  } else if constexpr (S == PRISM) {
+  } else if constexpr (S == PRISM && P <= kPrismUniformMaxP) {
     items<L, P1, NT>([&](int e, int q) {
       int off = 0;
 #pragma unroll
@@ -407,7 +484,7 @@ __device__ __forceinline__ void stage_b3(const FwdTab<S, P>& B, const double* __
     const int4* pairs = reinterpret_cast<const int4*>(gtab + GLayout<S, P>::PAIRS);
     items<L, Dm::NPAIR, NT>([&](int e, int ps) {
       const int4 pr = __ldg(pairs + ps);
-      const int m = (S == TET) ? pr.x + pr.y : cmax(pr.x, pr.y);
+      const int m = (S == TET) ? pr.x + pr.y : (S == PRISM) ? pr.x : cmax(pr.x, pr.y);
       const int n = P1 - m;
       const double* fam = gtab + (DER2 ? GLayout<S, P>::DC2 : GLayout<S, P>::C2);
       const double* tab = fam + wfam_off(Q2, P1, m);
@@ -421,12 +498,18 @@ __device__ __forceinline__ void stage_b3(const FwdTab<S, P>& B, const double* __
         }
       }
       double apex = 0.0;
-      if (pr.x == 0 && pr.y == 0) {
+      if (S != PRISM && pr.x == 0 && pr.y == 0) {
 #pragma unroll
         for (int k = 0; k < Q2; ++k) {
           const double y = sm[L::at(e, TAo + P1 * P1 * S2 + k)] + sm[L::at(e, TAo + (0 * P1 + 1) * S2 + k)];
           apex = fma(__ldg(fam + k * P1 + 1), y, apex);
         }
+      }
+      if (S == PRISM && pr.x == 0) {
+        // modes (0,q,1) += sum_k c2[0][k][1] TA[1][q][k] (operators.py:312-317)
+#pragma unroll
+        for (int k = 0; k < Q2; ++k)
+          apex = fma(__ldg(fam + k * P1 + 1), sm[L::at(e, TAo + (1 * P1 + pr.y) * S2 + k)], apex);
       }
 #pragma unroll
       for (int r = 0; r < P1; ++r) {

@@ -21,7 +21,7 @@ SHAPES = ["hex", "prism", "pyr", "tet"]
 
 def _declared():
     src = open(os.path.join(ROOT, "include", "sk200.h")).read()
-    return sorted(set(re.findall(r"\b(sk_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(sk_[a-z0-9_]+)\s*\(", src)))
 
 
 def test_exports_every_declared_symbol():
