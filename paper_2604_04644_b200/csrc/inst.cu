@@ -4,7 +4,10 @@
 // and exports them through sk::opset_impl<S,P>().
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <array>
 #include <cmath>
+#include <vector>
 #include <cstring>
 #include <mutex>
 
@@ -49,13 +52,40 @@ struct Cfg {
   static constexpr int SMEM = L::SMEM_DOUBLES * 8;
   // __launch_bounds__ min blocks: 1, or the CTAs per SM that shared memory
   // allows (forces ptxas to fit the registers; tuned, as it can spill)
-  static constexpr int MINB = (OP == OP_HELM && tuned_minb(S, P))
-                                  ? cmax(1, cmin(cmin(4, (220 * 1024) / (SMEM + 1024)), 2048 / NT))
-                                  : 1;
+  static constexpr int CLS = OP == OP_HELM ? 0 : OP == OP_MASS ? 1 : 2;
+  static constexpr int MINB = tuned_minb(S, P) ? cmax(1, cmin(cmin(tuned_minb_cap(CLS, S, P), (220 * 1024) / (SMEM + 1024)), 2048 / NT))
+                                               : 1;
 };
 
 // ---------------------------------------------------------------------------
 // host table fills
+// even-odd combination of the vertex columns of a full family (Q x P1)
+template <int Q, int P1>
+void fill_pm(const std::vector<double>& a, double* ap, double* am) {
+  for (int i = 0; i < Q; ++i) {
+    ap[i] = 0.5 * (a[i * P1] + a[i * P1 + 1]);
+    am[i] = 0.5 * (a[i * P1] - a[i * P1 + 1]);
+  }
+}
+
+// even-odd form of M (transposed when tr) -- see EOTab
+template <int Q>
+void fill_eo(const std::vector<double>& D, bool tr, EOTab<Q>& t) {
+  constexpr int H = Q / 2;
+  auto M = [&](int a, int b) { return tr ? D[b * Q + a] : D[a * Q + b]; };
+  std::memset(&t, 0, sizeof(t));
+  for (int a = 0; a < H; ++a) {
+    for (int b = 0; b < H; ++b) {
+      t.E[a * H + b] = 0.5 * (M(a, b) + M(a, Q - 1 - b));
+      t.O[a * H + b] = 0.5 * (M(a, b) - M(a, Q - 1 - b));
+    }
+    if (Q % 2) {
+      t.Em[a] = M(a, H);
+      t.Om[a] = M(H, a);
+    }
+  }
+}
+
 template <int S, int P>
 void fill_fwd(const HostBasis& hb, FwdTab<S, P>& t, bool deriv) {
   using Dm = Dims<S, P>;
@@ -64,12 +94,15 @@ void fill_fwd(const HostBasis& hb, FwdTab<S, P>& t, bool deriv) {
   std::memcpy(t.a0, a[0].data(), sizeof(double) * Dm::Q0 * Dm::P1);
   if constexpr (S != TET) std::memcpy(t.a1, a[1].data(), sizeof(double) * Dm::Q1 * Dm::P1);
   if constexpr (S == HEX) std::memcpy(t.a2, a[2].data(), sizeof(double) * Dm::Q2 * Dm::P1);
+  fill_pm<Dm::Q0, Dm::P1>(a[0], t.a0p, t.a0m);
+  if constexpr (S != TET) fill_pm<Dm::Q1, Dm::P1>(a[1], t.a1p, t.a1m);
+  if constexpr (S == HEX) fill_pm<Dm::Q2, Dm::P1>(a[2], t.a2p, t.a2m);
   if constexpr (S == TET) {
     const auto& fam = deriv ? hb.db1 : hb.b1;
     for (int p = 0; p < Dm::P1; ++p)
       std::memcpy(t.b1 + wfam_off(Dm::Q1, Dm::P1, p), fam[p].data(), sizeof(double) * fam[p].size());
   }
-  if constexpr (S == PRISM) {
+  if constexpr (S != HEX) {
     const auto& fam = deriv ? hb.dc2 : hb.c2;
     for (int p = 0; p < Dm::P1; ++p)
       std::memcpy(t.c2 + wfam_off(Dm::Q2, Dm::P1, p), fam[p].data(), sizeof(double) * fam[p].size());
@@ -82,9 +115,20 @@ void fill(const HostBasis& hb, void* fv, void* fd, void* dt) {
   fill_fwd<S, P>(hb, *static_cast<FwdTab<S, P>*>(fv), false);
   fill_fwd<S, P>(hb, *static_cast<FwdTab<S, P>*>(fd), true);
   auto& d = *static_cast<DTab<S, P>*>(dt);
+  std::memset(&d, 0, sizeof(d));
   std::memcpy(d.d0, hb.D[0].data(), sizeof(double) * Dm::Q0 * Dm::Q0);
   std::memcpy(d.d1, hb.D[1].data(), sizeof(double) * Dm::Q1 * Dm::Q1);
   std::memcpy(d.d2, hb.D[2].data(), sizeof(double) * Dm::Q2 * Dm::Q2);
+  fill_eo<Dm::Q0>(hb.D[0], false, d.e0);
+  fill_eo<Dm::Q0>(hb.D[0], true, d.e0t);
+  if constexpr (gll_dir(S, 1)) {
+    fill_eo<Dm::Q1>(hb.D[1], false, d.e1);
+    fill_eo<Dm::Q1>(hb.D[1], true, d.e1t);
+  }
+  if constexpr (gll_dir(S, 2)) {
+    fill_eo<Dm::Q2>(hb.D[2], false, d.e2);
+    fill_eo<Dm::Q2>(hb.D[2], true, d.e2t);
+  }
 }
 
 // extra runtime-indexed tables (after GLayout<S,P>::SIZE)
@@ -120,9 +164,12 @@ void fill_gtab(const HostBasis& hb, double* g) {
       std::memcpy(g + L::DC2 + wfam_off(Dm::Q2, Dm::P1, m), hb.dc2[m].data(), sizeof(double) * hb.dc2[m].size());
     }
   }
-  // (p, q) pairs of the ragged stages with their mode offset and run length
+  // (p, q) pairs of the ragged stages with their mode offset and run length,
+  // ordered by run length (= dir-2 slice P1 - m) so that the work items of a
+  // warp mostly share one slice (one branch of the slice dispatch)
   int* pr = reinterpret_cast<int*>(g + L::PAIRS);
-  int np = 0, off = 0;
+  std::vector<std::array<int, 4>> pl;
+  int off = 0;
   for (int p = 0; p < Dm::P1; ++p) {
     const int nq = (S == TET) ? Dm::P1 - p : Dm::P1;
     for (int q = 0; q < nq; ++q) {
@@ -130,16 +177,13 @@ void fill_gtab(const HostBasis& hb, double* g) {
       if (S == PRISM) nr = Dm::P1 - p;
       if (S == PYR) nr = Dm::P1 - cmax(p, q);
       if (S == TET) nr = Dm::P1 - p - q;
-      if (np < Dm::NPAIR && S != HEX) {
-        pr[4 * np + 0] = p;
-        pr[4 * np + 1] = q;
-        pr[4 * np + 2] = off;
-        pr[4 * np + 3] = nr;
-        ++np;
-      }
+      if ((int)pl.size() < Dm::NPAIR && S != HEX) pl.push_back({p, q, off, nr});
       off += nr;
     }
   }
+  std::stable_sort(pl.begin(), pl.end(), [](const std::array<int, 4>& a, const std::array<int, 4>& b) { return a[3] > b[3]; });
+  for (size_t i = 0; i < pl.size(); ++i)
+    for (int c = 0; c < 4; ++c) pr[4 * i + c] = pl[i][c];
   for (int i = 0; i < Dm::Q0; ++i)
     for (int j = 0; j < Dm::Q1; ++j)
       for (int k = 0; k < Dm::Q2; ++k) {
@@ -237,10 +281,11 @@ int launch(int op, const LaunchReq& r, void* stream) {
   const bool def = r.geo == GEO_DEFORMED;
   using namespace std;
   switch (op) {
-#ifndef SK_ONLY_HELM
+#if !defined(SK_ONLY_OP) || SK_ONLY_OP == 6
     case OP_HELM_NC:
       return launch_nc<S, P>(r, stream);
 #endif
+#if !defined(SK_ONLY_OP) || SK_ONLY_OP == 0
     case OP_HELM: {
       using C = Cfg<S, P, OP_HELM>;
       if (def) {
@@ -250,12 +295,15 @@ int launch(int op, const LaunchReq& r, void* stream) {
       if (r.lam != 0.0) return go<S, P, OP_HELM, k_helm<S, P, typename C::L, C::NT, C::PW, GEO_REGULAR, true, C::MINB>>(a, r, r.ncomp, stream);
       return go<S, P, OP_HELM, k_helm<S, P, typename C::L, C::NT, C::PW, GEO_REGULAR, false, C::MINB>>(a, r, r.ncomp, stream);
     }
-#ifndef SK_ONLY_HELM
+#endif
+#if !defined(SK_ONLY_OP) || SK_ONLY_OP == 1
     case OP_MASS: {
       using C = Cfg<S, P, OP_MASS>;
       if (def) return go<S, P, OP_MASS, k_mass<S, P, typename C::L, C::NT, C::PW, GEO_DEFORMED, C::MINB>>(a, r, r.ncomp, stream);
       return go<S, P, OP_MASS, k_mass<S, P, typename C::L, C::NT, C::PW, GEO_REGULAR, C::MINB>>(a, r, r.ncomp, stream);
     }
+#endif
+#if !defined(SK_ONLY_OP)
     case OP_BWD: {
       using C = Cfg<S, P, OP_BWD>;
       return go<S, P, OP_BWD, k_bwd<S, P, typename C::L, C::NT, C::MINB>>(a, r, r.ncomp, stream);

@@ -67,6 +67,14 @@ __host__ __device__ constexpr int wfam_off(int Q, int P1, int p) { return Q * (p
 
 // Basis tables consumed with compile-time indices: they live in the kernel
 // parameter space (constant bank) and enter DFMAs as uniform operands.
+// Directions whose 1D rule is Gauss-Lobatto (symmetric points z_{Q-1-i} =
+// -z_i): dir 0 always, dir 1 except tet, dir 2 for hex.  Their collocation
+// matrices are centro-antisymmetric, D[Q-1-a][Q-1-b] = -D[a][b], and the
+// modified basis has psi_p(-z) = (-1)^p psi_p(z) (p >= 2), psi_0(-z) =
+// psi_1(z), so every 1D contraction along them runs in even-odd form at
+// half the multiply-adds.
+__host__ __device__ constexpr bool gll_dir(int S, int d) { return d == 0 || (d == 1 && S != TET) || (d == 2 && S == HEX); }
+
 template <int S, int P>
 struct FwdTab {
   using Dm = Dims<S, P>;
@@ -74,7 +82,23 @@ struct FwdTab {
   double a1[(S != TET) ? Dm::Q1 * Dm::P1 : 1];      // dir 1 [j][q]
   double a2[(S == HEX) ? Dm::Q2 * Dm::P1 : 1];      // dir 2 [k][r]
   double b1[(S == TET) ? Dm::Q1 * Dm::NTRI : 1];    // tet dir 1, per p
-  double c2[(S == PRISM) ? Dm::Q2 * Dm::NTRI : 1];  // prism dir 2, per p
+  double c2[(S != HEX) ? Dm::Q2 * Dm::NTRI : 1];    // dir-2 family, per slice m
+  // even-odd vertex-mode combinations of the full families,
+  // (B[i][0] +- B[i][1]) / 2, rows i <= (Q-1)/2
+  double a0p[Dm::Q0], a0m[Dm::Q0];
+  double a1p[(S != TET) ? Dm::Q1 : 1], a1m[(S != TET) ? Dm::Q1 : 1];
+  double a2p[(S == HEX) ? Dm::Q2 : 1], a2m[(S == HEX) ? Dm::Q2 : 1];
+};
+
+// even-odd form of a centro-antisymmetric Q x Q matrix M, H = Q/2:
+// E[a][b] = (M[a][b] + M[a][Q-1-b]) / 2, O[a][b] = (M[a][b] - M[a][Q-1-b]) / 2
+// (a, b < H); odd Q adds the middle column Em[a] = M[a][H] and row
+// Om[b] = M[H][b]
+template <int Q>
+struct EOTab {
+  static constexpr int H = Q / 2;
+  double E[H * H], O[H * H];
+  double Em[H], Om[H];
 };
 
 template <int S, int P>
@@ -83,6 +107,10 @@ struct DTab {
   double d0[Dm::Q0 * Dm::Q0];
   double d1[Dm::Q1 * Dm::Q1];
   double d2[Dm::Q2 * Dm::Q2];
+  // even-odd forms of D_d and D_d^T on the Gauss-Lobatto directions
+  EOTab<Dm::Q0> e0, e0t;
+  EOTab<gll_dir(S, 1) ? Dm::Q1 : 2> e1, e1t;
+  EOTab<gll_dir(S, 2) ? Dm::Q2 : 2> e2, e2t;
 };
 
 // Layout of the per-basis device table buffer ("gtab"), runtime indexed.

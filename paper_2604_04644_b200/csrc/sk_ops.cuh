@@ -23,6 +23,7 @@
 #pragma once
 
 #include "sk_stages.cuh"
+#include "sk_tune.h"
 
 namespace sk {
 
@@ -94,14 +95,18 @@ __device__ __forceinline__ void field_range(long long e0, long long n, int N, in
 
 
 // prefetch the payload chunk of elements [e0, e0 + n): C*N doubles per
-// element, PW-element lane groups (pay_base layout)
+// element, PW-element lane groups (pay_base layout).  CR <= C: only the
+// first CR components are read (stiffness skips wJ, the last of the 7
+// Helmholtz components); with n <= PW (one tile = one lane group) they are
+// one contiguous range.
 template <int PW>
 __device__ __forceinline__ void prefetch_payload(const double* pay, long long e0, long long n, long long E, long long C,
-                                                 long long N) {
+                                                 long long N, long long CR = -1) {
   if (n <= 0) return;
   const long long per = C * N * 8;
   const long long lo = (e0 / PW) * PW * per;
-  const long long hi = ((e0 + n + PW - 1) / PW) * PW * per;
+  long long hi = ((e0 + n + PW - 1) / PW) * PW * per;
+  if (CR >= 0 && CR < C && n <= PW && e0 % PW == 0) hi = lo + CR * N * PW * 8;
   l2_prefetch(pay, lo, hi, ((E + PW - 1) / PW) * PW * per);
 }
 
@@ -143,7 +148,7 @@ struct k_helm {
     const long long n = A.E - e0 < EB ? A.E - e0 : EB;
     (void)n;
     (void)e0;
-    if constexpr (GEO == GEO_DEFORMED) prefetch_payload<PW>(A.pay, e0, n, A.E, LAMW ? 7 : 6, Dims<S, P>::NQ);
+    if constexpr (GEO == GEO_DEFORMED) prefetch_payload<PW>(A.pay, e0, n, A.E, 7, Dims<S, P>::NQ, LAMW ? 7 : 6);
   }
   __device__ static void prefetch_in(const OpArgs<S, P>& A, long long t) {
     const long long e0 = t * EB;
@@ -162,7 +167,7 @@ struct k_helm {
 
   load_tile<L, NM, NT>(src, c, xs);
   __syncthreads();
-  stage_f1<S, P, L, NT, TAo>(A.B, A.gtab, CoefIn<L, NM>{xs}, sm);
+  stage_f1<S, P, L, NT, TAo, CoefIn<L, NM>, false, ragged_dispatch(0, S, P)>(A.B, A.gtab, CoefIn<L, NM>{xs}, sm);
   __syncthreads();
   stage_f2<S, P, L, NT, TAo, TBo>(A.B, A.gtab, sm);
   __syncthreads();
@@ -172,8 +177,8 @@ struct k_helm {
     double x[P1], u[Q0], v[Q0];
 #pragma unroll
     for (int p = 0; p < P1; ++p) x[p] = sm[L::at(e, TBo + (p * Q1 + j) * S2 + k)];
-    line_a0<S, P>(A.B, x, u);
-    line_d<Q0>(A.D.d0, u, v);
+    line_a0_eo<S, P>(A.B, x, u);
+    line_dd<S, P, 0>(A.D, u, v);
 #pragma unroll
     for (int i = 0; i < Q0; ++i) {
       sm[L::at(e, UO + (i * Q1 + j) * S2 + k)] = u[i];
@@ -187,7 +192,7 @@ struct k_helm {
     double u[Q1], v[Q1];
 #pragma unroll
     for (int j = 0; j < Q1; ++j) u[j] = sm[L::at(e, UO + (i * Q1 + j) * S2 + k)];
-    line_d<Q1>(A.D.d1, u, v);
+    line_dd<S, P, 1>(A.D, u, v);
 #pragma unroll
     for (int j = 0; j < Q1; ++j) sm[L::at(e, V1O + (i * Q1 + j) * S2 + k)] = v[j];
   });
@@ -200,7 +205,7 @@ struct k_helm {
     double u[Q2], w2[Q2], z[Q2];
 #pragma unroll
     for (int k = 0; k < Q2; ++k) u[k] = sm[L::at(e, UO + row + k)];
-    line_d<Q2>(A.D.d2, u, w2);  // w2 holds v2 until overwritten per point
+    line_dd<S, P, 2>(A.D, u, w2);  // w2 holds v2 until overwritten per point
     if constexpr (GEO == GEO_DEFORMED) {
       const double* g = A.pay + pay_base<PW>(live ? eg : 0, 7, NQ) + (long long)ps * PW;
       // points in chunks of CH: a compiler fence between chunks keeps ptxas
@@ -268,7 +273,7 @@ struct k_helm {
         }
       }
     }
-    line_dt_acc<Q2>(A.D.d2, w2, z);
+    line_ddt_acc<S, P, 2>(A.D, w2, z);
 #pragma unroll
     for (int k = 0; k < Q2; ++k) sm[L::at(e, UO + row + k)] = z[k];
   });
@@ -282,7 +287,7 @@ struct k_helm {
       w[j] = sm[L::at(e, V1O + (i * Q1 + j) * S2 + k)];
       r[j] = sm[L::at(e, UO + (i * Q1 + j) * S2 + k)];
     }
-    line_dt_acc<Q1>(A.D.d1, w, r);
+    line_ddt_acc<S, P, 1>(A.D, w, r);
 #pragma unroll
     for (int j = 0; j < Q1; ++j) sm[L::at(e, UO + (i * Q1 + j) * S2 + k)] = r[j];
   });
@@ -296,15 +301,15 @@ struct k_helm {
       w[i] = sm[L::at(e, V0O + (i * Q1 + j) * S2 + k)];
       r[i] = sm[L::at(e, UO + (i * Q1 + j) * S2 + k)];
     }
-    line_dt_acc<Q0>(A.D.d0, w, r);
-    line_a0t<S, P>(A.B, r, t);
+    line_ddt_acc<S, P, 0>(A.D, w, r);
+    line_a0t_eo<S, P>(A.B, r, t);
 #pragma unroll
     for (int p = 0; p < P1; ++p) sm[L::at(e, TBo + (p * Q1 + j) * S2 + k)] = t[p];
   });
   __syncthreads();
   stage_b2<S, P, L, NT, TAo, TBo>(A.B, A.gtab, sm);
   __syncthreads();
-  stage_b3<S, P, L, NT, TAo>(A.B, A.gtab, CoefOut<L, NM>{xs}, sm);
+  stage_b3<S, P, L, NT, TAo, CoefOut<L, NM>, false, ragged_dispatch(0, S, P)>(A.B, A.gtab, CoefOut<L, NM>{xs}, sm);
   __syncthreads();
   store_tile<L, NM, NT>(dst, c, xs);
   }
@@ -350,7 +355,7 @@ struct k_mass {
   double* xs = sm + L::EB * PL;  // plane 1 (TB): staging before F2 and after B2
   load_tile<L, NM, NT>(src, c, xs);
   __syncthreads();
-  stage_f1<S, P, L, NT, TAo>(A.B, A.gtab, CoefIn<L, NM>{xs}, sm);
+  stage_f1<S, P, L, NT, TAo, CoefIn<L, NM>, false, ragged_dispatch(1, S, P)>(A.B, A.gtab, CoefIn<L, NM>{xs}, sm);
   __syncthreads();
   stage_f2<S, P, L, NT, TAo, TBo>(A.B, A.gtab, sm);
   __syncthreads();
@@ -361,17 +366,17 @@ struct k_mass {
     double x[P1], u[Q0];
 #pragma unroll
     for (int p = 0; p < P1; ++p) x[p] = sm[L::at(e, TBo + (p * Q1 + j) * S2 + k)];
-    line_a0<S, P>(A.B, x, u);
+    line_a0_eo<S, P>(A.B, x, u);
 #pragma unroll
     for (int i = 0; i < Q0; ++i) u[i] *= w_at<S, P, PW, GEO>(A, eg, live, (i * Q1 + j) * Q2 + k);
-    line_a0t<S, P>(A.B, u, x);
+    line_a0t_eo<S, P>(A.B, u, x);
 #pragma unroll
     for (int p = 0; p < P1; ++p) sm[L::at(e, TBo + (p * Q1 + j) * S2 + k)] = x[p];
   });
   __syncthreads();
   stage_b2<S, P, L, NT, TAo, TBo>(A.B, A.gtab, sm);
   __syncthreads();
-  stage_b3<S, P, L, NT, TAo>(A.B, A.gtab, CoefOut<L, NM>{xs}, sm);
+  stage_b3<S, P, L, NT, TAo, CoefOut<L, NM>, false, ragged_dispatch(1, S, P)>(A.B, A.gtab, CoefOut<L, NM>{xs}, sm);
   __syncthreads();
   store_tile<L, NM, NT>(dst, c, xs);
   }
@@ -406,7 +411,7 @@ struct k_bwd {
   double* xs = sm + L::EB * PL;
   load_tile<L, NM, NT>(src, c, xs);
   __syncthreads();
-  stage_f1<S, P, L, NT, TAo>(A.B, A.gtab, CoefIn<L, NM>{xs}, sm);
+  stage_f1<S, P, L, NT, TAo, CoefIn<L, NM>, false, ragged_dispatch(2, S, P)>(A.B, A.gtab, CoefIn<L, NM>{xs}, sm);
   __syncthreads();
   stage_f2<S, P, L, NT, TAo, TBo>(A.B, A.gtab, sm);
   __syncthreads();
@@ -416,7 +421,7 @@ struct k_bwd {
     double x[P1], u[Q0];
 #pragma unroll
     for (int p = 0; p < P1; ++p) x[p] = sm[L::at(e, TBo + (p * Q1 + j) * S2 + k)];
-    line_a0<S, P>(A.B, x, u);
+    line_a0_eo<S, P>(A.B, x, u);
     if (eg < c.Epad) {
       const long long base = lane_base(eg, Dm::NQ, c.W);
 #pragma unroll
@@ -464,14 +469,14 @@ struct k_iprod {
       const int l = (i * Q1 + j) * Q2 + k;
       u[i] = live ? __ldg(src + base + (long long)l * c.W) * w_at<S, P, PW, GEO>(A, eg, live, l) : 0.0;
     }
-    line_a0t<S, P>(A.B, u, t);
+    line_a0t_eo<S, P>(A.B, u, t);
 #pragma unroll
     for (int p = 0; p < P1; ++p) sm[L::at(e, TBo + (p * Q1 + j) * S2 + k)] = t[p];
   });
   __syncthreads();
   stage_b2<S, P, L, NT, TAo, TBo>(A.B, A.gtab, sm);
   __syncthreads();
-  stage_b3<S, P, L, NT, TAo>(A.B, A.gtab, CoefOut<L, NM>{xs}, sm);
+  stage_b3<S, P, L, NT, TAo, CoefOut<L, NM>, false, ragged_dispatch(2, S, P)>(A.B, A.gtab, CoefOut<L, NM>{xs}, sm);
   __syncthreads();
   store_tile<L, NM, NT>(dst, c, xs);
   }
@@ -509,7 +514,7 @@ struct k_pderiv {
     const long long base = lane_base(live ? eg : 0, NQ, c.W);
 #pragma unroll
     for (int i = 0; i < Q0; ++i) u[i] = live ? __ldg(A.in + base + (long long)((i * Q1 + j) * Q2 + k) * c.W) : 0.0;
-    line_d<Q0>(A.D.d0, u, v);
+    line_dd<S, P, 0>(A.D, u, v);
 #pragma unroll
     for (int i = 0; i < Q0; ++i) {
       sm[L::at(e, UO + (i * Q1 + j) * S2 + k)] = u[i];
@@ -522,7 +527,7 @@ struct k_pderiv {
     double u[Q1], v[Q1];
 #pragma unroll
     for (int j = 0; j < Q1; ++j) u[j] = sm[L::at(e, UO + (i * Q1 + j) * S2 + k)];
-    line_d<Q1>(A.D.d1, u, v);
+    line_dd<S, P, 1>(A.D, u, v);
 #pragma unroll
     for (int j = 0; j < Q1; ++j) sm[L::at(e, V1O + (i * Q1 + j) * S2 + k)] = v[j];
   });
@@ -535,7 +540,7 @@ struct k_pderiv {
     double u[Q2], v2[Q2];
 #pragma unroll
     for (int k = 0; k < Q2; ++k) u[k] = sm[L::at(e, UO + row + k)];
-    line_d<Q2>(A.D.d2, u, v2);
+    line_dd<S, P, 2>(A.D, u, v2);
     const long long base = lane_base(eg, NQ, c.W);
     const long long cs = A.out_cstride;
 #pragma unroll
@@ -617,7 +622,7 @@ struct k_ipderiv {
       w2[k] = live ? __ldg(A.in + 2 * cs + a) * wq : 0.0;
       r[k] = 0.0;
     }
-    line_dt_acc<Q2>(A.D.d2, w2, r);
+    line_ddt_acc<S, P, 2>(A.D, w2, r);
 #pragma unroll
     for (int k = 0; k < Q2; ++k) sm[L::at(e, UO + row + k)] = r[k];
   });
@@ -630,7 +635,7 @@ struct k_ipderiv {
       w[j] = sm[L::at(e, V1O + (i * Q1 + j) * S2 + k)];
       r[j] = sm[L::at(e, UO + (i * Q1 + j) * S2 + k)];
     }
-    line_dt_acc<Q1>(A.D.d1, w, r);
+    line_ddt_acc<S, P, 1>(A.D, w, r);
 #pragma unroll
     for (int j = 0; j < Q1; ++j) sm[L::at(e, UO + (i * Q1 + j) * S2 + k)] = r[j];
   });
@@ -643,15 +648,15 @@ struct k_ipderiv {
       w[i] = sm[L::at(e, V0O + (i * Q1 + j) * S2 + k)];
       r[i] = sm[L::at(e, UO + (i * Q1 + j) * S2 + k)];
     }
-    line_dt_acc<Q0>(A.D.d0, w, r);
-    line_a0t<S, P>(A.B, r, t);
+    line_ddt_acc<S, P, 0>(A.D, w, r);
+    line_a0t_eo<S, P>(A.B, r, t);
 #pragma unroll
     for (int p = 0; p < P1; ++p) sm[L::at(e, TBo + (p * Q1 + j) * S2 + k)] = t[p];
   });
   __syncthreads();
   stage_b2<S, P, L, NT, TAo, TBo>(A.B, A.gtab, sm);
   __syncthreads();
-  stage_b3<S, P, L, NT, TAo>(A.B, A.gtab, CoefOut<L, NM>{xs}, sm);
+  stage_b3<S, P, L, NT, TAo, CoefOut<L, NM>, false, ragged_dispatch(2, S, P)>(A.B, A.gtab, CoefOut<L, NM>{xs}, sm);
   __syncthreads();
   store_tile<L, NM, NT>(A.out, c, xs);
   }
@@ -679,7 +684,7 @@ struct k_helm_nc {
   __device__ static void prefetch_geo(const A_t& A, long long t) {
     const long long e0 = t * EB;
     const long long n = A.E - e0 < EB ? A.E - e0 : EB;
-    if constexpr (GEO == GEO_DEFORMED) prefetch_payload<PW>(A.pay, e0, n, A.E, LAMW ? 7 : 6, Dims<S, P>::NQ);
+    if constexpr (GEO == GEO_DEFORMED) prefetch_payload<PW>(A.pay, e0, n, A.E, 7, Dims<S, P>::NQ, LAMW ? 7 : 6);
   }
   __device__ static void prefetch_in(const A_t& A, long long t) {
     const long long e0 = t * EB;

@@ -31,6 +31,9 @@ namespace sk {
 // kPrismUniformMaxP and one per (element, p, q) pair above it.
 constexpr int kTetDispatchMaxP = 9;
 constexpr int kPrismUniformMaxP = 8;
+// pyr/tet r <-> k sweeps (slice c2[max(p,q)] / c2[p+q] varies per item):
+// compile-time slice dispatch (RD = true) or L1 table reads; chosen per
+// operator class (sk_tune.h kRaggedMaxP)
 
 // ---- coefficient tile staging ----------------------------------------------
 // xs[m * XSTR + e] <-> field value of mode m of element e0 + e; iteration order
@@ -94,11 +97,198 @@ struct CoefOut {
   }
 };
 
+// ---- F3 core: p -> i for one (j,k) line ------------------------------------
+template <int S, int P>
+__device__ __forceinline__ void line_a0(const FwdTab<S, P>& B, const double (&x)[P + 1],
+                                        double (&u)[Dims<S, P>::Q0]) {
+  using Dm = Dims<S, P>;
+#pragma unroll
+  for (int i = 0; i < Dm::Q0; ++i) {
+    double s = B.a0[i * Dm::P1] * x[0];
+#pragma unroll
+    for (int p = 1; p < Dm::P1; ++p) s = fma(B.a0[i * Dm::P1 + p], x[p], s);
+    u[i] = s;
+  }
+}
+
+// transposed p <- i for one (j,k) line
+template <int S, int P>
+__device__ __forceinline__ void line_a0t(const FwdTab<S, P>& B, const double (&r)[Dims<S, P>::Q0],
+                                         double (&t)[P + 1]) {
+  using Dm = Dims<S, P>;
+#pragma unroll
+  for (int p = 0; p < Dm::P1; ++p) {
+    double s = B.a0[p] * r[0];
+#pragma unroll
+    for (int i = 1; i < Dm::Q0; ++i) s = fma(B.a0[i * Dm::P1 + p], r[i], s);
+    t[p] = s;
+  }
+}
+
+// v = D u along a line of length Q (D row-major Q x Q)
+template <int Q>
+__device__ __forceinline__ void line_d(const double* D, const double (&u)[Q], double (&v)[Q]) {
+#pragma unroll
+  for (int a = 0; a < Q; ++a) {
+    double s = D[a * Q] * u[0];
+#pragma unroll
+    for (int b = 1; b < Q; ++b) s = fma(D[a * Q + b], u[b], s);
+    v[a] = s;
+  }
+}
+
+// r += D^T w along a line
+template <int Q>
+__device__ __forceinline__ void line_dt_acc(const double* D, const double (&w)[Q], double (&r)[Q]) {
+#pragma unroll
+  for (int a = 0; a < Q; ++a) {
+    double s = r[a];
+#pragma unroll
+    for (int b = 0; b < Q; ++b) s = fma(D[b * Q + a], w[b], s);
+    r[a] = s;
+  }
+}
+
+// ---- even-odd 1D contractions along Gauss-Lobatto directions -------------
+// (see gll_dir): half the multiply-adds of the plain forms above.
+
+// u[i] = sum_p B[i][p] x[p] for a full modified-basis family B (Q x P1)
+template <int Q, int P1>
+__device__ __forceinline__ void line_b_eo(const double* B, const double* bp, const double* bm, const double (&x)[P1],
+                                          double (&u)[Q]) {
+  constexpr int H = Q / 2;
+  const double xs = x[0] + x[1], xd = x[0] - x[1];
+#pragma unroll
+  for (int i = 0; i < (Q + 1) / 2; ++i) {
+    double pe = bp[i] * xs;
+#pragma unroll
+    for (int p = 2; p < P1; p += 2) pe = fma(B[i * P1 + p], x[p], pe);
+    if (i < H) {
+      double po = bm[i] * xd;
+#pragma unroll
+      for (int p = 3; p < P1; p += 2) po = fma(B[i * P1 + p], x[p], po);
+      u[i] = pe + po;
+      u[Q - 1 - i] = pe - po;
+    } else {
+      u[i] = pe;  // middle point: the odd modes vanish there
+    }
+  }
+}
+
+// t[p] = sum_i B[i][p] r[i]
+template <int Q, int P1>
+__device__ __forceinline__ void line_bt_eo(const double* B, const double* bp, const double* bm, const double (&r)[Q],
+                                           double (&t)[P1]) {
+  constexpr int H = Q / 2;
+  double re[H], ro[H];
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    re[i] = r[i] + r[Q - 1 - i];
+    ro[i] = r[i] - r[Q - 1 - i];
+  }
+  double sp = bp[0] * re[0], sm = bm[0] * ro[0];
+#pragma unroll
+  for (int i = 1; i < H; ++i) {
+    sp = fma(bp[i], re[i], sp);
+    sm = fma(bm[i], ro[i], sm);
+  }
+  if constexpr (Q % 2) sp = fma(bp[H], r[H], sp);
+  t[0] = sp + sm;
+  t[1] = sp - sm;
+#pragma unroll
+  for (int p = 2; p < P1; ++p) {
+    double s;
+    if (p % 2 == 0) {
+      s = B[p] * re[0];
+#pragma unroll
+      for (int i = 1; i < H; ++i) s = fma(B[i * P1 + p], re[i], s);
+      if constexpr (Q % 2) s = fma(B[H * P1 + p], r[H], s);
+    } else {
+      s = B[p] * ro[0];
+#pragma unroll
+      for (int i = 1; i < H; ++i) s = fma(B[i * P1 + p], ro[i], s);
+    }
+    t[p] = s;
+  }
+}
+
+// v = M u (ACC: r += M u) for a centro-antisymmetric M in even-odd form
+template <int Q, bool ACC>
+__device__ __forceinline__ void line_m_eo(const EOTab<Q>& T, const double (&u)[Q], double (&v)[Q]) {
+  constexpr int H = Q / 2;
+  double e[H], o[H];
+#pragma unroll
+  for (int b = 0; b < H; ++b) {
+    e[b] = u[b] + u[Q - 1 - b];
+    o[b] = u[b] - u[Q - 1 - b];
+  }
+#pragma unroll
+  for (int a = 0; a < H; ++a) {
+    double pe = T.E[a * H] * e[0], po = T.O[a * H] * o[0];
+#pragma unroll
+    for (int b = 1; b < H; ++b) {
+      pe = fma(T.E[a * H + b], e[b], pe);
+      po = fma(T.O[a * H + b], o[b], po);
+    }
+    if constexpr (Q % 2) pe = fma(T.Em[a], u[H], pe);
+    if constexpr (ACC) {
+      v[a] += pe + po;
+      v[Q - 1 - a] += po - pe;
+    } else {
+      v[a] = pe + po;
+      v[Q - 1 - a] = po - pe;
+    }
+  }
+  if constexpr (Q % 2) {
+    double s = T.Om[0] * o[0];
+#pragma unroll
+    for (int b = 1; b < H; ++b) s = fma(T.Om[b], o[b], s);
+    if constexpr (ACC)
+      v[H] += s;
+    else
+      v[H] = s;
+  }
+}
+
+// collocation derivative along direction DIR: v = D u, and r += D^T w
+template <int S, int P, int DIR, int Q>
+__device__ __forceinline__ void line_dd(const DTab<S, P>& D, const double (&u)[Q], double (&v)[Q]) {
+  if constexpr (DIR == 0) {
+    line_m_eo<Q, false>(D.e0, u, v);
+  } else if constexpr (DIR == 1) {
+    if constexpr (gll_dir(S, 1)) line_m_eo<Q, false>(D.e1, u, v); else line_d<Q>(D.d1, u, v);
+  } else {
+    if constexpr (gll_dir(S, 2)) line_m_eo<Q, false>(D.e2, u, v); else line_d<Q>(D.d2, u, v);
+  }
+}
+
+template <int S, int P, int DIR, int Q>
+__device__ __forceinline__ void line_ddt_acc(const DTab<S, P>& D, const double (&w)[Q], double (&r)[Q]) {
+  if constexpr (DIR == 0) {
+    line_m_eo<Q, true>(D.e0t, w, r);
+  } else if constexpr (DIR == 1) {
+    if constexpr (gll_dir(S, 1)) line_m_eo<Q, true>(D.e1t, w, r); else line_dt_acc<Q>(D.d1, w, r);
+  } else {
+    if constexpr (gll_dir(S, 2)) line_m_eo<Q, true>(D.e2t, w, r); else line_dt_acc<Q>(D.d2, w, r);
+  }
+}
+
+// dir-0 value contractions in even-odd form (value tables only)
+template <int S, int P>
+__device__ __forceinline__ void line_a0_eo(const FwdTab<S, P>& B, const double (&x)[P + 1], double (&u)[Dims<S, P>::Q0]) {
+  line_b_eo<Dims<S, P>::Q0, P + 1>(B.a0, B.a0p, B.a0m, x, u);
+}
+
+template <int S, int P>
+__device__ __forceinline__ void line_a0t_eo(const FwdTab<S, P>& B, const double (&r)[Dims<S, P>::Q0], double (&t)[P + 1]) {
+  line_bt_eo<Dims<S, P>::Q0, P + 1>(B.a0, B.a0p, B.a0m, r, t);
+}
+
 // ---- F1: r -> k.  TA[p][q][k] = sum_r C_(p,q)[k][r] uhat[p,q,r] ----------
 // DER2: the dir-2 family is the derivative one (reference dmode == 2; the
 // caller passes the derivative FwdTab for hex/prism, the device buffer's DC2
 // slices are used for pyr/tet)
-template <int S, int P, class L, int NT, int TAo, class In, bool DER2 = false>
+template <int S, int P, class L, int NT, int TAo, class In, bool DER2 = false, bool RD = false>
 __device__ __forceinline__ void stage_f1(const FwdTab<S, P>& B, const double* __restrict__ gtab, const In& xin,
                                          double* sm) {
   using Dm = Dims<S, P>;
@@ -108,12 +298,19 @@ __device__ __forceinline__ void stage_f1(const FwdTab<S, P>& B, const double* __
       double x[P1];
 #pragma unroll
       for (int r = 0; r < P1; ++r) x[r] = xin(e, ps * P1 + r);
+      if constexpr (!DER2) {
+        double u[Q2];
+        line_b_eo<Q2, P1>(B.a2, B.a2p, B.a2m, x, u);
 #pragma unroll
-      for (int k = 0; k < Q2; ++k) {
-        double s = B.a2[k * P1] * x[0];
+        for (int k = 0; k < Q2; ++k) sm[L::at(e, TAo + ps * S2 + k)] = u[k];
+      } else {
 #pragma unroll
-        for (int r = 1; r < P1; ++r) s = fma(B.a2[k * P1 + r], x[r], s);
-        sm[L::at(e, TAo + ps * S2 + k)] = s;
+        for (int k = 0; k < Q2; ++k) {
+          double s = B.a2[k * P1] * x[0];
+#pragma unroll
+          for (int r = 1; r < P1; ++r) s = fma(B.a2[k * P1 + r], x[r], s);
+          sm[L::at(e, TAo + ps * S2 + k)] = s;
+        }
       }
     });
   } else if constexpr (S == PRISM && P <= kPrismUniformMaxP) {
@@ -140,6 +337,36 @@ __device__ __forceinline__ void stage_f1(const FwdTab<S, P>& B, const double* __
         }
         off += P1 * n;
       }
+    });
+  } else if constexpr (S != PRISM && RD) {
+    // pyr / tet: item = (e, (p,q) pair), pairs ordered by slice; the slice
+    // m = max(p,q) (pyr) or p+q (tet) is dispatched to a compile-time
+    // constant so c2[m] entries are uniform operands (operators.py:209-351)
+    const int4* pairs = reinterpret_cast<const int4*>(gtab + GLayout<S, P>::PAIRS);
+    items<L, Dm::NPAIR, NT>([&](int e, int ps) {
+      const int4 pr = __ldg(pairs + ps);  // p, q, mode offset, nr
+      dispatch<0, P1>(P1 - pr.w, [&](auto mc) {
+        constexpr int m = decltype(mc)::value;
+        constexpr int n = P1 - m;
+        constexpr int co = wfam_off(Q2, P1, m);
+        double x[n];
+#pragma unroll
+        for (int r = 0; r < n; ++r) x[r] = xin(e, pr.z + r);
+#pragma unroll
+        for (int k = 0; k < Q2; ++k) {
+          double s = B.c2[co + k * n] * x[0];
+#pragma unroll
+          for (int r = 1; r < n; ++r) s = fma(B.c2[co + k * n + r], x[r], s);
+          sm[L::at(e, TAo + (pr.x * P1 + pr.y) * S2 + k)] = s;
+        }
+        if constexpr (m == 0) {
+          if (pr.x == 0 && pr.y == 0) {
+            // collapsed apex mode (0,0,1): Y[k] = c2[0][k][1] * uhat[0,0,1]
+#pragma unroll
+            for (int k = 0; k < Q2; ++k) sm[L::at(e, TAo + P1 * P1 * S2 + k)] = B.c2[k * P1 + 1] * x[1];
+          }
+        }
+      });
     });
   } else {
     // prism / pyr / tet: item = (e, (p,q) pair); the dir-2 slice c2[p]
@@ -193,6 +420,23 @@ __device__ __forceinline__ void stage_f2(const FwdTab<S, P>& B, const double* __
       for (int q = 0; q < P1; ++q) x[q] = sm[L::at(e, TAo + (p * P1 + q) * S2 + k)];
       double y = 0.0;
       if constexpr (S == PYR) y = sm[L::at(e, TAo + P1 * P1 * S2 + k)];
+      if constexpr (!DER1) {
+        // apex shares (operators.py:335-349): a1[j][1] y into p = 0, y into p = 1
+        if constexpr (S == PYR) {
+          if (p == 0) x[1] += y;
+        }
+        double u[Q1];
+        line_b_eo<Q1, P1>(B.a1, B.a1p, B.a1m, x, u);
+#pragma unroll
+        for (int j = 0; j < Q1; ++j) {
+          double s = u[j];
+          if constexpr (S == PYR) {
+            if (p == 1) s += y;
+          }
+          sm[L::at(e, TBo + (p * Q1 + j) * S2 + k)] = s;
+        }
+        return;
+      }
 #pragma unroll
       for (int j = 0; j < Q1; ++j) {
         double s = B.a1[j * P1] * x[0];
@@ -270,58 +514,6 @@ __device__ __forceinline__ void stage_f2(const FwdTab<S, P>& B, const double* __
   }
 }
 
-// ---- F3 core: p -> i for one (j,k) line ------------------------------------
-template <int S, int P>
-__device__ __forceinline__ void line_a0(const FwdTab<S, P>& B, const double (&x)[P + 1],
-                                        double (&u)[Dims<S, P>::Q0]) {
-  using Dm = Dims<S, P>;
-#pragma unroll
-  for (int i = 0; i < Dm::Q0; ++i) {
-    double s = B.a0[i * Dm::P1] * x[0];
-#pragma unroll
-    for (int p = 1; p < Dm::P1; ++p) s = fma(B.a0[i * Dm::P1 + p], x[p], s);
-    u[i] = s;
-  }
-}
-
-// transposed p <- i for one (j,k) line
-template <int S, int P>
-__device__ __forceinline__ void line_a0t(const FwdTab<S, P>& B, const double (&r)[Dims<S, P>::Q0],
-                                         double (&t)[P + 1]) {
-  using Dm = Dims<S, P>;
-#pragma unroll
-  for (int p = 0; p < Dm::P1; ++p) {
-    double s = B.a0[p] * r[0];
-#pragma unroll
-    for (int i = 1; i < Dm::Q0; ++i) s = fma(B.a0[i * Dm::P1 + p], r[i], s);
-    t[p] = s;
-  }
-}
-
-// v = D u along a line of length Q (D row-major Q x Q)
-template <int Q>
-__device__ __forceinline__ void line_d(const double* D, const double (&u)[Q], double (&v)[Q]) {
-#pragma unroll
-  for (int a = 0; a < Q; ++a) {
-    double s = D[a * Q] * u[0];
-#pragma unroll
-    for (int b = 1; b < Q; ++b) s = fma(D[a * Q + b], u[b], s);
-    v[a] = s;
-  }
-}
-
-// r += D^T w along a line
-template <int Q>
-__device__ __forceinline__ void line_dt_acc(const double* D, const double (&w)[Q], double (&r)[Q]) {
-#pragma unroll
-  for (int a = 0; a < Q; ++a) {
-    double s = r[a];
-#pragma unroll
-    for (int b = 0; b < Q; ++b) s = fma(D[b * Q + a], w[b], s);
-    r[a] = s;
-  }
-}
-
 // ---- B2: j -> q.  TA[p][q][k] = sum_j B_p[j][q] TB[p][j][k] ---------------
 // DER1: derivative dir-1 family (transposed dmode == 1, apex "ones" share
 // vanishes); ACC: add into TA and the spare rows instead of overwriting
@@ -335,13 +527,23 @@ __device__ __forceinline__ void stage_b2(const FwdTab<S, P>& B, const double* __
       double x[Q1];
 #pragma unroll
       for (int j = 0; j < Q1; ++j) x[j] = sm[L::at(e, TBo + (p * Q1 + j) * S2 + k)];
+      if constexpr (!DER1) {
+        double t[P1];
+        line_bt_eo<Q1, P1>(B.a1, B.a1p, B.a1m, x, t);
 #pragma unroll
-      for (int q = 0; q < P1; ++q) {
-        double s = B.a1[q] * x[0];
+        for (int q = 0; q < P1; ++q) {
+          double& d = sm[L::at(e, TAo + (p * P1 + q) * S2 + k)];
+          d = ACC ? d + t[q] : t[q];
+        }
+      } else {
 #pragma unroll
-        for (int j = 1; j < Q1; ++j) s = fma(B.a1[j * P1 + q], x[j], s);
-        double& t = sm[L::at(e, TAo + (p * P1 + q) * S2 + k)];
-        t = ACC ? t + s : s;
+        for (int q = 0; q < P1; ++q) {
+          double s = B.a1[q] * x[0];
+#pragma unroll
+          for (int j = 1; j < Q1; ++j) s = fma(B.a1[j * P1 + q], x[j], s);
+          double& t = sm[L::at(e, TAo + (p * P1 + q) * S2 + k)];
+          t = ACC ? t + s : s;
+        }
       }
       if constexpr (S == PYR) {
         if (p == 1) {  // Y[k] = sum_j TB[1][j][k] (apex share, operators.py:371)
@@ -432,7 +634,7 @@ __device__ __forceinline__ void stage_b2(const FwdTab<S, P>& B, const double* __
 // ---- B3: k -> r, produce coefficients ----------------------------------------
 // DER2: derivative dir-2 family (transposed dmode == 2); accumulation into
 // the output is the Out functor's business
-template <int S, int P, class L, int NT, int TAo, class Out, bool DER2 = false>
+template <int S, int P, class L, int NT, int TAo, class Out, bool DER2 = false, bool RD = false>
 __device__ __forceinline__ void stage_b3(const FwdTab<S, P>& B, const double* __restrict__ gtab, const Out& out,
                                          const double* sm) {
   using Dm = Dims<S, P>;
@@ -442,12 +644,19 @@ __device__ __forceinline__ void stage_b3(const FwdTab<S, P>& B, const double* __
       double x[Q2];
 #pragma unroll
       for (int k = 0; k < Q2; ++k) x[k] = sm[L::at(e, TAo + ps * S2 + k)];
+      if constexpr (!DER2) {
+        double t[P1];
+        line_bt_eo<Q2, P1>(B.a2, B.a2p, B.a2m, x, t);
 #pragma unroll
-      for (int r = 0; r < P1; ++r) {
-        double s = B.a2[r] * x[0];
+        for (int r = 0; r < P1; ++r) out(e, ps * P1 + r, t[r]);
+      } else {
 #pragma unroll
-        for (int k = 1; k < Q2; ++k) s = fma(B.a2[k * P1 + r], x[k], s);
-        out(e, ps * P1 + r, s);
+        for (int r = 0; r < P1; ++r) {
+          double s = B.a2[r] * x[0];
+#pragma unroll
+          for (int k = 1; k < Q2; ++k) s = fma(B.a2[k * P1 + r], x[k], s);
+          out(e, ps * P1 + r, s);
+        }
       }
     });
   } else if constexpr (S == PRISM && P <= kPrismUniformMaxP) {
@@ -479,6 +688,44 @@ __device__ __forceinline__ void stage_b3(const FwdTab<S, P>& B, const double* __
         }
         off += P1 * n;
       }
+    });
+  } else if constexpr (S != PRISM && RD) {
+    // pyr / tet with the slice dispatched to a compile-time constant
+    const int4* pairs = reinterpret_cast<const int4*>(gtab + GLayout<S, P>::PAIRS);
+    items<L, Dm::NPAIR, NT>([&](int e, int ps) {
+      const int4 pr = __ldg(pairs + ps);
+      double x[Q2];
+#pragma unroll
+      for (int k = 0; k < Q2; ++k) x[k] = sm[L::at(e, TAo + (pr.x * P1 + pr.y) * S2 + k)];
+      if constexpr (S == TET) {
+        if (pr.x == 0 && pr.y == 1) {
+#pragma unroll
+          for (int k = 0; k < Q2; ++k) x[k] += sm[L::at(e, TAo + (P1 * P1 + 1) * S2 + k)];
+        }
+      }
+      dispatch<0, P1>(P1 - pr.w, [&](auto mc) {
+        constexpr int m = decltype(mc)::value;
+        constexpr int n = P1 - m;
+        constexpr int co = wfam_off(Q2, P1, m);
+        double apex = 0.0;
+        if constexpr (m == 0) {
+          if (pr.x == 0 && pr.y == 0) {
+#pragma unroll
+            for (int k = 0; k < Q2; ++k) {
+              const double y = sm[L::at(e, TAo + P1 * P1 * S2 + k)] + sm[L::at(e, TAo + (0 * P1 + 1) * S2 + k)];
+              apex = fma(B.c2[k * P1 + 1], y, apex);
+            }
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < n; ++r) {
+          double s = B.c2[co + r] * x[0];
+#pragma unroll
+          for (int k = 1; k < Q2; ++k) s = fma(B.c2[co + k * n + r], x[k], s);
+          if (r == 1) s += apex;
+          out(e, pr.z + r, s);
+        }
+      });
     });
   } else {
     const int4* pairs = reinterpret_cast<const int4*>(gtab + GLayout<S, P>::PAIRS);

@@ -1,14 +1,27 @@
 #!/bin/bash
-# Build tuning variants of libsk200 (Helmholtz kernels only):
-#   tools/build_variants.sh eb16_nt1_mb0 eb8_nt2_mb1 ...
+# Build tuning variants of libsk200 restricted to one operator class:
+#   tools/build_variants.sh op0_eb8_nt1_mb1_cap4 op1_eb16_nt2_mb1_cap8_rd9 ...
+# keys: op (0 Helmholtz/stiffness, 1 mass), eb (tile elements), nt (thread
+# divisor), mb (min-blocks rule on/off), cap (CTAs/SM cap), rd (ragged
+# dispatch max order); omitted keys keep the sk_tune.h tables.
 # -> paper_2604_04644_b200/libsk200_<name>.so, used by tools/tune_eb.py.
 set -e
 cd "$(dirname "$0")/../paper_2604_04644_b200/csrc"
 for v in "$@"; do
-  eb=$(echo "$v" | sed -E 's/eb([0-9]+)_nt([0-9]+)_mb([0-9]+)/\1/')
-  nt=$(echo "$v" | sed -E 's/eb([0-9]+)_nt([0-9]+)_mb([0-9]+)/\2/')
-  mb=$(echo "$v" | sed -E 's/eb([0-9]+)_nt([0-9]+)_mb([0-9]+)/\3/')
-  make -j"$(nproc)" BUILD=/tmp/sk200_build_$v LIB=../libsk200_$v.so LINEINFO= \
-    EXTRA="-DSK_ONLY_HELM -DSK_EB_FIXED=$eb -DSK_NT_DIV=$nt -DSK_MINB=$mb" > /dev/null 2>&1
-  echo "built libsk200_$v.so"
+  extra=""
+  for kv in ${v//_/ }; do
+    k=$(echo "$kv" | sed -E 's/^([a-z]+)[0-9]+$/\1/')
+    n=$(echo "$kv" | sed -E 's/^[a-z]+([0-9]+)$/\1/')
+    case $k in
+      op) extra="$extra -DSK_ONLY_OP=$n" ;;
+      eb) extra="$extra -DSK_EB_FIXED=$n" ;;
+      nt) extra="$extra -DSK_NT_DIV=$n" ;;
+      mb) extra="$extra -DSK_MINB=$n" ;;
+      cap) extra="$extra -DSK_MINB_CAP=$n" ;;
+      rd) extra="$extra -DSK_RAGGED_MAXP=$n" ;;
+      pd) extra="$extra -DSK_GEO_PD=$n" ;;
+    esac
+  done
+  make -j"$(nproc)" BUILD=/tmp/sk200_build_$v LIB=../libsk200_$v.so LINEINFO= EXTRA="$extra" > /tmp/sk200_build_$v.log 2>&1 \
+    && echo "built libsk200_$v.so ($extra)" || { echo "FAILED $v"; tail -5 /tmp/sk200_build_$v.log; }
 done

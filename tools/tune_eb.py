@@ -18,18 +18,20 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--variants", default="eb16_nt1_mb0,eb8_nt1_mb0,eb4_nt1_mb0,eb2_nt1_mb0,eb1_nt1_mb0")
+    ap.add_argument("--variants", default="op0_eb16,op0_eb8,op0_eb4,op0_eb2,op0_eb1")
     ap.add_argument("--ops", default="helm")
     ap.add_argument("--orders", default="1-10")
+    ap.add_argument("--shapes", default="hex,prism,pyr,tet")
     ap.add_argument("--gbytes", default="1.0")
     ap.add_argument("--reps", default="8")
     a = ap.parse_args()
     best = {}
     for v in a.variants.split(","):
         lib = os.path.join(ROOT, "paper_2604_04644_b200", f"libsk200_{v}.so")
-        eb_, nt_, mb_ = (int(t[2:]) for t in v.split("_"))
+        kv = {t.rstrip("0123456789"): int(t[len(t.rstrip("0123456789")):]) for t in v.split("_")}
+        nt_, mb_ = kv.get("nt", 0), kv.get("mb", -1)
         env = dict(os.environ, SK200_LIB=lib)
-        cmd = [sys.executable, os.path.join(ROOT, "tools", "sweep.py"), "--ops", a.ops, "--orders", a.orders,
+        cmd = [sys.executable, os.path.join(ROOT, "tools", "sweep.py"), "--ops", a.ops, "--orders", a.orders, "--shapes", a.shapes,
                "--gbytes", a.gbytes, "--reps", a.reps]
         out = subprocess.run(cmd, env=env, capture_output=True, text=True)
         if out.returncode:
