@@ -113,6 +113,24 @@ int sk_mass_apply(const sk_basis* b, int geo_class, int64_t E, int W, int ncomp,
 int sk_helmholtz_apply(const sk_basis* b, int geo_class, int form, int64_t E, int W, int ncomp,
                        const double* uhat, const double* hpay, double lam, double* out, void* stream);
 
+/* ---- host-buffer applies with transfer/compute overlap ----------------------
+ * The reference's callers hold their blocks in host memory (field_block.py:
+ * 67-149 MemoryRegion HOST space).  sk_apply_streamed runs a coefficient ->
+ * coefficient operator on host input and returns host output, pipelined over
+ * element chunks: H2D of chunk i+1, the kernel on chunk i and D2H of chunk
+ * i-1 run concurrently (two internal copy streams + the caller's stream).
+ * host_in/host_out should be pinned (page-locked) for the copies to overlap;
+ * dev_in/dev_out are the caller's device buffers of the full block (both
+ * hold the block afterwards), pay is the device payload of the operator.
+ * Stream-ordered: host_out is complete when `stream` reaches this point.
+ * op: SK_STREAM_HELMHOLTZ (payload HELMHOLTZ, lam >= 0), SK_STREAM_HELMHOLTZ_NC
+ * (payload HELMHOLTZ_NC), SK_STREAM_MASS (payload W, lam ignored).
+ * chunk_elements <= 0 picks a default (~16 chunks). */
+enum { SK_STREAM_HELMHOLTZ = 0, SK_STREAM_HELMHOLTZ_NC = 1, SK_STREAM_MASS = 2 };
+int sk_apply_streamed(const sk_basis* b, int op, int geo_class, int64_t E, int W, int ncomp,
+                      const double* host_in, double* dev_in, const double* pay, double lam, double* dev_out,
+                      double* host_out, int64_t chunk_elements, void* stream);
+
 /* ---- assembled C0 variant (hex, conforming, axis-aligned) --------
  * No reference counterpart (global assembly is outside speckern, SPEC.md:8,
  * 452).  Mesh nx x ny x nz_local element slab, e = (ez*ny + ey)*nx + ex; the

@@ -19,6 +19,7 @@ SK_OK, SK_ERR_STATE, SK_ERR_UNSUPPORTED, SK_ERR_ARG, SK_ERR_CUDA = range(5)
 SK_GEO_REGULAR, SK_GEO_DEFORMED = 0, 1
 SK_PAYLOAD_HELMHOLTZ, SK_PAYLOAD_W, SK_PAYLOAD_DERIV, SK_PAYLOAD_HELMHOLTZ_NC = 0, 1, 2, 3
 SK_FORM_COLL, SK_FORM_NONCOLL = 0, 1
+SK_STREAM_HELMHOLTZ, SK_STREAM_HELMHOLTZ_NC, SK_STREAM_MASS = 0, 1, 2
 
 #: every exported symbol and its (restype, argtypes)
 _P = ctypes.c_void_p
@@ -43,6 +44,7 @@ SIGNATURES = {
     "sk_iproduct_wrt_deriv_base": (_I, [_P, _I, _L, _I, _P, _P, _P, _P]),
     "sk_mass_apply": (_I, [_P, _I, _L, _I, _I, _P, _P, _P, _P]),
     "sk_helmholtz_apply": (_I, [_P, _I, _I, _L, _I, _I, _P, _P, _D, _P, _P]),
+    "sk_apply_streamed": (_I, [_P, _I, _I, _L, _I, _I, _P, _P, _P, _D, _P, _P, _L, _P]),
     "sk_c0_gather": (_I, [_I, _I, _I, _L, _P, _I, _P, _P]),
     "sk_c0_scatter": (_I, [_I, _I, _I, _L, _P, _I, _P, _P]),
     "sk_launch_count": (_L, []),
@@ -67,7 +69,10 @@ def load() -> ctypes.CDLL:
                     "(python -c 'import __graft_entry__ as g; g.build()')"
                 )
             lib = ctypes.CDLL(LIB_PATH)
+            variant = "SK200_LIB" in os.environ  # tuning builds may predate newer entry points
             for name, (res, args) in SIGNATURES.items():
+                if variant and not hasattr(lib, name):
+                    continue
                 fn = getattr(lib, name)
                 fn.restype = res
                 fn.argtypes = args

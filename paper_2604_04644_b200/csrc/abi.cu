@@ -6,6 +6,7 @@
 #include <cstring>
 #include <memory>
 #include <mutex>
+#include <algorithm>
 #include <string>
 #include <vector>
 
@@ -197,7 +198,7 @@ int sk_payload_size(const sk_basis* b, int geo_class, int kind, int64_t E, int64
   if (geo_class != SK_GEO_REGULAR && geo_class != SK_GEO_DEFORMED) return fail(SK_ERR_ARG, "bad geometry class");
   if (kind < 0 || kind > 3) return fail(SK_ERR_ARG, "bad payload kind");
   if (E < 0) return fail(SK_ERR_ARG, "element count must be nonnegative");
-  *n = b->ops->payload_doubles(kind, geo_class) * b->ops->payload_elements(E);
+  *n = b->ops->payload_doubles(kind, geo_class) * b->ops->payload_elements(kind, E);
   return SK_OK;
 }
 
@@ -308,6 +309,118 @@ int sk_helmholtz_apply(const sk_basis* b, int geo, int form, int64_t E, int W, i
   if (int st = check_layout(E, W, ncomp)) return st;
   return run(const_cast<sk_basis*>(b), form == SK_FORM_NONCOLL ? sk::OP_HELM_NC : sk::OP_HELM, geo, E, W, ncomp, uhat,
              out, hpay, lam, b->hb.nm, b->hb.nm, stream);
+}
+
+namespace {
+long long gcd_ll(long long a, long long b) { return b ? gcd_ll(b, a % b) : a; }
+
+// per-thread copy streams of the streamed applies (one pair per device)
+struct CopyStreams {
+  int dev = -1;
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+};
+thread_local CopyStreams g_cs;
+
+int copy_streams(cudaStream_t* h2d, cudaStream_t* d2h) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_status(e, "cudaGetDevice");
+  if (g_cs.dev != dev) {
+    // streams of another device are simply abandoned (device switches are rare)
+    g_cs = CopyStreams();
+    e = cudaStreamCreateWithFlags(&g_cs.h2d, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&g_cs.d2h, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return cuda_status(e, "copy stream creation");
+    g_cs.dev = dev;
+  }
+  *h2d = g_cs.h2d;
+  *d2h = g_cs.d2h;
+  return SK_OK;
+}
+}  // namespace
+
+int sk_apply_streamed(const sk_basis* b, int op, int geo, int64_t E, int W, int ncomp, const double* host_in,
+                      double* dev_in, const double* pay, double lam, double* dev_out, double* host_out,
+                      int64_t chunk, void* stream) {
+  if (!b || (E > 0 && (!host_in || !dev_in || !pay || !dev_out || !host_out))) return fail(SK_ERR_ARG, "null argument");
+  if (geo != SK_GEO_REGULAR && geo != SK_GEO_DEFORMED) return fail(SK_ERR_ARG, "bad geometry class");
+  if (op != SK_STREAM_HELMHOLTZ && op != SK_STREAM_HELMHOLTZ_NC && op != SK_STREAM_MASS)
+    return fail(SK_ERR_ARG, "unknown streamed operator");
+  if (op != SK_STREAM_MASS && !(lam >= 0.0)) return fail(SK_ERR_ARG, "reaction coefficient must be nonnegative");
+  if (int st = check_layout(E, W, ncomp)) return st;
+  const int kop = op == SK_STREAM_MASS ? sk::OP_MASS : op == SK_STREAM_HELMHOLTZ_NC ? sk::OP_HELM_NC : sk::OP_HELM;
+  const int kind = op == SK_STREAM_MASS ? SK_PAYLOAD_W : op == SK_STREAM_HELMHOLTZ_NC ? SK_PAYLOAD_HELMHOLTZ_NC
+                                                                                     : SK_PAYLOAD_HELMHOLTZ;
+  const long long Epad = padded(E, W);
+  if (Epad == 0) return SK_OK;
+  int st = SK_OK;
+  const double* g = device_gtab(const_cast<sk_basis*>(b), &st);
+  if (st) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream), sh = nullptr, sd = nullptr;
+  if ((st = copy_streams(&sh, &sd))) return st;
+  // chunks start on a multiple of the interleave width, the tile width and
+  // the payload lane width (= tile width), so every chunk is a sub-block
+  int64_t cfg[3];
+  b->ops->config(kop, cfg);
+  const long long eb = cfg[0] > 0 ? cfg[0] : 1;
+  const long long unit = (long long)W / gcd_ll(W, eb) * eb;
+  if (chunk <= 0) chunk = (Epad + 15) / 16;
+  if (chunk < 4096) chunk = 4096;
+  chunk = (chunk + unit - 1) / unit * unit;
+  const long long nm = b->hb.nm, cs = Epad * nm, per_el = b->ops->payload_doubles(kind, geo);
+  const int nchunk = (int)((Epad + chunk - 1) / chunk);
+  std::vector<cudaEvent_t> ev(2 * nchunk + 2, nullptr);
+  cudaError_t e = cudaSuccess;
+  for (auto& x : ev)
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x, cudaEventDisableTiming);
+  auto cleanup = [&] {
+    for (auto& x : ev)
+      if (x) cudaEventDestroy(x);  // deferred by the runtime until the event completes
+  };
+  if (e != cudaSuccess) {
+    cleanup();
+    return cuda_status(e, "event creation");
+  }
+  // copies start after earlier work on the caller's stream (e.g. writers of dev_in)
+  e = cudaEventRecord(ev[2 * nchunk], s);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(sh, ev[2 * nchunk], 0);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(sd, ev[2 * nchunk], 0);
+  sk::LaunchReq r;
+  r.fwd = b->fwd_vals.data();
+  r.fwd_d = b->fwd_ders.data();
+  r.dtab = b->dtab.data();
+  r.gtab = g;
+  r.in_cs = cs;
+  r.out_cs = cs;
+  r.W = W;
+  r.ncomp = ncomp;
+  r.geo = geo;
+  r.lam = op == SK_STREAM_MASS ? 0.0 : lam;
+  for (int i = 0; i < nchunk && e == cudaSuccess; ++i) {
+    const long long e0 = (long long)i * chunk, e1 = std::min<long long>(Epad, e0 + chunk);
+    const size_t bytes = sizeof(double) * (size_t)((e1 - e0) * nm);
+    for (int c = 0; c < ncomp && e == cudaSuccess; ++c)
+      e = cudaMemcpyAsync(dev_in + c * cs + e0 * nm, host_in + c * cs + e0 * nm, bytes, cudaMemcpyHostToDevice, sh);
+    if (e == cudaSuccess) e = cudaEventRecord(ev[2 * i], sh);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ev[2 * i], 0);
+    if (e != cudaSuccess) break;
+    r.in = dev_in + e0 * nm;
+    r.out = dev_out + e0 * nm;
+    r.pay = pay + e0 * per_el;  // chunks start on a payload lane group
+    r.E = std::max<long long>(0, std::min<long long>(E, e1) - e0);
+    r.Epad = e1 - e0;
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    e = static_cast<cudaError_t>(b->ops->launch(kop, r, stream));
+    if (e == cudaSuccess) e = cudaEventRecord(ev[2 * i + 1], s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(sd, ev[2 * i + 1], 0);
+    for (int c = 0; c < ncomp && e == cudaSuccess; ++c)
+      e = cudaMemcpyAsync(host_out + c * cs + e0 * nm, dev_out + c * cs + e0 * nm, bytes, cudaMemcpyDeviceToHost, sd);
+  }
+  // the caller's stream resumes once every chunk is back on the host
+  if (e == cudaSuccess) e = cudaEventRecord(ev[2 * nchunk + 1], sd);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ev[2 * nchunk + 1], 0);
+  cleanup();
+  return cuda_status(e, "streamed apply");
 }
 
 int64_t sk_launch_count(void) { return g_launches.load(); }

@@ -34,26 +34,32 @@ struct Mode {
   static constexpr int fit(int eb, int budget) {
     return (eb <= 1 || smem_bytes(eb) <= budget) ? eb : fit(eb / 2, budget);
   }
-  static constexpr int EB = tuned_eb(S, P) > 0 ? fit(tuned_eb(S, P), 200 * 1024) : fit(16, 100 * 1024);
-  static constexpr int PW = EB;  // payload lane width, shared by every op of (S, P)
+  // Helmholtz family (Helmholtz / stiffness / non-collocated / phys_deriv;
+  // payload kinds 0, 2, 3) and W family (mass / iproduct / iproduct-deriv /
+  // bwd_trans; payload kind 1): independent tile widths
+  static constexpr int EBH = tuned_eb(0, S, P) > 0 ? fit(tuned_eb(0, S, P), 200 * 1024) : fit(16, 100 * 1024);
+  static constexpr int EBW = tuned_eb(1, S, P) > 0 ? fit(tuned_eb(1, S, P), 200 * 1024) : fit(16, 100 * 1024);
+  // payload lane width of each payload kind = tile width of its consumers
+  SK_HD static constexpr int pw(int kind) { return kind == 1 ? EBW : EBH; }
+  SK_HD static constexpr int eb(int op) { return (op == OP_HELM || op == OP_HELM_NC || op == OP_PDERIV) ? EBH : EBW; }
 };
 
 template <int S, int P, int OP>
 struct Cfg {
   using Dm = Dims<S, P>;
-  static constexpr int EB = Mode<S, P>::EB;
-  static constexpr int PW = Mode<S, P>::PW;
+  static constexpr int EB = Mode<S, P>::eb(OP);
+  static constexpr int PW = EB;
   static constexpr int planes = OP == OP_HELM_NC ? 5 : (OP == OP_HELM || OP == OP_PDERIV || OP == OP_IPDERIV) ? 3 : 2;
   static constexpr int items = cmax(cmax(cmax(Dm::Q1 * Dm::Q2, Dm::Q0 * Dm::Q2), cmax(Dm::Q0 * Dm::Q1, Dm::P1 * Dm::P1)),
                                     cmax(Dm::NPAIR, Dm::P1 * Dm::Q2));
   using L = Lay<S, P, planes, EB>;
-  static constexpr int NT0 = ((EB * items / tuned_nt_div(S, P) + 31) / 32) * 32;
+  static constexpr int CLS = OP == OP_HELM ? 0 : OP == OP_MASS ? 1 : 2;
+  static constexpr int NT0 = ((EB * items / tuned_nt_div(CLS, S, P) + 31) / 32) * 32;
   static constexpr int NT = NT0 > 512 ? 512 : (NT0 < 64 ? 64 : NT0);
   static constexpr int SMEM = L::SMEM_DOUBLES * 8;
   // __launch_bounds__ min blocks: 1, or the CTAs per SM that shared memory
   // allows (forces ptxas to fit the registers; tuned, as it can spill)
-  static constexpr int CLS = OP == OP_HELM ? 0 : OP == OP_MASS ? 1 : 2;
-  static constexpr int MINB = tuned_minb(S, P) ? cmax(1, cmin(cmin(tuned_minb_cap(CLS, S, P), (220 * 1024) / (SMEM + 1024)), 2048 / NT))
+  static constexpr int MINB = tuned_minb(CLS, S, P) ? cmax(1, cmin(cmin(tuned_minb_cap(CLS, S, P), (220 * 1024) / (SMEM + 1024)), 2048 / NT))
                                                : 1;
 };
 
@@ -214,25 +220,44 @@ static void ensure_smem(K kernel, int bytes) {
   if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
 
+#ifndef SK_PERSIST
+#define SK_PERSIST 0
+#endif
+
 template <int S, int P, int OP, class Op, class Args>
 static int go(const Args& a, const LaunchReq& r, int gy, void* stream) {
   using C = Cfg<S, P, OP>;
   static_assert(C::EB == C::PW, "tiles must align with payload lanes");
+  constexpr bool persist = Op::PERSIST && SK_PERSIST;
+  auto kern = [] {
+    if constexpr (persist)
+      return k_persist<Op, Args>;
+    else
+      return k_tile<Op, Args>;
+  }();
   static std::once_flag once;  // one per kernel instantiation
-  static int resident = 1;
-  std::call_once(once, [] {
-    ensure_smem(k_tile<Op, Args>, C::SMEM);
-    int per_sm = 1, sms = 148, dev = 0;
+  static int per_sm = 1, sms = 148;
+  std::call_once(once, [&] {
+    ensure_smem(kern, C::SMEM);
+    int dev = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Op::NT, C::SMEM);
     cudaGetDevice(&dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tile<Op, Args>, Op::NT, C::SMEM);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    resident = (per_sm > 0 ? per_sm : 1) * sms;
+    if (per_sm < 1) per_sm = 1;
   });
   const long long tiles = (r.Epad + C::EB - 1) / C::EB;
   if (tiles == 0) return 0;
   Args& args = const_cast<Args&>(a);
-  args.pf_ahead = resident / (gy > 0 ? gy : 1);
-  k_tile<Op, Args><<<dim3((unsigned)tiles, (unsigned)gy), Op::NT, C::SMEM, static_cast<cudaStream_t>(stream)>>>(args);
+  const int g = gy > 0 ? gy : 1;
+  const long long resident = (long long)per_sm * sms;
+  args.pf_ahead = resident / g;
+  long long grid = tiles;
+  if constexpr (persist) {
+    // one resident wave, shared by the components (grid.y)
+    const long long wave = resident / g > 0 ? resident / g : 1;
+    grid = tiles < wave ? tiles : wave;
+  }
+  kern<<<dim3((unsigned)grid, (unsigned)gy), Op::NT, C::SMEM, static_cast<cudaStream_t>(stream)>>>(args);
   return (int)cudaGetLastError();
 }
 
@@ -359,8 +384,8 @@ long long payload_doubles(int kind, int geo) {
 }
 
 template <int S, int P>
-long long payload_elements(long long E) {
-  constexpr long long PW = Mode<S, P>::PW;
+long long payload_elements(int kind, long long E) {
+  const long long PW = Mode<S, P>::pw(kind);
   return (E + PW - 1) / PW * PW;
 }
 
@@ -369,11 +394,11 @@ template <int S, int P>
 __device__ __forceinline__ void put_point(int kind, long long e, int l, const double (&dxi)[3][3], double wjac,
                                           double* __restrict__ pay, const double* __restrict__ gtab) {
   using Dm = Dims<S, P>;
-  constexpr int NQ = Dm::NQ, PW = Mode<S, P>::PW;
+  constexpr int NQ = Dm::NQ, PW = Mode<S, P>::pw(0), PWW = Mode<S, P>::pw(1);
   const int k = l % Dm::Q2, ij = l / Dm::Q2;
   const long long km = k * Dm::Q0 * Dm::Q1 + ij;
   if (kind == 1) {
-    pay[pay_base<PW>(e, 1, NQ) + (long long)l * PW] = wjac;
+    pay[pay_base<PWW>(e, 1, NQ) + (long long)l * PWW] = wjac;
     return;
   }
   double G[3][3];
@@ -437,7 +462,7 @@ __global__ void k_pack_deformed(int kind, long long E, const double* __restrict_
 template <int S, int P>
 __global__ void k_pack_regular(int kind, long long E, const double* __restrict__ dxi, const double* __restrict__ jac,
                                double* __restrict__ pay) {
-  constexpr int PW = Mode<S, P>::PW;
+  constexpr int PW = Mode<S, P>::pw(0), PWW = Mode<S, P>::pw(1);
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < E; e += (long long)gridDim.x * blockDim.x) {
     const double* d = dxi + e * 9;
     if (kind == 0 || kind == 3) {
@@ -451,7 +476,7 @@ __global__ void k_pack_regular(int kind, long long E, const double* __restrict__
       o[6 * PW] = jac[e];
       o[7 * PW] = 0.0;
     } else if (kind == 1) {
-      pay[pay_base<PW>(e, 1, 1)] = jac[e];
+      pay[pay_base<PWW>(e, 1, 1)] = jac[e];
     } else {
       double* o = pay + pay_base<PW>(e, 9, 1);
       for (int a = 0; a < 9; ++a) o[a * PW] = d[a];

@@ -75,6 +75,12 @@ __host__ __device__ constexpr int wfam_off(int Q, int P1, int p) { return Q * (p
 // half the multiply-adds.
 __host__ __device__ constexpr bool gll_dir(int S, int d) { return d == 0 || (d == 1 && S != TET) || (d == 2 && S == HEX); }
 
+// even-odd kernels in use for (shape, order) (tables are filled regardless)
+#ifndef SK_EO_MINP
+#define SK_EO_MINP 1
+#endif
+__host__ __device__ constexpr bool use_eo(int, int P) { return P >= SK_EO_MINP; }
+
 template <int S, int P>
 struct FwdTab {
   using Dm = Dims<S, P>;

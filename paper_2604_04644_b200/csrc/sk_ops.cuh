@@ -136,6 +136,35 @@ __global__ void __launch_bounds__(Op::NT, Op::MINB) k_tile(const __grid_constant
   Op::run(A, t, sm);
 }
 
+// Persistent driver: one resident wave of CTAs strides over the tiles.  The
+// coefficient loads of tile t + grid are issued (into registers) before tile
+// t's sweeps, and warp 0 prefetches into L2 the geometry payload one tile
+// and the coefficients two tiles ahead, so the global latency of every
+// tile after the first overlaps the previous tile's arithmetic.
+template <class Op, class Args>
+__global__ void __launch_bounds__(Op::NT, Op::MINB) k_persist(const __grid_constant__ Args A) {
+  extern __shared__ double sm[];
+  const long long ntiles = (A.Epad + Op::EB - 1) / Op::EB;
+  const long long stride = gridDim.x;
+  long long t = blockIdx.x;
+  typename Op::Pre pre;
+  if (t < ntiles) {
+    if (threadIdx.x < 32) Op::prefetch_geo(A, t);
+    Op::pre_load(A, t, pre);
+  }
+  for (; t < ntiles; t += stride) {
+    if (threadIdx.x < 32) {
+      if (t + stride < ntiles) Op::prefetch_geo(A, t + stride);
+      if (t + 2 * stride < ntiles) Op::prefetch_in(A, t + 2 * stride);
+    }
+    __syncthreads();  // the previous tile is done with the staging area
+    Op::pre_put(A, pre, sm);
+    if (t + stride < ntiles) Op::pre_load(A, t + stride, pre);
+    __syncthreads();
+    Op::body(A, t, sm);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Helmholtz, collocated: 9 sweeps + coefficient tile staging, 10 CTA barriers
 template <int S, int P, class L, int NT_, int PW, int GEO, bool LAMW, int MINB_>
@@ -155,7 +184,20 @@ struct k_helm {
     const long long n = A.Epad - e0 < EB ? A.Epad - e0 : EB;
     prefetch_field<Dims<S, P>::NM>(A.in, A.in_cstride, gridDim.y, e0, n, A.Epad, A.W);
   }
+  static constexpr bool PERSIST = true;
+  using Pre = TileRegs<L, Dims<S, P>::NM, NT_>;
+  __device__ static void pre_load(const OpArgs<S, P>& A, long long t, Pre& p) {
+    p.load(A.in + blockIdx.y * A.in_cstride, make_ctx<L::EB>(t, A.E, A.Epad, A.W));
+  }
+  __device__ static void pre_put(const OpArgs<S, P>& A, const Pre& p, double* sm) { p.put(A.W, sm + L::EB * L::PLANE); }
   __device__ static void run(const OpArgs<S, P>& A, long long tile, double* sm) {
+    using Dm = Dims<S, P>;
+    const Ctx c = make_ctx<L::EB>(tile, A.E, A.Epad, A.W);
+    load_tile<L, Dm::NM, NT>(A.in + blockIdx.y * A.in_cstride, c, sm + L::EB * L::PLANE);
+    __syncthreads();
+    body(A, tile, sm);
+  }
+  __device__ static void body(const OpArgs<S, P>& A, long long tile, double* sm) {
   using Dm = Dims<S, P>;
   constexpr int P1 = Dm::P1, Q0 = Dm::Q0, Q1 = Dm::Q1, Q2 = Dm::Q2, S2 = L::S2;
   constexpr int NQ = Dm::NQ, NM = Dm::NM, PL = L::PLANE;
@@ -165,8 +207,6 @@ struct k_helm {
   double* dst = A.out + blockIdx.y * A.out_cstride;
   double* xs = sm + L::EB * PL;  // plane 1: coefficient tile staging
 
-  load_tile<L, NM, NT>(src, c, xs);
-  __syncthreads();
   stage_f1<S, P, L, NT, TAo, CoefIn<L, NM>, false, ragged_dispatch(0, S, P)>(A.B, A.gtab, CoefIn<L, NM>{xs}, sm);
   __syncthreads();
   stage_f2<S, P, L, NT, TAo, TBo>(A.B, A.gtab, sm);
@@ -345,7 +385,20 @@ struct k_mass {
     const long long n = A.Epad - e0 < EB ? A.Epad - e0 : EB;
     prefetch_field<Dims<S, P>::NM>(A.in, A.in_cstride, gridDim.y, e0, n, A.Epad, A.W);
   }
+  static constexpr bool PERSIST = true;
+  using Pre = TileRegs<L, Dims<S, P>::NM, NT_>;
+  __device__ static void pre_load(const OpArgs<S, P>& A, long long t, Pre& p) {
+    p.load(A.in + blockIdx.y * A.in_cstride, make_ctx<L::EB>(t, A.E, A.Epad, A.W));
+  }
+  __device__ static void pre_put(const OpArgs<S, P>& A, const Pre& p, double* sm) { p.put(A.W, sm + L::EB * L::PLANE); }
   __device__ static void run(const OpArgs<S, P>& A, long long tile, double* sm) {
+    using Dm = Dims<S, P>;
+    const Ctx c = make_ctx<L::EB>(tile, A.E, A.Epad, A.W);
+    load_tile<L, Dm::NM, NT>(A.in + blockIdx.y * A.in_cstride, c, sm + L::EB * L::PLANE);
+    __syncthreads();
+    body(A, tile, sm);
+  }
+  __device__ static void body(const OpArgs<S, P>& A, long long tile, double* sm) {
   using Dm = Dims<S, P>;
   constexpr int P1 = Dm::P1, Q0 = Dm::Q0, Q1 = Dm::Q1, Q2 = Dm::Q2, S2 = L::S2, NM = Dm::NM;
   constexpr int PL = L::PLANE, TAo = 0, TBo = PL;
@@ -353,8 +406,6 @@ struct k_mass {
   const double* src = A.in + blockIdx.y * A.in_cstride;
   double* dst = A.out + blockIdx.y * A.out_cstride;
   double* xs = sm + L::EB * PL;  // plane 1 (TB): staging before F2 and after B2
-  load_tile<L, NM, NT>(src, c, xs);
-  __syncthreads();
   stage_f1<S, P, L, NT, TAo, CoefIn<L, NM>, false, ragged_dispatch(1, S, P)>(A.B, A.gtab, CoefIn<L, NM>{xs}, sm);
   __syncthreads();
   stage_f2<S, P, L, NT, TAo, TBo>(A.B, A.gtab, sm);
@@ -389,6 +440,7 @@ struct k_bwd {
   static constexpr int NT = NT_;
   static constexpr int EB = L::EB;
   static constexpr int MINB = MINB_;
+  static constexpr bool PERSIST = false;
   __device__ static void prefetch_geo(const OpArgs<S, P>& A, long long t) {
     const long long e0 = t * EB;
     const long long n = A.E - e0 < EB ? A.E - e0 : EB;
@@ -438,6 +490,7 @@ struct k_iprod {
   static constexpr int NT = NT_;
   static constexpr int EB = L::EB;
   static constexpr int MINB = MINB_;
+  static constexpr bool PERSIST = false;
   __device__ static void prefetch_geo(const OpArgs<S, P>& A, long long t) {
     const long long e0 = t * EB;
     const long long n = A.E - e0 < EB ? A.E - e0 : EB;
@@ -489,6 +542,7 @@ struct k_pderiv {
   static constexpr int NT = NT_;
   static constexpr int EB = L::EB;
   static constexpr int MINB = MINB_;
+  static constexpr bool PERSIST = false;
   __device__ static void prefetch_geo(const OpArgs<S, P>& A, long long t) {
     const long long e0 = t * EB;
     const long long n = A.E - e0 < EB ? A.E - e0 : EB;
@@ -587,6 +641,7 @@ struct k_ipderiv {
   static constexpr int NT = NT_;
   static constexpr int EB = L::EB;
   static constexpr int MINB = MINB_;
+  static constexpr bool PERSIST = false;
   __device__ static void prefetch_geo(const OpArgs<S, P>& A, long long t) {
     const long long e0 = t * EB;
     const long long n = A.E - e0 < EB ? A.E - e0 : EB;
@@ -680,6 +735,7 @@ struct k_helm_nc {
   static constexpr int NT = NT_;
   static constexpr int EB = L::EB;
   static constexpr int MINB = MINB_;
+  static constexpr bool PERSIST = false;
   using A_t = NcArgs<S, P>;
   __device__ static void prefetch_geo(const A_t& A, long long t) {
     const long long e0 = t * EB;

@@ -35,7 +35,7 @@ struct OpSet {
   void (*config)(int op, int64_t out[3]);
   // payload kinds: 0 HELMHOLTZ (k-major), 1 W, 2 DERIV, 3 HELMHOLTZ (standard order)
   long long (*payload_doubles)(int kind, int geo);  // per element
-  long long (*payload_elements)(long long E);       // elements incl. lane padding
+  long long (*payload_elements)(int kind, long long E);  // elements incl. lane padding
   int (*pack)(int kind, int geo, long long E, const double* dxi, const double* jac, double* pay,
               const double* gtab, void* stream);
   // geometry builder: mode 0 from coords (E,NQ,3), mode 1 from params (E,12).

@@ -79,6 +79,52 @@ __device__ __forceinline__ void store_tile(double* __restrict__ dst, const Ctx& 
   }
 }
 
+// Register-staged coefficient tile for the persistent kernels: the loads of
+// the next tile are issued before the current tile's sweeps (they land during
+// them) and written to the staging area at the top of the next iteration.
+// Same thread -> element mapping as load_tile.
+template <class L, int N, int NT>
+struct TileRegs {
+  static constexpr int EB = L::EB, XS = L::XSTR, CPT = (EB * N + NT - 1) / NT;
+  double v[CPT];
+  __device__ __forceinline__ void load(const double* __restrict__ src, const Ctx& c) {
+    if (c.W == 1) {
+      const double* base = src + c.e0 * N;
+      const long long lim = (c.E - c.e0) * N;
+#pragma unroll
+      for (int i = 0; i < CPT; ++i) {
+        const int g = threadIdx.x + i * NT;
+        v[i] = (g < EB * N && g < lim) ? __ldg(base + g) : 0.0;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < CPT; ++i) {
+        const int g = threadIdx.x + i * NT;
+        const int m = g / EB, e = g - m * EB;
+        const long long eg = c.e0 + e;
+        v[i] = (g < EB * N && eg < c.E) ? __ldg(src + lane_base(eg, N, c.W) + (long long)m * c.W) : 0.0;
+      }
+    }
+  }
+  __device__ __forceinline__ void put(int W, double* xs) const {
+#pragma unroll
+    for (int i = 0; i < CPT; ++i) {
+      const int g = threadIdx.x + i * NT;
+      if (g < EB * N) {
+        int e, m;
+        if (W == 1) {
+          e = g / N;
+          m = g - e * N;
+        } else {
+          m = g / EB;
+          e = g - m * EB;
+        }
+        xs[m * XS + e] = v[i];
+      }
+    }
+  }
+};
+
 // coefficient m of tile element e from / to the staged tile
 template <class L, int NM>
 struct CoefIn {
@@ -253,7 +299,9 @@ __device__ __forceinline__ void line_m_eo(const EOTab<Q>& T, const double (&u)[Q
 // collocation derivative along direction DIR: v = D u, and r += D^T w
 template <int S, int P, int DIR, int Q>
 __device__ __forceinline__ void line_dd(const DTab<S, P>& D, const double (&u)[Q], double (&v)[Q]) {
-  if constexpr (DIR == 0) {
+  if constexpr (!use_eo(S, P)) {
+    line_d<Q>(DIR == 0 ? D.d0 : DIR == 1 ? D.d1 : D.d2, u, v);
+  } else if constexpr (DIR == 0) {
     line_m_eo<Q, false>(D.e0, u, v);
   } else if constexpr (DIR == 1) {
     if constexpr (gll_dir(S, 1)) line_m_eo<Q, false>(D.e1, u, v); else line_d<Q>(D.d1, u, v);
@@ -264,7 +312,9 @@ __device__ __forceinline__ void line_dd(const DTab<S, P>& D, const double (&u)[Q
 
 template <int S, int P, int DIR, int Q>
 __device__ __forceinline__ void line_ddt_acc(const DTab<S, P>& D, const double (&w)[Q], double (&r)[Q]) {
-  if constexpr (DIR == 0) {
+  if constexpr (!use_eo(S, P)) {
+    line_dt_acc<Q>(DIR == 0 ? D.d0 : DIR == 1 ? D.d1 : D.d2, w, r);
+  } else if constexpr (DIR == 0) {
     line_m_eo<Q, true>(D.e0t, w, r);
   } else if constexpr (DIR == 1) {
     if constexpr (gll_dir(S, 1)) line_m_eo<Q, true>(D.e1t, w, r); else line_dt_acc<Q>(D.d1, w, r);
@@ -276,12 +326,18 @@ __device__ __forceinline__ void line_ddt_acc(const DTab<S, P>& D, const double (
 // dir-0 value contractions in even-odd form (value tables only)
 template <int S, int P>
 __device__ __forceinline__ void line_a0_eo(const FwdTab<S, P>& B, const double (&x)[P + 1], double (&u)[Dims<S, P>::Q0]) {
-  line_b_eo<Dims<S, P>::Q0, P + 1>(B.a0, B.a0p, B.a0m, x, u);
+  if constexpr (use_eo(S, P))
+    line_b_eo<Dims<S, P>::Q0, P + 1>(B.a0, B.a0p, B.a0m, x, u);
+  else
+    line_a0<S, P>(B, x, u);
 }
 
 template <int S, int P>
 __device__ __forceinline__ void line_a0t_eo(const FwdTab<S, P>& B, const double (&r)[Dims<S, P>::Q0], double (&t)[P + 1]) {
-  line_bt_eo<Dims<S, P>::Q0, P + 1>(B.a0, B.a0p, B.a0m, r, t);
+  if constexpr (use_eo(S, P))
+    line_bt_eo<Dims<S, P>::Q0, P + 1>(B.a0, B.a0p, B.a0m, r, t);
+  else
+    line_a0t<S, P>(B, r, t);
 }
 
 // ---- F1: r -> k.  TA[p][q][k] = sum_r C_(p,q)[k][r] uhat[p,q,r] ----------
@@ -298,7 +354,7 @@ __device__ __forceinline__ void stage_f1(const FwdTab<S, P>& B, const double* __
       double x[P1];
 #pragma unroll
       for (int r = 0; r < P1; ++r) x[r] = xin(e, ps * P1 + r);
-      if constexpr (!DER2) {
+      if constexpr (!DER2 && use_eo(S, P)) {
         double u[Q2];
         line_b_eo<Q2, P1>(B.a2, B.a2p, B.a2m, x, u);
 #pragma unroll
@@ -420,7 +476,7 @@ __device__ __forceinline__ void stage_f2(const FwdTab<S, P>& B, const double* __
       for (int q = 0; q < P1; ++q) x[q] = sm[L::at(e, TAo + (p * P1 + q) * S2 + k)];
       double y = 0.0;
       if constexpr (S == PYR) y = sm[L::at(e, TAo + P1 * P1 * S2 + k)];
-      if constexpr (!DER1) {
+      if constexpr (!DER1 && use_eo(S, P)) {
         // apex shares (operators.py:335-349): a1[j][1] y into p = 0, y into p = 1
         if constexpr (S == PYR) {
           if (p == 0) x[1] += y;
@@ -527,7 +583,7 @@ __device__ __forceinline__ void stage_b2(const FwdTab<S, P>& B, const double* __
       double x[Q1];
 #pragma unroll
       for (int j = 0; j < Q1; ++j) x[j] = sm[L::at(e, TBo + (p * Q1 + j) * S2 + k)];
-      if constexpr (!DER1) {
+      if constexpr (!DER1 && use_eo(S, P)) {
         double t[P1];
         line_bt_eo<Q1, P1>(B.a1, B.a1p, B.a1m, x, t);
 #pragma unroll
@@ -644,7 +700,7 @@ __device__ __forceinline__ void stage_b3(const FwdTab<S, P>& B, const double* __
       double x[Q2];
 #pragma unroll
       for (int k = 0; k < Q2; ++k) x[k] = sm[L::at(e, TAo + ps * S2 + k)];
-      if constexpr (!DER2) {
+      if constexpr (!DER2 && use_eo(S, P)) {
         double t[P1];
         line_bt_eo<Q2, P1>(B.a2, B.a2p, B.a2m, x, t);
 #pragma unroll

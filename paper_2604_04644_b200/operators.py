@@ -109,6 +109,37 @@ def _geo(block: Block) -> int:
     return _lib.SK_GEO_DEFORMED if block.geometry_class is GeometryClass.DEFORMED else _lib.SK_GEO_REGULAR
 
 
+#: inputs at least this large (bytes) that live only in host memory are
+#: applied chunk-pipelined (H2D / kernel / D2H overlapped, sk_apply_streamed);
+#: smaller ones take the plain transfer-then-apply path
+STREAM_MIN_BYTES = 32 << 20
+
+
+def _streamed(block: Block, out: Block, op: int, pay, lam: float) -> bool:
+    """Host-resident input: run the operator pipelined over element chunks,
+    leaving input and output live in both spaces (one transfer each, as the
+    plain path would count them).  Returns False when not applicable."""
+    reg = block.region
+    if not reg.host_resident() or out is block or reg.length * 8 < STREAM_MIN_BYTES:
+        return False
+    import torch
+
+    h_in, d_in = reg.buffers()
+    h_out, d_out = out.region.buffers()
+    _lib.check(
+        _lib.load().sk_apply_streamed(
+            block.basis.handle, op, _geo(block), block.n_elements, block.interleave_width, block.n_components,
+            _p(h_in), _p(d_in), _p(pay), float(lam), _p(d_out), _p(h_out), 0, _stream(),
+        ),
+        "sk_apply_streamed",
+    )
+    ev = torch.cuda.Event()
+    ev.record()
+    reg.mark_streamed(ev, wrote_host=False)
+    out.region.mark_streamed(ev, wrote_host=True)
+    return True
+
+
 def bwd_trans(block: Block, strategy: Strategy = Strategy.SUM_FAC_TOP, out: Block | None = None) -> Block:
     """u = B uhat (operators.py:551-561)."""
     _check_strategy(strategy)
@@ -188,6 +219,8 @@ def mass_apply(block: Block, strategy: Strategy = Strategy.SUM_FAC_TOP, out: Blo
     _require_state(block, FieldState.COEFF, "mass_apply")
     out = _out_block(block, out, FieldState.COEFF, block.n_components)
     pay = block.payload(_lib.SK_PAYLOAD_W)
+    if _streamed(block, out, _lib.SK_STREAM_MASS, pay, 0.0):
+        return out
     xin = block.device(AccessQualifier.READ_ONLY)
     xout = out.device(AccessQualifier.WRITE_ONLY)
     _lib.check(
@@ -206,6 +239,9 @@ def _helmholtz(block: Block, lam: float, form: int, out: Block | None, name: str
         raise ValueError(f"reaction coefficient must be nonnegative, got {lam}")
     out = _out_block(block, out, FieldState.COEFF, block.n_components)
     pay = block.payload(_lib.SK_PAYLOAD_HELMHOLTZ if form == _lib.SK_FORM_COLL else _lib.SK_PAYLOAD_HELMHOLTZ_NC)
+    sop = _lib.SK_STREAM_HELMHOLTZ if form == _lib.SK_FORM_COLL else _lib.SK_STREAM_HELMHOLTZ_NC
+    if _streamed(block, out, sop, pay, lam):
+        return out
     xin = block.device(AccessQualifier.READ_ONLY)
     xout = out.device(AccessQualifier.WRITE_ONLY)
     _lib.check(

@@ -6,7 +6,12 @@
 # dispatch max order); omitted keys keep the sk_tune.h tables.
 # -> paper_2604_04644_b200/libsk200_<name>.so, used by tools/tune_eb.py.
 set -e
-cd "$(dirname "$0")/../paper_2604_04644_b200/csrc"
+ROOT=$(cd "$(dirname "$0")/.." && pwd)
+# build from a snapshot of the sources, so editing them meanwhile is safe
+SNAP=$(mktemp -d /tmp/sk200_src_XXXX)
+mkdir -p "$SNAP/paper_2604_04644_b200" && cp -r "$ROOT/include" "$SNAP/" && cp -r "$ROOT/paper_2604_04644_b200/csrc" "$SNAP/paper_2604_04644_b200/"
+rm -rf "$SNAP/paper_2604_04644_b200/csrc/build"
+cd "$SNAP/paper_2604_04644_b200/csrc"
 for v in "$@"; do
   extra=""
   for kv in ${v//_/ }; do
@@ -20,8 +25,10 @@ for v in "$@"; do
       cap) extra="$extra -DSK_MINB_CAP=$n" ;;
       rd) extra="$extra -DSK_RAGGED_MAXP=$n" ;;
       pd) extra="$extra -DSK_GEO_PD=$n" ;;
+      ps) extra="$extra -DSK_PERSIST=$n" ;;
+      eo) extra="$extra -DSK_EO_MINP=$n" ;;
     esac
   done
-  make -j"$(nproc)" BUILD=/tmp/sk200_build_$v LIB=../libsk200_$v.so LINEINFO= EXTRA="$extra" > /tmp/sk200_build_$v.log 2>&1 \
+  make -j"$(nproc)" BUILD=/tmp/sk200_build_$v LIB=$ROOT/paper_2604_04644_b200/libsk200_$v.so LINEINFO= EXTRA="$extra" > /tmp/sk200_build_$v.log 2>&1 \
     && echo "built libsk200_$v.so ($extra)" || { echo "FAILED $v"; tail -5 /tmp/sk200_build_$v.log; }
 done

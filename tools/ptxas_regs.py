@@ -21,7 +21,7 @@ for line in out.splitlines():
         spill = (m.group(1), m.group(2))
     m = re.search(r"Used (\d+) registers", line)
     if m and name:
-        k = re.search(r"k_tileINS_\d+(k_\w+?)I", name)
+        k = re.search(r"k_(?:tile|persist)INS_\d+(k_\w+?)I", name)
         if k:
             short = k.group(1) + " " + re.sub(r"ILi|Li|E|NS_|Lb", " ", name[name.index(k.group(1)) + len(k.group(1)):][:90])
             print(f"{m.group(1):>4} regs  spill {spill[0]}/{spill[1]}  {short}")
