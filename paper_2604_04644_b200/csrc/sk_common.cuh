@@ -75,11 +75,16 @@ __host__ __device__ constexpr int wfam_off(int Q, int P1, int p) { return Q * (p
 // half the multiply-adds.
 __host__ __device__ constexpr bool gll_dir(int S, int d) { return d == 0 || (d == 1 && S != TET) || (d == 2 && S == HEX); }
 
-// even-odd kernels in use for (shape, order) (tables are filled regardless)
-#ifndef SK_EO_MINP
-#define SK_EO_MINP 1
-#endif
+// even-odd kernels in use from this order on, per shape (measured: at low
+// order the extra even/odd combinations cost more than the halved
+// multiply-adds save on hex; tables are filled regardless)
+#ifdef SK_EO_MINP
 __host__ __device__ constexpr bool use_eo(int, int P) { return P >= SK_EO_MINP; }
+#else
+__host__ __device__ constexpr bool use_eo(int S, int P) {
+  return P >= (S == HEX ? 6 : S == TET ? 4 : 3);
+}
+#endif
 
 template <int S, int P>
 struct FwdTab {

@@ -24,11 +24,11 @@ constexpr int kTunedEB[2][4][11] = {
      {0, 16, 16, 16, 4, 8, 4, 2, 2, 1, 1},   // prism
      {0, 16, 8, 16, 8, 4, 4, 1, 1, 1, 1},    // pyr
      {0, 16, 16, 8, 8, 8, 4, 4, 4, 4, 2}},   // tet
-    // W family
-    {{0, 16, 16, 16, 8, 2, 2, 4, 1, 1, 2},
-     {0, 16, 16, 16, 8, 8, 4, 4, 4, 4, 1},
-     {0, 16, 16, 8, 8, 4, 4, 2, 1, 1, 2},
-     {0, 16, 16, 16, 8, 8, 4, 4, 4, 4, 2}},
+    // W family (mass, iproduct, iproduct-deriv, bwd_trans)
+    {{0, 16, 16, 16, 16, 8, 2, 8, 1, 1, 2},
+     {0, 16, 16, 16, 16, 16, 8, 4, 4, 16, 1},
+     {0, 16, 16, 8, 16, 8, 8, 8, 4, 2, 1},
+     {0, 16, 16, 16, 16, 8, 8, 16, 16, 8, 8}},
 };
 
 // threads per CTA = EB x (largest sweep item count) / divisor
@@ -37,10 +37,10 @@ constexpr int kTunedNTDiv[3][4][11] = {
      {1, 2, 2, 1, 1, 1, 1, 1, 1, 1, 1},
      {1, 2, 1, 2, 1, 1, 1, 1, 1, 1, 1},
      {1, 2, 2, 1, 1, 1, 1, 1, 1, 1, 1}},
-    {{1, 2, 1, 2, 1, 1, 1, 1, 1, 1, 1},
-     {1, 2, 2, 1, 1, 1, 1, 1, 1, 1, 1},
-     {1, 2, 2, 1, 1, 1, 1, 1, 1, 1, 1},
-     {1, 2, 2, 1, 1, 1, 1, 1, 1, 1, 1}},
+    {{1, 2, 2, 2, 1, 2, 1, 2, 1, 1, 1},
+     {1, 2, 2, 2, 2, 2, 2, 1, 2, 1, 1},
+     {1, 2, 1, 2, 1, 1, 1, 1, 1, 1, 1},
+     {1, 1, 2, 1, 1, 1, 1, 1, 2, 1, 1}},
     {{1, 2, 1, 2, 1, 1, 1, 1, 1, 1, 1},
      {1, 2, 2, 1, 1, 1, 1, 1, 1, 1, 1},
      {1, 2, 2, 1, 1, 1, 1, 1, 1, 1, 1},
@@ -54,10 +54,10 @@ constexpr int kTunedMinB[3][4][11] = {
      {0, 0, 1, 1, 1, 1, 1, 1, 1, 1, 1},
      {0, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1},
      {0, 0, 0, 1, 1, 1, 1, 1, 1, 0, 1}},
-    {{0, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1},
-     {0, 0, 1, 1, 1, 1, 1, 1, 1, 1, 1},
-     {0, 1, 0, 1, 1, 1, 1, 1, 1, 1, 1},
-     {0, 0, 0, 1, 1, 1, 1, 1, 1, 0, 0}},
+    {{0, 1, 1, 1, 1, 1, 1, 1, 0, 1, 1},
+     {0, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1},
+     {0, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1},
+     {0, 1, 1, 1, 1, 1, 1, 1, 1, 1, 0}},
     {{0, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1},
      {0, 0, 1, 1, 1, 1, 1, 1, 1, 1, 1},
      {0, 1, 0, 1, 1, 1, 1, 1, 1, 1, 1},
@@ -71,9 +71,9 @@ constexpr int kMinBCap[3][4][11] = {
      {4, 4, 8, 4, 4, 4, 8, 8, 4, 4, 4},
      {4, 4, 4, 8, 4, 4, 4, 4, 8, 4, 4}},
     {{4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 4},
-     {4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 4},
-     {4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 4},
-     {4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 4}},
+     {4, 4, 4, 4, 4, 4, 4, 8, 4, 4, 4},
+     {4, 4, 8, 4, 4, 4, 4, 8, 8, 4, 4},
+     {4, 8, 4, 8, 4, 8, 4, 4, 4, 4, 4}},
     {{4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 4},
      {4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 4},
      {4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 4},
