@@ -250,7 +250,7 @@ struct k_helm {
       const double* g = A.pay + pay_base<PW>(live ? eg : 0, 7, NQ) + (long long)ps * PW;
       // points in chunks of CH: a compiler fence between chunks keeps ptxas
       // from hoisting all 7*Q2 geometry loads (register pressure at high P)
-      constexpr int CH = Q2 <= 6 ? Q2 : 4;
+      constexpr int CH = Q2 <= 6 ? Q2 : kGeoChunk;
 #pragma unroll
       for (int k = 0; k < Q2; ++k) {
         if (k > 0 && k % CH == 0) asm volatile("" ::: "memory");

@@ -80,6 +80,14 @@ constexpr int kMinBCap[3][4][11] = {
      {4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 4}},
 };
 
+// points per geometry-load chunk in the Helmholtz metric sweep (lines longer
+// than 6 points): 7*CH doubles in flight per thread
+#ifdef SK_GEO_CH
+constexpr int kGeoChunk = SK_GEO_CH;
+#else
+constexpr int kGeoChunk = 4;
+#endif
+
 // pyr/tet ragged r <-> k sweeps: compile-time slice dispatch up to this
 // order (uniform table operands), L1 table reads above it (code size)
 constexpr int kRaggedMaxP[3][4] = {
