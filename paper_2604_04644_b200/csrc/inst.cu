@@ -220,15 +220,11 @@ static void ensure_smem(K kernel, int bytes) {
   if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
 
-#ifndef SK_PERSIST
-#define SK_PERSIST 0
-#endif
-
 template <int S, int P, int OP, class Op, class Args>
 static int go(const Args& a, const LaunchReq& r, int gy, void* stream) {
   using C = Cfg<S, P, OP>;
   static_assert(C::EB == C::PW, "tiles must align with payload lanes");
-  constexpr bool persist = Op::PERSIST && SK_PERSIST;
+  constexpr bool persist = Op::PERSIST && tuned_persist(C::CLS, S, P);
   auto kern = [] {
     if constexpr (persist)
       return k_persist<Op, Args>;

@@ -138,9 +138,10 @@ __global__ void __launch_bounds__(Op::NT, Op::MINB) k_tile(const __grid_constant
 
 // Persistent driver: one resident wave of CTAs strides over the tiles.  The
 // coefficient loads of tile t + grid are issued (into registers) before tile
-// t's sweeps, and warp 0 prefetches into L2 the geometry payload one tile
-// and the coefficients two tiles ahead, so the global latency of every
-// tile after the first overlaps the previous tile's arithmetic.
+// t's sweeps; warp 0 prefetches into L2 the coefficients two tiles ahead and
+// (from inside the body, right after the metric sweep) the geometry of the
+// next tile, so the global latency of every tile after the first overlaps
+// the previous tile's arithmetic while L2 holds ~one wave of geometry.
 template <class Op, class Args>
 __global__ void __launch_bounds__(Op::NT, Op::MINB) k_persist(const __grid_constant__ Args A) {
   extern __shared__ double sm[];
@@ -149,19 +150,21 @@ __global__ void __launch_bounds__(Op::NT, Op::MINB) k_persist(const __grid_const
   long long t = blockIdx.x;
   typename Op::Pre pre;
   if (t < ntiles) {
-    if (threadIdx.x < 32) Op::prefetch_geo(A, t);
+    if (threadIdx.x < 32) {
+      Op::prefetch_geo(A, t);
+      if (t + stride < ntiles) Op::prefetch_in(A, t + stride);
+    }
     Op::pre_load(A, t, pre);
   }
   for (; t < ntiles; t += stride) {
-    if (threadIdx.x < 32) {
-      if (t + stride < ntiles) Op::prefetch_geo(A, t + stride);
-      if (t + 2 * stride < ntiles) Op::prefetch_in(A, t + 2 * stride);
-    }
+    if (threadIdx.x < 32 && t + 2 * stride < ntiles) Op::prefetch_in(A, t + 2 * stride);
     __syncthreads();  // the previous tile is done with the staging area
     Op::pre_put(A, pre, sm);
     if (t + stride < ntiles) Op::pre_load(A, t + stride, pre);
     __syncthreads();
-    Op::body(A, t, sm);
+    // the body prefetches the next tile's geometry once its own is consumed,
+    // so the L2 holds about one wave of geometry at any time
+    Op::body(A, t, sm, t + stride < ntiles ? t + stride : -1);
   }
 }
 
@@ -195,9 +198,9 @@ struct k_helm {
     const Ctx c = make_ctx<L::EB>(tile, A.E, A.Epad, A.W);
     load_tile<L, Dm::NM, NT>(A.in + blockIdx.y * A.in_cstride, c, sm + L::EB * L::PLANE);
     __syncthreads();
-    body(A, tile, sm);
+    body(A, tile, sm, -1);
   }
-  __device__ static void body(const OpArgs<S, P>& A, long long tile, double* sm) {
+  __device__ static void body(const OpArgs<S, P>& A, long long tile, double* sm, long long tnext) {
   using Dm = Dims<S, P>;
   constexpr int P1 = Dm::P1, Q0 = Dm::Q0, Q1 = Dm::Q1, Q2 = Dm::Q2, S2 = L::S2;
   constexpr int NQ = Dm::NQ, NM = Dm::NM, PL = L::PLANE;
@@ -318,6 +321,7 @@ struct k_helm {
     for (int k = 0; k < Q2; ++k) sm[L::at(e, UO + row + k)] = z[k];
   });
   __syncthreads();
+  if (tnext >= 0 && threadIdx.x < 32) prefetch_geo(A, tnext);
   // M3: U += D1^T w1 along j
   items<L, Q0 * Q2, NT>([&](int e, int ps) {
     const int i = ps / Q2, k = ps - i * Q2;
@@ -396,9 +400,9 @@ struct k_mass {
     const Ctx c = make_ctx<L::EB>(tile, A.E, A.Epad, A.W);
     load_tile<L, Dm::NM, NT>(A.in + blockIdx.y * A.in_cstride, c, sm + L::EB * L::PLANE);
     __syncthreads();
-    body(A, tile, sm);
+    body(A, tile, sm, -1);
   }
-  __device__ static void body(const OpArgs<S, P>& A, long long tile, double* sm) {
+  __device__ static void body(const OpArgs<S, P>& A, long long tile, double* sm, long long tnext) {
   using Dm = Dims<S, P>;
   constexpr int P1 = Dm::P1, Q0 = Dm::Q0, Q1 = Dm::Q1, Q2 = Dm::Q2, S2 = L::S2, NM = Dm::NM;
   constexpr int PL = L::PLANE, TAo = 0, TBo = PL;
@@ -425,6 +429,7 @@ struct k_mass {
     for (int p = 0; p < P1; ++p) sm[L::at(e, TBo + (p * Q1 + j) * S2 + k)] = x[p];
   });
   __syncthreads();
+  if (tnext >= 0 && threadIdx.x < 32) prefetch_geo(A, tnext);
   stage_b2<S, P, L, NT, TAo, TBo>(A.B, A.gtab, sm);
   __syncthreads();
   stage_b3<S, P, L, NT, TAo, CoefOut<L, NM>, false, ragged_dispatch(1, S, P)>(A.B, A.gtab, CoefOut<L, NM>{xs}, sm);

@@ -29,7 +29,11 @@ namespace sk {
 // L1-table loop above it (instruction-cache footprint); prism r <-> k sweeps
 // run one thread per (element, q) with uniform slice tables up to
 // kPrismUniformMaxP and one per (element, p, q) pair above it.
+#ifdef SK_TET_DISPATCH_MAXP
+constexpr int kTetDispatchMaxP = SK_TET_DISPATCH_MAXP;
+#else
 constexpr int kTetDispatchMaxP = 9;
+#endif
 constexpr int kPrismUniformMaxP = 8;
 // pyr/tet r <-> k sweeps (slice c2[max(p,q)] / c2[p+q] varies per item):
 // compile-time slice dispatch (RD = true) or L1 table reads; chosen per

@@ -66,10 +66,10 @@ constexpr int kTunedMinB[3][4][11] = {
 
 // CTAs/SM cap of the min-blocks rule
 constexpr int kMinBCap[3][4][11] = {
-    {{4, 4, 8, 4, 4, 4, 4, 4, 4, 4, 4},
-     {4, 4, 4, 4, 8, 4, 8, 8, 8, 4, 4},
-     {4, 4, 8, 4, 4, 4, 8, 8, 4, 4, 4},
-     {4, 4, 4, 8, 4, 4, 4, 4, 8, 4, 4}},
+    {{4, 4, 8, 4, 4, 5, 4, 5, 4, 4, 4},
+     {4, 4, 4, 5, 8, 6, 8, 8, 8, 4, 4},
+     {4, 4, 8, 4, 6, 4, 8, 8, 5, 4, 4},
+     {4, 4, 4, 8, 5, 4, 4, 4, 8, 4, 4}},
     {{4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 4},
      {4, 4, 4, 4, 4, 4, 4, 8, 4, 4, 4},
      {4, 4, 8, 4, 4, 4, 4, 8, 8, 4, 4},
@@ -87,6 +87,16 @@ constexpr int kGeoChunk = SK_GEO_CH;
 #else
 constexpr int kGeoChunk = 4;
 #endif
+
+// 1: persistent CTAs (one resident wave striding over the tiles, next tile's
+// coefficients register-prefetched, its geometry L2-prefetched after the
+// metric sweep); Helmholtz class only, where measured faster
+constexpr int kPersist[4][11] = {
+    {0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 0},  // hex
+    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},  // prism
+    {0, 0, 0, 1, 0, 0, 0, 0, 0, 0, 0},  // pyr
+    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},  // tet
+};
 
 // pyr/tet ragged r <-> k sweeps: compile-time slice dispatch up to this
 // order (uniform table operands), L1 table reads above it (code size)
@@ -116,6 +126,11 @@ SK_HD constexpr int tuned_minb(int cls, int S, int P) { return kTunedMinB[cls][S
 SK_HD constexpr int tuned_minb_cap(int, int, int) { return SK_MINB_CAP; }
 #else
 SK_HD constexpr int tuned_minb_cap(int cls, int S, int P) { return kMinBCap[cls][S][P]; }
+#endif
+#ifdef SK_PERSIST
+constexpr bool tuned_persist(int, int, int) { return SK_PERSIST; }
+#else
+constexpr bool tuned_persist(int cls, int S, int P) { return cls == 0 && kPersist[S][P]; }
 #endif
 #ifdef SK_RAGGED_MAXP
 SK_HD constexpr bool ragged_dispatch(int, int, int P) { return P <= SK_RAGGED_MAXP; }
