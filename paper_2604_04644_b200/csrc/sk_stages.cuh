@@ -348,7 +348,7 @@ __device__ __forceinline__ void line_a0t_eo(const FwdTab<S, P>& B, const double 
 // DER2: the dir-2 family is the derivative one (reference dmode == 2; the
 // caller passes the derivative FwdTab for hex/prism, the device buffer's DC2
 // slices are used for pyr/tet)
-template <int S, int P, class L, int NT, int TAo, class In, bool DER2 = false, bool RD = false>
+template <int S, int P, class L, int NT, int TAo, class In, bool DER2 = false, bool RD = false, bool SPL = false>
 __device__ __forceinline__ void stage_f1(const FwdTab<S, P>& B, const double* __restrict__ gtab, const In& xin,
                                          double* sm) {
   using Dm = Dims<S, P>;
@@ -402,8 +402,13 @@ __device__ __forceinline__ void stage_f1(const FwdTab<S, P>& B, const double* __
     // pyr / tet: item = (e, (p,q) pair), pairs ordered by slice; the slice
     // m = max(p,q) (pyr) or p+q (tet) is dispatched to a compile-time
     // constant so c2[m] entries are uniform operands (operators.py:209-351)
+    // SPLIT = 2 when the pairs fill at most half the CTA: each (e, pair)
+    // line is computed by two threads (halves of k, half index slowest so a
+    // warp takes one half), so no warp idles through the stage
+    constexpr int SPLIT = SPL && 2 * L::EB * Dm::NPAIR <= NT ? 2 : 1;
     const int4* pairs = reinterpret_cast<const int4*>(gtab + GLayout<S, P>::PAIRS);
-    items<L, Dm::NPAIR, NT>([&](int e, int ps) {
+    items<L, Dm::NPAIR * SPLIT, NT>([&](int e, int ps2) {
+      const int h = ps2 / Dm::NPAIR, ps = ps2 - h * Dm::NPAIR;
       const int4 pr = __ldg(pairs + ps);  // p, q, mode offset, nr
       dispatch<0, P1>(P1 - pr.w, [&](auto mc) {
         constexpr int m = decltype(mc)::value;
@@ -414,16 +419,19 @@ __device__ __forceinline__ void stage_f1(const FwdTab<S, P>& B, const double* __
         for (int r = 0; r < n; ++r) x[r] = xin(e, pr.z + r);
 #pragma unroll
         for (int k = 0; k < Q2; ++k) {
-          double s = B.c2[co + k * n] * x[0];
+          if (SPLIT == 1 || (k * SPLIT) / Q2 == h) {
+            double s = B.c2[co + k * n] * x[0];
 #pragma unroll
-          for (int r = 1; r < n; ++r) s = fma(B.c2[co + k * n + r], x[r], s);
-          sm[L::at(e, TAo + (pr.x * P1 + pr.y) * S2 + k)] = s;
+            for (int r = 1; r < n; ++r) s = fma(B.c2[co + k * n + r], x[r], s);
+            sm[L::at(e, TAo + (pr.x * P1 + pr.y) * S2 + k)] = s;
+          }
         }
         if constexpr (m == 0) {
           if (pr.x == 0 && pr.y == 0) {
             // collapsed apex mode (0,0,1): Y[k] = c2[0][k][1] * uhat[0,0,1]
 #pragma unroll
-            for (int k = 0; k < Q2; ++k) sm[L::at(e, TAo + P1 * P1 * S2 + k)] = B.c2[k * P1 + 1] * x[1];
+            for (int k = 0; k < Q2; ++k)
+              if (SPLIT == 1 || (k * SPLIT) / Q2 == h) sm[L::at(e, TAo + P1 * P1 * S2 + k)] = B.c2[k * P1 + 1] * x[1];
           }
         }
       });
@@ -432,8 +440,10 @@ __device__ __forceinline__ void stage_f1(const FwdTab<S, P>& B, const double* __
     // prism / pyr / tet: item = (e, (p,q) pair); the dir-2 slice c2[p]
     // (prism), c2[max(p,q)] (pyr) or c2[p+q] (tet) differs per item -> read
     // from the device table buffer through L1 (operators.py:209-351)
+    constexpr int SPLIT = SPL && 2 * L::EB * Dm::NPAIR <= NT ? 2 : 1;  // see the dispatch path
     const int4* pairs = reinterpret_cast<const int4*>(gtab + GLayout<S, P>::PAIRS);
-    items<L, Dm::NPAIR, NT>([&](int e, int ps) {
+    items<L, Dm::NPAIR * SPLIT, NT>([&](int e, int ps2) {
+      const int h = ps2 / Dm::NPAIR, ps = ps2 - h * Dm::NPAIR;
       const int4 pr = __ldg(pairs + ps);  // p, q, mode offset, nr
       const int m = (S == TET) ? pr.x + pr.y : (S == PRISM) ? pr.x : cmax(pr.x, pr.y);
       const int n = P1 - m;
@@ -446,19 +456,22 @@ __device__ __forceinline__ void stage_f1(const FwdTab<S, P>& B, const double* __
       const double u0q1 = (S == PRISM && pr.x == 1) ? xin(e, pr.y * P1 + 1) : 0.0;
 #pragma unroll
       for (int k = 0; k < Q2; ++k) {
-        double s = 0.0;
+        if (SPLIT == 1 || (k * SPLIT) / Q2 == h) {
+          double s = 0.0;
 #pragma unroll
-        for (int r = 0; r < P1; ++r)
-          if (r < pr.w) s = fma(__ldg(tab + k * n + r), x[r], s);
-        if constexpr (S == PRISM) {
-          if (pr.x == 1) s = fma(u0q1, __ldg(fam + k * P1 + 1), s);
+          for (int r = 0; r < P1; ++r)
+            if (r < pr.w) s = fma(__ldg(tab + k * n + r), x[r], s);
+          if constexpr (S == PRISM) {
+            if (pr.x == 1) s = fma(u0q1, __ldg(fam + k * P1 + 1), s);
+          }
+          sm[L::at(e, TAo + (pr.x * P1 + pr.y) * S2 + k)] = s;
         }
-        sm[L::at(e, TAo + (pr.x * P1 + pr.y) * S2 + k)] = s;
       }
       if (S != PRISM && pr.x == 0 && pr.y == 0) {
         // collapsed apex mode (0,0,1): Y[k] = c2[0][k][1] * uhat[0,0,1]
 #pragma unroll
-        for (int k = 0; k < Q2; ++k) sm[L::at(e, TAo + P1 * P1 * S2 + k)] = __ldg(fam + k * P1 + 1) * x[1];
+        for (int k = 0; k < Q2; ++k)
+          if (SPLIT == 1 || (k * SPLIT) / Q2 == h) sm[L::at(e, TAo + P1 * P1 * S2 + k)] = __ldg(fam + k * P1 + 1) * x[1];
       }
     });
   }
@@ -694,7 +707,7 @@ __device__ __forceinline__ void stage_b2(const FwdTab<S, P>& B, const double* __
 // ---- B3: k -> r, produce coefficients ----------------------------------------
 // DER2: derivative dir-2 family (transposed dmode == 2); accumulation into
 // the output is the Out functor's business
-template <int S, int P, class L, int NT, int TAo, class Out, bool DER2 = false, bool RD = false>
+template <int S, int P, class L, int NT, int TAo, class Out, bool DER2 = false, bool RD = false, bool SPL = false>
 __device__ __forceinline__ void stage_b3(const FwdTab<S, P>& B, const double* __restrict__ gtab, const Out& out,
                                          const double* sm) {
   using Dm = Dims<S, P>;
@@ -750,9 +763,12 @@ __device__ __forceinline__ void stage_b3(const FwdTab<S, P>& B, const double* __
       }
     });
   } else if constexpr (S != PRISM && RD) {
-    // pyr / tet with the slice dispatched to a compile-time constant
+    // pyr / tet with the slice dispatched to a compile-time constant; outputs
+    // split over two threads (r parity) when the pairs fill half the CTA
+    constexpr int SPLIT = SPL && 2 * L::EB * Dm::NPAIR <= NT ? 2 : 1;
     const int4* pairs = reinterpret_cast<const int4*>(gtab + GLayout<S, P>::PAIRS);
-    items<L, Dm::NPAIR, NT>([&](int e, int ps) {
+    items<L, Dm::NPAIR * SPLIT, NT>([&](int e, int ps2) {
+      const int h = ps2 / Dm::NPAIR, ps = ps2 - h * Dm::NPAIR;
       const int4 pr = __ldg(pairs + ps);
       double x[Q2];
 #pragma unroll
@@ -769,7 +785,7 @@ __device__ __forceinline__ void stage_b3(const FwdTab<S, P>& B, const double* __
         constexpr int co = wfam_off(Q2, P1, m);
         double apex = 0.0;
         if constexpr (m == 0) {
-          if (pr.x == 0 && pr.y == 0) {
+          if (pr.x == 0 && pr.y == 0 && (SPLIT == 1 || h == 1)) {
 #pragma unroll
             for (int k = 0; k < Q2; ++k) {
               const double y = sm[L::at(e, TAo + P1 * P1 * S2 + k)] + sm[L::at(e, TAo + (0 * P1 + 1) * S2 + k)];
@@ -779,17 +795,21 @@ __device__ __forceinline__ void stage_b3(const FwdTab<S, P>& B, const double* __
         }
 #pragma unroll
         for (int r = 0; r < n; ++r) {
-          double s = B.c2[co + r] * x[0];
+          if (SPLIT == 1 || r % SPLIT == h) {
+            double s = B.c2[co + r] * x[0];
 #pragma unroll
-          for (int k = 1; k < Q2; ++k) s = fma(B.c2[co + k * n + r], x[k], s);
-          if (r == 1) s += apex;
-          out(e, pr.z + r, s);
+            for (int k = 1; k < Q2; ++k) s = fma(B.c2[co + k * n + r], x[k], s);
+            if (r == 1) s += apex;
+            out(e, pr.z + r, s);
+          }
         }
       });
     });
   } else {
+    constexpr int SPLIT = SPL && 2 * L::EB * Dm::NPAIR <= NT ? 2 : 1;  // see the dispatch path
     const int4* pairs = reinterpret_cast<const int4*>(gtab + GLayout<S, P>::PAIRS);
-    items<L, Dm::NPAIR, NT>([&](int e, int ps) {
+    items<L, Dm::NPAIR * SPLIT, NT>([&](int e, int ps2) {
+      const int h = ps2 / Dm::NPAIR, ps = ps2 - h * Dm::NPAIR;
       const int4 pr = __ldg(pairs + ps);
       const int m = (S == TET) ? pr.x + pr.y : (S == PRISM) ? pr.x : cmax(pr.x, pr.y);
       const int n = P1 - m;
@@ -805,14 +825,14 @@ __device__ __forceinline__ void stage_b3(const FwdTab<S, P>& B, const double* __
         }
       }
       double apex = 0.0;
-      if (S != PRISM && pr.x == 0 && pr.y == 0) {
+      if (S != PRISM && pr.x == 0 && pr.y == 0 && (SPLIT == 1 || h == 1)) {
 #pragma unroll
         for (int k = 0; k < Q2; ++k) {
           const double y = sm[L::at(e, TAo + P1 * P1 * S2 + k)] + sm[L::at(e, TAo + (0 * P1 + 1) * S2 + k)];
           apex = fma(__ldg(fam + k * P1 + 1), y, apex);
         }
       }
-      if (S == PRISM && pr.x == 0) {
+      if (S == PRISM && pr.x == 0 && (SPLIT == 1 || h == 1)) {
         // modes (0,q,1) += sum_k c2[0][k][1] TA[1][q][k] (operators.py:312-317)
 #pragma unroll
         for (int k = 0; k < Q2; ++k)
@@ -820,7 +840,7 @@ __device__ __forceinline__ void stage_b3(const FwdTab<S, P>& B, const double* __
       }
 #pragma unroll
       for (int r = 0; r < P1; ++r) {
-        if (r < pr.w) {
+        if (r < pr.w && (SPLIT == 1 || r % SPLIT == h)) {
           double s = 0.0;
 #pragma unroll
           for (int k = 0; k < Q2; ++k) s = fma(__ldg(tab + k * n + r), x[k], s);

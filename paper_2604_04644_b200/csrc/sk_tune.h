@@ -68,7 +68,7 @@ constexpr int kTunedMinB[3][4][11] = {
 constexpr int kMinBCap[3][4][11] = {
     {{4, 4, 8, 4, 4, 5, 4, 5, 4, 4, 4},
      {4, 4, 4, 5, 8, 6, 8, 8, 8, 4, 4},
-     {4, 4, 8, 4, 6, 4, 8, 8, 5, 4, 4},
+     {4, 4, 8, 4, 4, 4, 8, 8, 5, 4, 4},
      {4, 4, 4, 8, 5, 4, 4, 4, 8, 4, 4}},
     {{4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 4},
      {4, 4, 4, 4, 4, 4, 4, 8, 4, 4, 4},
@@ -106,6 +106,12 @@ constexpr int kRaggedMaxP[3][4] = {
     {0, 0, 8, 8},  // transforms
 };
 
+// pyr/tet ragged r <-> k sweeps split over two threads per (element, pair)
+// line when the pairs fill at most half the CTA, from this order on, per
+// operator class (measured: tet Helmholtz P=9/10 +3 %/+15 %, P=3-8 -2..-7 %,
+// mass no gain)
+constexpr int kSplitMinP[3] = {9, 99, 99};
+
 // Overrides for tuning builds (-DSK_EB_FIXED=... etc.) apply to every class.
 #ifdef SK_EB_FIXED
 SK_HD constexpr int tuned_eb(int, int, int) { return SK_EB_FIXED; }
@@ -136,6 +142,12 @@ constexpr bool tuned_persist(int cls, int S, int P) { return cls == 0 && kPersis
 SK_HD constexpr bool ragged_dispatch(int, int, int P) { return P <= SK_RAGGED_MAXP; }
 #else
 SK_HD constexpr bool ragged_dispatch(int cls, int S, int P) { return P <= kRaggedMaxP[cls][S]; }
+#endif
+
+#ifdef SK_SPLIT_MINP
+SK_HD constexpr bool ragged_split(int, int, int P) { return P >= SK_SPLIT_MINP; }
+#else
+SK_HD constexpr bool ragged_split(int cls, int, int P) { return P >= kSplitMinP[cls]; }
 #endif
 
 }  // namespace sk
