@@ -29,7 +29,7 @@ template <int S, int P>
 struct Mode {
   using Dm = Dims<S, P>;
   static constexpr int smem_bytes(int eb) {
-    return 3 * Dm::Q0 * Dm::Q1 * (eb >= 16 ? Dm::Q2 : (Dm::Q2 | 1)) * eb * 8;
+    return 3 * Dm::Q0 * Dm::Q1 * row_stride(S, P, eb) * eb * 8;
   }
   static constexpr int fit(int eb, int budget) {
     return (eb <= 1 || smem_bytes(eb) <= budget) ? eb : fit(eb / 2, budget);

@@ -46,11 +46,31 @@ struct Dims {
 // reads 16 consecutive doubles whatever the sweep direction, and for
 // EB < 16 an odd row stride S2 keeps consecutive passive indices in
 // distinct bank groups, so every sweep is (nearly) bank-conflict free.
+// k-row stride of the work planes: the line length Q2 for EB >= 16, the
+// next odd value below that (16/EB passive indices per half-warp at odd
+// strides), or a per-(shape, order) override for single-element tiles where
+// no interleave separates the sweep patterns (SK_S2 / kRowStride, measured)
+#ifndef SK_S2
+#define SK_S2 0
+#endif
+constexpr int kRowStride[4][11] = {
+    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},  // hex
+    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},  // prism
+    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},  // pyr
+    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},  // tet
+};
+__host__ __device__ constexpr int row_stride(int S, int P, int EB) {
+  return EB >= 16 ? (S == HEX ? P + 2 : P + 1)
+         : SK_S2 >= (S == HEX ? P + 2 : P + 1) ? SK_S2
+         : kRowStride[S][P] > 0 ? kRowStride[S][P]
+                                : ((S == HEX ? P + 2 : P + 1) | 1);
+}
+
 template <int S, int P, int NPL, int EB_>
 struct Lay {
   using Dm = Dims<S, P>;
   static constexpr int EB = EB_;
-  static constexpr int S2 = EB >= 16 ? Dm::Q2 : (Dm::Q2 | 1);
+  static constexpr int S2 = row_stride(S, P, EB);
   static constexpr int PLANE = Dm::Q0 * Dm::Q1 * S2;
   // tile staging area for coefficients, [mode][XSTR] from the start of plane
   // 1: an odd stride keeps the transposing copy conflict free; it must fit

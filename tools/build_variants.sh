@@ -30,7 +30,7 @@ for v in "$@"; do
       ch) extra="$extra -DSK_GEO_CH=$n" ;;
       td) extra="$extra -DSK_TET_DISPATCH_MAXP=$n" ;;
       sl) extra="$extra -DSK_STREAM_LD=$n" ;;
-      ga) extra="$extra -DSK_GEO_ASYNC=$n" ;;
+      s) extra="$extra -DSK_S2=$n" ;;
     esac
   done
   make -j"$(nproc)" BUILD=/tmp/sk200_build_$v LIB=$ROOT/paper_2604_04644_b200/libsk200_$v.so LINEINFO= EXTRA="$extra" > /tmp/sk200_build_$v.log 2>&1 \
