@@ -7,7 +7,9 @@ Same flags, the same CSV schema (``CSV_HEADER``, bench.py:57) and exit codes
 two independent device routes at 1e-10 (the reference pairs two strategies,
 bench.py:196-216): Helmholtz collocated vs non-collocated kernels; mass vs
 ``iproduct_wrt_base(bwd_trans(u))``; bwd_trans into a fresh vs a reused
-output block.  Each batch is timed with the device synchronised on both sides.
+output block.  Each batch is timed with the device synchronised on both
+sides; ``seconds`` is the median batch time and ``dof_per_s`` = ndof x
+applies per batch / seconds, as in the reference.
 """
 
 from __future__ import annotations
@@ -27,7 +29,6 @@ from paper_2604_04644_b200.operators import (
     apply_operator,
     bwd_trans,
     iproduct_wrt_base,
-    operator_bytes,
     operator_flops,
 )
 from paper_2604_04644_b200.shapes import DEVICE_SHAPES, Shape, build_shape_basis
@@ -134,7 +135,7 @@ def run_bench(op, shapes, orders, nelems, geometry, form, lam, width, reps, warm
                 ndof = basis.n_modes * ne
                 rows.append(",".join([
                     op, shape.value, str(P), Strategy.SUM_FAC_TOP.value, geometry.value,
-                    form if op == "helmholtz" else "-", str(ne), str(ndof), f"{med / iters:.9e}",
+                    form if op == "helmholtz" else "-", str(ne), str(ndof), f"{med:.9e}",
                     f"{ndof * iters / med:.6e}", str(operator_flops(kind, shape, P)),
                 ]))
     return rows
