@@ -113,6 +113,8 @@ def _geo(block: Block) -> int:
 #: applied chunk-pipelined (H2D / kernel / D2H overlapped, sk_apply_streamed);
 #: smaller ones take the plain transfer-then-apply path
 STREAM_MIN_BYTES = 32 << 20
+#: elements per streamed chunk (0: the library default, ~16 chunks)
+STREAM_CHUNK_ELEMENTS = 0
 
 
 def _streamed(block: Block, out: Block, op: int, pay, lam: float) -> bool:
@@ -129,7 +131,7 @@ def _streamed(block: Block, out: Block, op: int, pay, lam: float) -> bool:
     _lib.check(
         _lib.load().sk_apply_streamed(
             block.basis.handle, op, _geo(block), block.n_elements, block.interleave_width, block.n_components,
-            _p(h_in), _p(d_in), _p(pay), float(lam), _p(d_out), _p(h_out), 0, _stream(),
+            _p(h_in), _p(d_in), _p(pay), float(lam), _p(d_out), _p(h_out), STREAM_CHUNK_ELEMENTS, _stream(),
         ),
         "sk_apply_streamed",
     )
