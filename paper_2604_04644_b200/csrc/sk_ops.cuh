@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(Op::NT, Op::MINB) k_tile(const __grid_constant
   const long long t = blockIdx.x;
   if (threadIdx.x < 32) {
     const long long ntiles = (A.Epad + Op::EB - 1) / Op::EB;
-    Op::prefetch_geo(A, t);
+    if (Op::GEO_PF_AT_START) Op::prefetch_geo(A, t);
     if (t + A.pf_ahead < ntiles) Op::prefetch_in(A, t + A.pf_ahead);
   }
   Op::run(A, t, sm);
@@ -188,6 +188,7 @@ struct k_helm {
     prefetch_field<Dims<S, P>::NM>(A.in, A.in_cstride, gridDim.y, e0, n, A.Epad, A.W);
   }
   static constexpr bool PERSIST = true;
+  static constexpr bool GEO_PF_AT_START = kGeoPrefetch == 1;
   using Pre = TileRegs<L, Dims<S, P>::NM, NT_>;
   __device__ static void pre_load(const OpArgs<S, P>& A, long long t, Pre& p) {
     p.load(A.in + blockIdx.y * A.in_cstride, make_ctx<L::EB>(t, A.E, A.Epad, A.W));
@@ -214,6 +215,7 @@ struct k_helm {
   __syncthreads();
   stage_f2<S, P, L, NT, TAo, TBo>(A.B, A.gtab, sm);
   __syncthreads();
+  if (kGeoPrefetch == 2 && tnext < 0 && threadIdx.x < 32) prefetch_geo(A, tile);
   // F3 + D0: u along i, v0 = D0 u
   items<L, Q1 * Q2, NT>([&](int e, int ps) {
     const int j = ps / Q2, k = ps - j * Q2;
@@ -390,6 +392,7 @@ struct k_mass {
     prefetch_field<Dims<S, P>::NM>(A.in, A.in_cstride, gridDim.y, e0, n, A.Epad, A.W);
   }
   static constexpr bool PERSIST = true;
+  static constexpr bool GEO_PF_AT_START = true;
   using Pre = TileRegs<L, Dims<S, P>::NM, NT_>;
   __device__ static void pre_load(const OpArgs<S, P>& A, long long t, Pre& p) {
     p.load(A.in + blockIdx.y * A.in_cstride, make_ctx<L::EB>(t, A.E, A.Epad, A.W));
@@ -446,6 +449,7 @@ struct k_bwd {
   static constexpr int EB = L::EB;
   static constexpr int MINB = MINB_;
   static constexpr bool PERSIST = false;
+  static constexpr bool GEO_PF_AT_START = true;
   __device__ static void prefetch_geo(const OpArgs<S, P>& A, long long t) {
     const long long e0 = t * EB;
     const long long n = A.E - e0 < EB ? A.E - e0 : EB;
@@ -496,6 +500,7 @@ struct k_iprod {
   static constexpr int EB = L::EB;
   static constexpr int MINB = MINB_;
   static constexpr bool PERSIST = false;
+  static constexpr bool GEO_PF_AT_START = true;
   __device__ static void prefetch_geo(const OpArgs<S, P>& A, long long t) {
     const long long e0 = t * EB;
     const long long n = A.E - e0 < EB ? A.E - e0 : EB;
@@ -548,6 +553,7 @@ struct k_pderiv {
   static constexpr int EB = L::EB;
   static constexpr int MINB = MINB_;
   static constexpr bool PERSIST = false;
+  static constexpr bool GEO_PF_AT_START = true;
   __device__ static void prefetch_geo(const OpArgs<S, P>& A, long long t) {
     const long long e0 = t * EB;
     const long long n = A.E - e0 < EB ? A.E - e0 : EB;
@@ -647,6 +653,7 @@ struct k_ipderiv {
   static constexpr int EB = L::EB;
   static constexpr int MINB = MINB_;
   static constexpr bool PERSIST = false;
+  static constexpr bool GEO_PF_AT_START = true;
   __device__ static void prefetch_geo(const OpArgs<S, P>& A, long long t) {
     const long long e0 = t * EB;
     const long long n = A.E - e0 < EB ? A.E - e0 : EB;
@@ -741,6 +748,7 @@ struct k_helm_nc {
   static constexpr int EB = L::EB;
   static constexpr int MINB = MINB_;
   static constexpr bool PERSIST = false;
+  static constexpr bool GEO_PF_AT_START = true;
   using A_t = NcArgs<S, P>;
   __device__ static void prefetch_geo(const A_t& A, long long t) {
     const long long e0 = t * EB;

@@ -80,6 +80,14 @@ constexpr int kMinBCap[3][4][11] = {
      {4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 4}},
 };
 
+// Helmholtz geometry L2 prefetch of a tile: 1 = at tile start (bulk TMA
+// prefetch, SASS UBLKPF), 2 = after the F2 sweep, 0 = none
+#ifdef SK_GEO_PF
+constexpr int kGeoPrefetch = SK_GEO_PF;
+#else
+constexpr int kGeoPrefetch = 1;
+#endif
+
 // points per geometry-load chunk in the Helmholtz metric sweep (lines longer
 // than 6 points): 7*CH doubles in flight per thread
 #ifdef SK_GEO_CH
