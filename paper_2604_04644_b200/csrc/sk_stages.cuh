@@ -373,32 +373,7 @@ __device__ __forceinline__ void stage_f1(const FwdTab<S, P>& B, const double* __
         }
       }
     });
-  } else if constexpr (S == PRISM && P <= kPrismUniformMaxP) {
-    // item = (e, q); p unrolled so c2[p] is uniform (operators.py:275-295)
-    items<L, P1, NT>([&](int e, int q) {
-      double u0q1 = 0.0;
-      int off = 0;
-#pragma unroll
-      for (int p = 0; p < P1; ++p) {
-        const int n = P1 - p;
-        double x[P1];
-#pragma unroll
-        for (int r = 0; r < P1; ++r) x[r] = r < n ? xin(e, off + q * n + r) : 0.0;
-        if (p == 0) u0q1 = x[1];  // mode (0, q, 1): collapsed-edge share
-        const int co = wfam_off(Q2, P1, p);
-#pragma unroll
-        for (int k = 0; k < Q2; ++k) {
-          double s = B.c2[co + k * n] * x[0];
-#pragma unroll
-          for (int r = 1; r < P1; ++r)
-            if (r < n) s = fma(B.c2[co + k * n + r], x[r], s);
-          if (p == 1) s = fma(u0q1, B.c2[k * P1 + 1], s);
-          sm[L::at(e, TAo + (p * P1 + q) * S2 + k)] = s;
-        }
-        off += P1 * n;
-      }
-    });
-  } else if constexpr (S != PRISM && RD) {
+  } else if constexpr ((S == PYR || S == TET) && RD) {
     // pyr / tet: item = (e, (p,q) pair), pairs ordered by slice; the slice
     // m = max(p,q) (pyr) or p+q (tet) is dispatched to a compile-time
     // constant so c2[m] entries are uniform operands (operators.py:209-351)
@@ -435,6 +410,37 @@ __device__ __forceinline__ void stage_f1(const FwdTab<S, P>& B, const double* __
           }
         }
       });
+    });
+  } else if constexpr (S == PRISM && P <= kPrismUniformMaxP && !RD) {
+    // item = (e, q[, p parity]); p unrolled so c2[p] is uniform
+    // (operators.py:275-295).  SPLIT = 2 halves the slices between two
+    // threads (even / odd p, parity slowest so warps stay uniform) when the
+    // items fill at most half the CTA
+    constexpr int SPLIT = SPL && 2 * L::EB * P1 <= NT ? 2 : 1;
+    items<L, P1 * SPLIT, NT>([&](int e, int q2) {
+      const int h = q2 / P1, q = q2 - h * P1;
+      const double u0q1 = xin(e, q * P1 + 1);  // mode (0, q, 1): collapsed-edge share
+      int off = 0;
+#pragma unroll
+      for (int p = 0; p < P1; ++p) {
+        const int n = P1 - p;
+        if (SPLIT == 1 || p % SPLIT == h) {
+          double x[P1];
+#pragma unroll
+          for (int r = 0; r < P1; ++r) x[r] = r < n ? xin(e, off + q * n + r) : 0.0;
+          const int co = wfam_off(Q2, P1, p);
+#pragma unroll
+          for (int k = 0; k < Q2; ++k) {
+            double s = B.c2[co + k * n] * x[0];
+#pragma unroll
+            for (int r = 1; r < P1; ++r)
+              if (r < n) s = fma(B.c2[co + k * n + r], x[r], s);
+            if (p == 1) s = fma(u0q1, B.c2[k * P1 + 1], s);
+            sm[L::at(e, TAo + (p * P1 + q) * S2 + k)] = s;
+          }
+        }
+        off += P1 * n;
+      }
     });
   } else {
     // prism / pyr / tet: item = (e, (p,q) pair); the dir-2 slice c2[p]
@@ -732,37 +738,7 @@ __device__ __forceinline__ void stage_b3(const FwdTab<S, P>& B, const double* __
         }
       }
     });
-  } else if constexpr (S == PRISM && P <= kPrismUniformMaxP) {
-    items<L, P1, NT>([&](int e, int q) {
-      int off = 0;
-#pragma unroll
-      for (int p = 0; p < P1; ++p) {
-        const int n = P1 - p;
-        const int co = wfam_off(Q2, P1, p);
-        double x[Q2];
-#pragma unroll
-        for (int k = 0; k < Q2; ++k) x[k] = sm[L::at(e, TAo + (p * P1 + q) * S2 + k)];
-#pragma unroll
-        for (int r = 0; r < P1; ++r) {
-          if (r < n) {
-            double s = B.c2[co + r] * x[0];
-#pragma unroll
-            for (int k = 1; k < Q2; ++k) s = fma(B.c2[co + k * n + r], x[k], s);
-            if (p == 0 && r == 1) {
-              // modes (0,q,1) += sum_k c2[0][k][1] TA[1][q][k] (operators.py:312-317)
-              double corr = 0.0;
-#pragma unroll
-              for (int k = 0; k < Q2; ++k)
-                corr = fma(B.c2[k * P1 + 1], sm[L::at(e, TAo + (1 * P1 + q) * S2 + k)], corr);
-              s += corr;
-            }
-            out(e, off + q * n + r, s);
-          }
-        }
-        off += P1 * n;
-      }
-    });
-  } else if constexpr (S != PRISM && RD) {
+  } else if constexpr ((S == PYR || S == TET) && RD) {
     // pyr / tet with the slice dispatched to a compile-time constant; outputs
     // split over two threads (r parity) when the pairs fill half the CTA
     constexpr int SPLIT = SPL && 2 * L::EB * Dm::NPAIR <= NT ? 2 : 1;
@@ -804,6 +780,42 @@ __device__ __forceinline__ void stage_b3(const FwdTab<S, P>& B, const double* __
           }
         }
       });
+    });
+  } else if constexpr (S == PRISM && P <= kPrismUniformMaxP && !RD) {
+    constexpr int SPLIT = SPL && 2 * L::EB * P1 <= NT ? 2 : 1;  // see stage_f1
+    items<L, P1 * SPLIT, NT>([&](int e, int q2) {
+      const int h = q2 / P1, q = q2 - h * P1;
+      int off = 0;
+#pragma unroll
+      for (int p = 0; p < P1; ++p) {
+        const int n = P1 - p;
+        if (SPLIT > 1 && p % SPLIT != h) {
+          off += P1 * n;
+          continue;
+        }
+        const int co = wfam_off(Q2, P1, p);
+        double x[Q2];
+#pragma unroll
+        for (int k = 0; k < Q2; ++k) x[k] = sm[L::at(e, TAo + (p * P1 + q) * S2 + k)];
+#pragma unroll
+        for (int r = 0; r < P1; ++r) {
+          if (r < n) {
+            double s = B.c2[co + r] * x[0];
+#pragma unroll
+            for (int k = 1; k < Q2; ++k) s = fma(B.c2[co + k * n + r], x[k], s);
+            if (p == 0 && r == 1) {
+              // modes (0,q,1) += sum_k c2[0][k][1] TA[1][q][k] (operators.py:312-317)
+              double corr = 0.0;
+#pragma unroll
+              for (int k = 0; k < Q2; ++k)
+                corr = fma(B.c2[k * P1 + 1], sm[L::at(e, TAo + (1 * P1 + q) * S2 + k)], corr);
+              s += corr;
+            }
+            out(e, off + q * n + r, s);
+          }
+        }
+        off += P1 * n;
+      }
     });
   } else {
     constexpr int SPLIT = SPL && 2 * L::EB * Dm::NPAIR <= NT ? 2 : 1;  // see the dispatch path

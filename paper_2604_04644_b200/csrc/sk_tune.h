@@ -107,18 +107,26 @@ constexpr int kPersist[4][11] = {
 };
 
 // pyr/tet ragged r <-> k sweeps: compile-time slice dispatch up to this
-// order (uniform table operands), L1 table reads above it (code size)
+// order (uniform table operands), L1 table reads above it (code size).
+// Prism: up to this order one item per (element, p, q) pair with L1 tables
+// instead of one per (element, q) with all p unrolled (balances the stage
+// across the CTA; the unrolled form idles most threads)
 constexpr int kRaggedMaxP[3][4] = {
     {0, 0, 6, 5},  // Helmholtz / stiffness
     {0, 0, 8, 8},  // mass
     {0, 0, 8, 8},  // transforms
 };
 
-// pyr/tet ragged r <-> k sweeps split over two threads per (element, pair)
-// line when the pairs fill at most half the CTA, from this order on, per
-// operator class (measured: tet Helmholtz P=9/10 +3 %/+15 %, P=3-8 -2..-7 %,
-// mass no gain)
-constexpr int kSplitMinP[3] = {9, 99, 99};
+// r <-> k sweeps split over two threads per line when the lines fill at most
+// half the CTA (pyr/tet (p,q) pairs: halves of k / r parity; prism (e, q)
+// lines: p parity), from this order on, per operator class x shape.
+// Measured: tet Helmholtz P=9/10 +3 %/+15 % (P=3-8 -2..-7 %), prism mass
+// P>=5 +2..5 %, elsewhere no gain (tune14_op1.jsonl)
+constexpr int kSplitMinP[3][4] = {
+    {99, 99, 99, 9},  // Helmholtz / stiffness
+    {99, 5, 99, 99},  // mass
+    {99, 99, 99, 99},  // transforms
+};
 
 // Overrides for tuning builds (-DSK_EB_FIXED=... etc.) apply to every class.
 #ifdef SK_EB_FIXED
@@ -155,7 +163,7 @@ SK_HD constexpr bool ragged_dispatch(int cls, int S, int P) { return P <= kRagge
 #ifdef SK_SPLIT_MINP
 SK_HD constexpr bool ragged_split(int, int, int P) { return P >= SK_SPLIT_MINP; }
 #else
-SK_HD constexpr bool ragged_split(int cls, int, int P) { return P >= kSplitMinP[cls]; }
+SK_HD constexpr bool ragged_split(int cls, int S, int P) { return P >= kSplitMinP[cls][S]; }
 #endif
 
 }  // namespace sk
