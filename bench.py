@@ -512,6 +512,26 @@ def run_c0(args, ws, rank, dist, dev, wl):
         dist.destroy_process_group()
 
 
+def run_reference_sweep(args):
+    """Reference CPU path (oracle port of speckern's sum-factorised Helmholtz,
+    all host cores) per shape x order: one JSON line each, to sit beside the
+    device sweep (tools/sweep.py).  Bounded samples (~2 s per case)."""
+    cores = os.cpu_count() or 1
+    for shape in ("hex", "prism", "pyr", "tet"):
+        for P in range(1, 11):
+            per_core = max(8, int(2048 * (5.0 / (P + 1)) ** 3))
+            ref = CpuReference(cores, per_core, [(shape, P)])
+            reps = ref.calibrate(1.5)
+            vals = []
+            for _ in range(3):
+                dof, dt = ref.run(reps)
+                vals.append(dof / dt / 1e9)
+            ref.close()
+            print(json.dumps({"impl": "reference", "op": "helm", "shape": shape, "P": P,
+                              "gdof_s": statistics.median(vals), "cores": cores, "kind": "port",
+                              "sample": f"{per_core * cores} elements x {reps} passes, median of 3"}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -520,8 +540,13 @@ def main():
     ap.add_argument("--impl", choices=["sk", "reference"], default="sk")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="tet4")
     ap.add_argument("--elements", type=int, default=0, help="override elements per block per GPU")
+    ap.add_argument("--sweep", action="store_true", help="with --impl reference: CPU GDOF/s per shape x order")
     args = ap.parse_args()
     ws, rank, local = _dist()
+    if args.impl == "reference" and args.sweep:
+        if rank == 0:
+            run_reference_sweep(args)
+        return
     if args.impl == "reference":
         run_reference(args, ws, rank)
         return
