@@ -229,3 +229,19 @@ def test_streamed_host_apply(sk, shape, P, width, ncomp):
         assert np.array_equal(got, want), kind
         # the device copy of the streamed output is live and identical
         assert np.array_equal(out.device().cpu().numpy(), out.host().reshape(-1))
+
+
+@pytest.mark.parametrize("shape,P,n", [("hex", 9, 2500), ("pyr", 3, 40000)])
+def test_persistent_tiles_at_scale(sk, shape, P, n):
+    """(shape, P) launched as persistent CTAs (sk_tune.h kPersist): enough
+    elements that every CTA strides over several tiles, exercising the
+    register-staged next tile and the in-body geometry prefetch; compared
+    with the oracle on every element."""
+    el = O.element(shape, P)
+    geo = O.synthetic_geometry(el, True, n, seed=7)
+    blk = _block_from(sk, shape, P, geo, 1)
+    x = np.random.default_rng(3).uniform(-1, 1, (el.nm, n))
+    blk.set_elements(x[None])
+    blk.device()
+    got = sk.helmholtz_apply(blk, 0.7).get_elements()[0]
+    assert _err(got, O.helmholtz_coll(el, geo, x, 0.7)) <= TOL
