@@ -144,6 +144,11 @@ int sk_c0_gather(int order, int nx, int ny, int64_t nz_local, const double* x, i
                  void* stream);
 int sk_c0_scatter(int order, int nx, int ny, int64_t nz_local, const double* local, int W, double* y,
                   void* stream);
+/* Elemental Helmholtz of the slab with the gather fused into the kernel's
+ * tile load: out (element-major, W = 1) = H_e (A x) without materialising
+ * A x.  Deformed geometry, lam > 0, hex bases only. */
+int sk_helmholtz_apply_c0(const sk_basis* b, int geo_class, int nx, int ny, int64_t nz_local, const double* x,
+                          const double* hpay, double lam, double* out, void* stream);
 
 /* ---- diagnostics ------------------------------------------------------------ */
 /* Number of kernel launches this thread issued through the library. */

@@ -47,6 +47,7 @@ SIGNATURES = {
     "sk_apply_streamed": (_I, [_P, _I, _I, _L, _I, _I, _P, _P, _P, _D, _P, _P, _L, _P]),
     "sk_c0_gather": (_I, [_I, _I, _I, _L, _P, _I, _P, _P]),
     "sk_c0_scatter": (_I, [_I, _I, _I, _L, _P, _I, _P, _P]),
+    "sk_helmholtz_apply_c0": (_I, [_P, _I, _I, _I, _L, _P, _P, _D, _P, _P]),
     "sk_launch_count": (_L, []),
     "sk_last_error": (ctypes.c_char_p, []),
     "sk_launch_config": (_I, [_P, _I, _PL]),

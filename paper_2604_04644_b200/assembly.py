@@ -1,9 +1,10 @@
 """Assembled C0 Helmholtz on a conforming hex mesh, sharded by z-slabs
 (BASELINE configs[4] "with assembled C0 variant").
 
-y = A^T H_e A x: the elemental collocated Helmholtz kernel between a
-device gather (global C0 DOFs -> element modal coefficients) and a
-deterministic device scatter (sk_c0_gather / sk_c0_scatter).  Each rank owns
+y = A^T H_e A x: the elemental collocated Helmholtz kernel with the gather
+(global C0 DOFs -> element modal coefficients) fused into its tile load
+(sk_helmholtz_apply_c0; the stand-alone sk_c0_gather serves lam = 0), then a
+deterministic device scatter (sk_c0_scatter).  Each rank owns
 a contiguous slab of element layers; the two DOF layers on a slab boundary
 are shared with the neighbouring ranks and are summed by one neighbour
 exchange over NCCL (``torch.distributed`` P2P: send/recv of one
@@ -97,13 +98,24 @@ class C0HexMesh:
 
         lib = _lib.load()
         s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
-        local = self.block.device(AccessQualifier.WRITE_ONLY)
-        _lib.check(
-            lib.sk_c0_gather(self.P, self.nx, self.ny, self.nzl, ctypes.c_void_p(x.data_ptr()), 1,
-                             ctypes.c_void_p(local.data_ptr()), s),
-            "sk_c0_gather",
-        )
-        helmholtz_apply(self.block, lam, out=self.out)
+        if lam > 0.0:
+            # gather fused into the Helmholtz tile load (no A x round trip through HBM)
+            pay = self.block.payload(_lib.SK_PAYLOAD_HELMHOLTZ)
+            out = self.out.device(AccessQualifier.WRITE_ONLY)
+            _lib.check(
+                lib.sk_helmholtz_apply_c0(self.basis.handle, _lib.SK_GEO_DEFORMED, self.nx, self.ny, self.nzl,
+                                          ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(pay.data_ptr()),
+                                          float(lam), ctypes.c_void_p(out.data_ptr()), s),
+                "sk_helmholtz_apply_c0",
+            )
+        else:
+            local = self.block.device(AccessQualifier.WRITE_ONLY)
+            _lib.check(
+                lib.sk_c0_gather(self.P, self.nx, self.ny, self.nzl, ctypes.c_void_p(x.data_ptr()), 1,
+                                 ctypes.c_void_p(local.data_ptr()), s),
+                "sk_c0_gather",
+            )
+            helmholtz_apply(self.block, lam, out=self.out)
         y = torch.empty(self.n_dofs, dtype=torch.float64, device=x.device)
         loc = self.out.device(AccessQualifier.READ_ONLY)
         _lib.check(

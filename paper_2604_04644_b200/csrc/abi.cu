@@ -423,6 +423,39 @@ int sk_apply_streamed(const sk_basis* b, int op, int geo, int64_t E, int W, int 
   return cuda_status(e, "streamed apply");
 }
 
+int sk_helmholtz_apply_c0(const sk_basis* b, int geo, int nx, int ny, int64_t nz_local, const double* x,
+                          const double* hpay, double lam, double* out, void* stream) {
+  if (!b || nx < 1 || ny < 1 || nz_local < 0) return fail(SK_ERR_ARG, "bad C0 slab");
+  if (b->ops->S != sk::HEX) return fail(SK_ERR_UNSUPPORTED, "assembled C0 variant is hex only");
+  if (geo != SK_GEO_DEFORMED || !(lam > 0.0)) return fail(SK_ERR_UNSUPPORTED, "fused C0 gather: deformed, lam > 0");
+  const long long E = (long long)nx * ny * nz_local;
+  if (E > 0 && (!x || !hpay || !out)) return fail(SK_ERR_ARG, "null argument");
+  if (E == 0) return SK_OK;
+  int st = SK_OK;
+  const double* g = device_gtab(const_cast<sk_basis*>(b), &st);
+  if (st) return st;
+  sk::LaunchReq r;
+  r.fwd = b->fwd_vals.data();
+  r.fwd_d = b->fwd_ders.data();
+  r.dtab = b->dtab.data();
+  r.in = x;
+  r.out = out;
+  r.pay = hpay;
+  r.gtab = g;
+  r.E = E;
+  r.Epad = E;
+  r.in_cs = 0;
+  r.out_cs = E * b->hb.nm;
+  r.W = 1;
+  r.ncomp = 1;
+  r.geo = geo;
+  r.lam = lam;
+  r.c0_nx = nx;
+  r.c0_ny = ny;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cuda_status(b->ops->launch(sk::OP_HELM, r, stream), "kernel launch");
+}
+
 int64_t sk_launch_count(void) { return g_launches.load(); }
 
 }  // extern "C"

@@ -297,6 +297,8 @@ int launch(int op, const LaunchReq& r, void* stream) {
   a.in_cstride = r.in_cs;
   a.out_cstride = r.out_cs;
   a.W = r.W;
+  a.c0_nx = r.c0_nx;
+  a.c0_ny = r.c0_ny;
   a.pad_ = 0;
   a.lam = r.lam;
   const bool def = r.geo == GEO_DEFORMED;
@@ -309,6 +311,14 @@ int launch(int op, const LaunchReq& r, void* stream) {
 #if !defined(SK_ONLY_OP) || SK_ONLY_OP == 0
     case OP_HELM: {
       using C = Cfg<S, P, OP_HELM>;
+      if (r.c0_nx > 0) {
+        // assembled C0 hex: gather fused into the tile load (deformed, lam > 0)
+        if constexpr (S == HEX) {
+          if (def && r.lam != 0.0)
+            return go<S, P, OP_HELM, k_helm<S, P, typename C::L, C::NT, C::PW, GEO_DEFORMED, true, C::MINB, true>>(a, r, 1, stream);
+        }
+        return (int)cudaErrorInvalidValue;
+      }
       if (def) {
         if (r.lam != 0.0) return go<S, P, OP_HELM, k_helm<S, P, typename C::L, C::NT, C::PW, GEO_DEFORMED, true, C::MINB>>(a, r, r.ncomp, stream);
         return go<S, P, OP_HELM, k_helm<S, P, typename C::L, C::NT, C::PW, GEO_DEFORMED, false, C::MINB>>(a, r, r.ncomp, stream);

@@ -39,9 +39,34 @@ struct OpArgs {
   long long in_cstride, out_cstride;  // doubles between components
   long long pf_ahead;  // tiles between a CTA and the one whose input it prefetches
   int W;
+  int c0_nx, c0_ny;  // assembled C0 hex slab (fused gather from the global DOF vector)
   int pad_;
   double lam;
 };
+
+// Assembled C0 hex slab: the coefficient tile gathered straight from the
+// global C0 DOF vector x (fuses sk_c0_gather into the Helmholtz load; the
+// map is assembly.cu's: element e = (ez*ny + ey)*nx + ex, 1D DOF of mode k of
+// element el = el*P + (0, P, k-1 for k = 0, 1, >= 2)).  Consecutive threads
+// take consecutive elements of one mode (addresses P doubles apart; the
+// neighbouring modes' loads hit the same lines in L1).
+template <class L, int P, int NT>
+__device__ __forceinline__ void load_tile_c0(const double* __restrict__ x, const Ctx& c, int nx, int ny, double* xs) {
+  constexpr int P1 = P + 1, NM = P1 * P1 * P1, EB = L::EB, XS = L::XSTR;
+  const long long Nx = (long long)nx * P + 1, Ny = (long long)ny * P + 1;
+  auto md = [](long long el, int k) { return el * P + (k == 0 ? 0 : k == 1 ? P : k - 1); };
+  for (int g = threadIdx.x; g < EB * NM; g += NT) {
+    const int m = g / EB, e = g - m * EB;
+    const long long eg = c.e0 + e;
+    double v = 0.0;
+    if (eg < c.E) {
+      const int r = m % P1, q = (m / P1) % P1, p = m / (P1 * P1);
+      const long long ex = eg % nx, ey = (eg / nx) % ny, ez = eg / ((long long)nx * ny);
+      v = __ldg(x + (md(ez, r) * Ny + md(ey, q)) * Nx + md(ex, p));
+    }
+    xs[m * XS + e] = v;
+  }
+}
 
 // arguments of the non-collocated Helmholtz: value and derivative tables
 template <int S, int P>
@@ -170,7 +195,7 @@ __global__ void __launch_bounds__(Op::NT, Op::MINB) k_persist(const __grid_const
 
 // ---------------------------------------------------------------------------
 // Helmholtz, collocated: 9 sweeps + coefficient tile staging, 10 CTA barriers
-template <int S, int P, class L, int NT_, int PW, int GEO, bool LAMW, int MINB_>
+template <int S, int P, class L, int NT_, int PW, int GEO, bool LAMW, int MINB_, bool C0 = false>
 struct k_helm {
   static constexpr int NT = NT_;
   static constexpr int EB = L::EB;
@@ -183,11 +208,12 @@ struct k_helm {
     if constexpr (GEO == GEO_DEFORMED) prefetch_payload<PW>(A.pay, e0, n, A.E, 7, Dims<S, P>::NQ, LAMW ? 7 : 6);
   }
   __device__ static void prefetch_in(const OpArgs<S, P>& A, long long t) {
+    if constexpr (C0) return;  // input is the global DOF vector, read through L1
     const long long e0 = t * EB;
     const long long n = A.Epad - e0 < EB ? A.Epad - e0 : EB;
     prefetch_field<Dims<S, P>::NM>(A.in, A.in_cstride, gridDim.y, e0, n, A.Epad, A.W);
   }
-  static constexpr bool PERSIST = true;
+  static constexpr bool PERSIST = !C0;  // the register-staged next tile assumes the field layout
   static constexpr bool GEO_PF_AT_START = kGeoPrefetch == 1;
   using Pre = TileRegs<L, Dims<S, P>::NM, NT_>;
   __device__ static void pre_load(const OpArgs<S, P>& A, long long t, Pre& p) {
@@ -197,7 +223,10 @@ struct k_helm {
   __device__ static void run(const OpArgs<S, P>& A, long long tile, double* sm) {
     using Dm = Dims<S, P>;
     const Ctx c = make_ctx<L::EB>(tile, A.E, A.Epad, A.W);
-    load_tile<L, Dm::NM, NT>(A.in + blockIdx.y * A.in_cstride, c, sm + L::EB * L::PLANE);
+    if constexpr (C0)
+      load_tile_c0<L, P, NT>(A.in, c, A.c0_nx, A.c0_ny, sm + L::EB * L::PLANE);
+    else
+      load_tile<L, Dm::NM, NT>(A.in + blockIdx.y * A.in_cstride, c, sm + L::EB * L::PLANE);
     __syncthreads();
     body(A, tile, sm, -1);
   }

@@ -22,6 +22,7 @@ struct LaunchReq {
   long long E, Epad, in_cs, out_cs;
   int W, ncomp, geo;
   double lam;
+  int c0_nx = 0, c0_ny = 0;  // > 0: assembled C0 hex slab, `in` is the global DOF vector
 };
 
 struct OpSet {

@@ -47,3 +47,18 @@ def test_assembled_stiffness_annihilates_constants(torch):
     # and the mass of the constant is the (deformed) volume
     vol = c @ mesh.helmholtz(torch.from_numpy(c).cuda(), 1.0).cpu().numpy()
     assert abs(vol - nx * ny * nz) <= 1e-6 * nx * ny * nz
+
+
+@pytest.mark.parametrize("P,dims", [(4, (13, 7, 11)), (3, (9, 5, 6)), (8, (5, 4, 3))])
+def test_fused_gather_many_tiles(torch, P, dims):
+    """The gather fused into the Helmholtz tile load (sk_helmholtz_apply_c0):
+    tiles straddle mesh rows (nx not a multiple of the tile width) and
+    element layers; identical to the stand-alone gather route and to the
+    oracle."""
+    from paper_2604_04644_b200.assembly import C0HexMesh
+
+    nx, ny, nz = dims
+    mesh = C0HexMesh(nx, ny, nz, P)
+    x = np.random.default_rng(P + 100).standard_normal(mesh.n_dofs)
+    y = mesh.helmholtz(torch.from_numpy(x).cuda(), 0.8).cpu().numpy()
+    assert O.rel_diff(y, A.assembled_helmholtz(nx, ny, nz, P, x, 0.8)) <= 1e-12

@@ -231,15 +231,15 @@ def test_streamed_host_apply(sk, shape, P, width, ncomp):
         assert np.array_equal(out.device().cpu().numpy(), out.host().reshape(-1))
 
 
-@pytest.mark.parametrize("shape,P,n", [("hex", 9, 2500), ("pyr", 3, 40000)])
-def test_persistent_tiles_at_scale(sk, shape, P, n):
+@pytest.mark.parametrize("shape,P,n,width", [("hex", 9, 2500, 1), ("pyr", 3, 40001, 1), ("pyr", 3, 30011, 3)])
+def test_persistent_tiles_at_scale(sk, shape, P, n, width):
     """(shape, P) launched as persistent CTAs (sk_tune.h kPersist): enough
     elements that every CTA strides over several tiles, exercising the
     register-staged next tile and the in-body geometry prefetch; compared
     with the oracle on every element."""
     el = O.element(shape, P)
     geo = O.synthetic_geometry(el, True, n, seed=7)
-    blk = _block_from(sk, shape, P, geo, 1)
+    blk = _block_from(sk, shape, P, geo, width)
     x = np.random.default_rng(3).uniform(-1, 1, (el.nm, n))
     blk.set_elements(x[None])
     blk.device()
