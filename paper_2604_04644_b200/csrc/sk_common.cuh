@@ -198,9 +198,16 @@ __device__ __forceinline__ void dispatch(int v, F&& f) {
   }
 }
 
+// passes of a sweep's item loop unrolled together (independent items give
+// the scheduler ILP across them; 1 keeps code size and registers minimal)
+#ifndef SK_ITEMS_UNROLL
+#define SK_ITEMS_UNROLL 1
+#endif
+constexpr int kItemsUnroll = SK_ITEMS_UNROLL;
+
 template <class L, int NPASS, int NT, class F>
 __device__ __forceinline__ void items(F&& f) {
-#pragma unroll 1
+#pragma unroll kItemsUnroll
   for (int w = threadIdx.x; w < L::EB * NPASS; w += NT) {
     const int ps = w / L::EB;
     f(w - ps * L::EB, ps);
