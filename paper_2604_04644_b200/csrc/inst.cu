@@ -115,6 +115,10 @@ void fill_fwd(const HostBasis& hb, FwdTab<S, P>& t, bool deriv) {
   }
 }
 
+// Duffy scale of the 1D weights per shape x direction (basis_host.cpp
+// build_basis: refw = (w0 s0)(w1 s1)(w2 s2), shapes.py ref_weights)
+constexpr double kWScale[4][3] = {{1.0, 1.0, 1.0}, {1.0, 1.0, 0.5}, {1.0, 1.0, 0.25}, {1.0, 0.5, 0.25}};
+
 template <int S, int P>
 void fill(const HostBasis& hb, void* fv, void* fd, void* dt) {
   using Dm = Dims<S, P>;
@@ -134,6 +138,10 @@ void fill(const HostBasis& hb, void* fv, void* fd, void* dt) {
   if constexpr (gll_dir(S, 2)) {
     fill_eo<Dm::Q2>(hb.D[2], false, d.e2);
     fill_eo<Dm::Q2>(hb.D[2], true, d.e2t);
+  }
+  for (int k = 0; k < Dm::Q2; ++k) {
+    d.ak[k] = S == HEX ? 0.0 : 1.0 / (1.0 - hb.z[2][k]);
+    d.w2k[k] = hb.w[2][k] * kWScale[S][2];
   }
 }
 
@@ -205,6 +213,22 @@ void fill_gtab(const HostBasis& hb, double* g) {
         g[L::REFW + l] = hb.refw[l];
         for (int a = 0; a < 9; ++a) g[X::GST + 9 * l + a] = G[a];
       }
+  for (int i = 0; i < Dm::Q0; ++i)
+    for (int j = 0; j < Dm::Q1; ++j) {
+      const int ps = i * Dm::Q1 + j, n2 = Dm::Q0 * Dm::Q1;
+      const double e1 = hb.z[0][i], e2 = hb.z[1][j];
+      double c00 = 0.0, c20 = 0.0, c21 = 0.0;
+      if (S == PRISM) c00 = 2.0, c20 = 1.0 + e1;
+      if (S == PYR) c00 = 2.0, c20 = 1.0 + e1, c21 = 1.0 + e2;
+      if (S == TET) {
+        const double b = 1.0 / (1.0 - e2);
+        c00 = 4.0 * b, c20 = 2.0 * (1.0 + e1) * b, c21 = 1.0 + e2;
+      }
+      g[L::REGIJ + 0 * n2 + ps] = (hb.w[0][i] * kWScale[S][0]) * (hb.w[1][j] * kWScale[S][1]);
+      g[L::REGIJ + 1 * n2 + ps] = c00;
+      g[L::REGIJ + 2 * n2 + ps] = c20;
+      g[L::REGIJ + 3 * n2 + ps] = c21;
+    }
   std::memcpy(g + X::DM0, hb.D[0].data(), sizeof(double) * Dm::Q0 * Dm::Q0);
   std::memcpy(g + X::DM1, hb.D[1].data(), sizeof(double) * Dm::Q1 * Dm::Q1);
   std::memcpy(g + X::DM2, hb.D[2].data(), sizeof(double) * Dm::Q2 * Dm::Q2);

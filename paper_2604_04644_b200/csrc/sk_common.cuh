@@ -142,6 +142,10 @@ struct DTab {
   EOTab<Dm::Q0> e0, e0t;
   EOTab<gll_dir(S, 1) ? Dm::Q1 : 2> e1, e1t;
   EOTab<gll_dir(S, 2) ? Dm::Q2 : 2> e2, e2t;
+  // regular geometry: Duffy factor a_k = 1/(1 - z2[k]) and scaled dir-2
+  // weights, per k (uniform operands of the unrolled metric loop)
+  double ak[Dm::Q2];
+  double w2k[Dm::Q2];
 };
 
 // Layout of the per-basis device table buffer ("gtab"), runtime indexed.
@@ -155,7 +159,11 @@ struct GLayout {
   static constexpr int REFW = REGK + 6 * Dm::NQ;         // [i][j][k] refw
   static constexpr int B1 = REFW + Dm::NQ;               // tet dir-1 family values
   static constexpr int DB1 = B1 + Dm::Q1 * Dm::NTRI;     // tet dir-1 family derivatives
-  static constexpr int SIZE = DB1 + Dm::Q1 * Dm::NTRI;
+  // regular-geometry metric, per (i, j) line: [4][i*Q1+j] = w0 w1 (scaled
+  // 1D weights), c00, c20, c21 with G00 = a c00, G20 = a c20, G21 = a c21,
+  // a = 1/(1 - z2[k]) (DTab::ak); tet G10 = G20, G11 = 2a (pyr, tet)
+  static constexpr int REGIJ = DB1 + Dm::Q1 * Dm::NTRI;
+  static constexpr int SIZE = REGIJ + 4 * Dm::Q0 * Dm::Q1;
 };
 
 // Geometry payload addressing: [E/PW][C][NQ][PW], i.e. PW = EB elements

@@ -311,29 +311,54 @@ struct k_helm {
       const double l00 = __ldg(ge + 0 * PW), l01 = __ldg(ge + 1 * PW), l02 = __ldg(ge + 2 * PW),
                    l11 = __ldg(ge + 3 * PW), l12 = __ldg(ge + 4 * PW), l22 = __ldg(ge + 5 * PW),
                    jac = __ldg(ge + 6 * PW);
-      const double* rk = A.gtab + GLayout<S, P>::REGK + ps;
+      // G and the reference weights factor over the tensor directions: the
+      // (i, j) factors come from a small per-line table, the k factors are
+      // uniform parameter-space constants (no per-point loads)
+      constexpr int N2 = Q0 * Q1;
+      const double* rij = A.gtab + GLayout<S, P>::REGIJ + ps;
+      const double wij = __ldg(rij);
+      double c00 = 0.0, c20 = 0.0, c21 = 0.0;
+      if constexpr (S != HEX) {
+        c00 = __ldg(rij + 1 * N2);
+        c20 = __ldg(rij + 2 * N2);
+        if constexpr (S != PRISM) c21 = __ldg(rij + 3 * N2);
+      }
 #pragma unroll
       for (int k = 0; k < Q2; ++k) {
-        const double* rp = rk + k * (Q0 * Q1);
-        const double rw = __ldg(rp);
+        const double rw = wij * A.D.w2k[k];
         const double v0 = sm[L::at(e, V0O + row + k)], v1 = sm[L::at(e, V1O + row + k)], v2 = w2[k];
         double t0 = v0, t1 = v1, t2 = v2;
         double g00 = 1.0, g10 = 0.0, g11 = 1.0, g20 = 0.0, g21 = 0.0;
         if constexpr (S != HEX) {
-          g00 = __ldg(rp + 1 * NQ);
-          g10 = __ldg(rp + 2 * NQ);
-          g11 = __ldg(rp + 3 * NQ);
-          g20 = __ldg(rp + 4 * NQ);
-          g21 = __ldg(rp + 5 * NQ);
-          t0 = g00 * v0;
-          t1 = fma(g11, v1, g10 * v0);
-          t2 = fma(g21, v1, fma(g20, v0, v2));
+          const double a = A.D.ak[k];
+          g00 = a * c00;
+          g20 = a * c20;
+          if constexpr (S == PRISM) {
+            t0 = g00 * v0;
+            t2 = fma(g20, v0, v2);
+          } else {
+            g11 = 2.0 * a;
+            g21 = a * c21;
+            if constexpr (S == TET) {
+              g10 = g20;
+              t1 = fma(g11, v1, g10 * v0);
+            } else {
+              t1 = g11 * v1;
+            }
+            t0 = g00 * v0;
+            t2 = fma(g21, v1, fma(g20, v0, v2));
+          }
         }
         const double s0 = rw * fma(l02, t2, fma(l01, t1, l00 * t0));
         const double s1 = rw * fma(l12, t2, fma(l11, t1, l01 * t0));
         const double s2 = rw * fma(l22, t2, fma(l12, t1, l02 * t0));
         double a0 = s0, a1 = s1;
-        if constexpr (S != HEX) {
+        if constexpr (S == PRISM) {
+          a0 = fma(g20, s2, g00 * s0);
+        } else if constexpr (S == PYR) {
+          a0 = fma(g20, s2, g00 * s0);
+          a1 = fma(g21, s2, g11 * s1);
+        } else if constexpr (S == TET) {
           a0 = fma(g20, s2, fma(g10, s1, g00 * s0));
           a1 = fma(g21, s2, g11 * s1);
         }

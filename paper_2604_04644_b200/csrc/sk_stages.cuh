@@ -373,10 +373,11 @@ __device__ __forceinline__ void stage_f1(const FwdTab<S, P>& B, const double* __
         }
       }
     });
-  } else if constexpr ((S == PYR || S == TET) && RD) {
-    // pyr / tet: item = (e, (p,q) pair), pairs ordered by slice; the slice
-    // m = max(p,q) (pyr) or p+q (tet) is dispatched to a compile-time
-    // constant so c2[m] entries are uniform operands (operators.py:209-351)
+  } else if constexpr (S != HEX && RD) {
+    // prism / pyr / tet: item = (e, (p,q) pair), pairs ordered by slice; the
+    // slice m = p (prism), max(p,q) (pyr) or p+q (tet) is dispatched to a
+    // compile-time constant so c2[m] entries are uniform operands
+    // (operators.py:209-351)
     // SPLIT = 2 when the pairs fill at most half the CTA: each (e, pair)
     // line is computed by two threads (halves of k, half index slowest so a
     // warp takes one half), so no warp idles through the stage
@@ -398,10 +399,12 @@ __device__ __forceinline__ void stage_f1(const FwdTab<S, P>& B, const double* __
             double s = B.c2[co + k * n] * x[0];
 #pragma unroll
             for (int r = 1; r < n; ++r) s = fma(B.c2[co + k * n + r], x[r], s);
+            // prism collapsed-edge share of mode (0, q, 1) (operators.py:288-293)
+            if constexpr (S == PRISM && m == 1) s = fma(xin(e, pr.y * P1 + 1), B.c2[k * P1 + 1], s);
             sm[L::at(e, TAo + (pr.x * P1 + pr.y) * S2 + k)] = s;
           }
         }
-        if constexpr (m == 0) {
+        if constexpr (S != PRISM && m == 0) {
           if (pr.x == 0 && pr.y == 0) {
             // collapsed apex mode (0,0,1): Y[k] = c2[0][k][1] * uhat[0,0,1]
 #pragma unroll
@@ -738,9 +741,10 @@ __device__ __forceinline__ void stage_b3(const FwdTab<S, P>& B, const double* __
         }
       }
     });
-  } else if constexpr ((S == PYR || S == TET) && RD) {
-    // pyr / tet with the slice dispatched to a compile-time constant; outputs
-    // split over two threads (r parity) when the pairs fill half the CTA
+  } else if constexpr (S != HEX && RD) {
+    // prism / pyr / tet with the slice dispatched to a compile-time constant;
+    // outputs split over two threads (r parity) when the pairs fill half the
+    // CTA
     constexpr int SPLIT = SPL && 2 * L::EB * Dm::NPAIR <= NT ? 2 : 1;
     const int4* pairs = reinterpret_cast<const int4*>(gtab + GLayout<S, P>::PAIRS);
     items<L, Dm::NPAIR * SPLIT, NT>([&](int e, int ps2) {
@@ -760,7 +764,13 @@ __device__ __forceinline__ void stage_b3(const FwdTab<S, P>& B, const double* __
         constexpr int n = P1 - m;
         constexpr int co = wfam_off(Q2, P1, m);
         double apex = 0.0;
-        if constexpr (m == 0) {
+        if constexpr (S == PRISM && m == 0) {
+          if (SPLIT == 1 || h == 1) {
+            // modes (0,q,1) += sum_k c2[0][k][1] TA[1][q][k] (operators.py:312-317)
+#pragma unroll
+            for (int k = 0; k < Q2; ++k) apex = fma(B.c2[k * P1 + 1], sm[L::at(e, TAo + (1 * P1 + pr.y) * S2 + k)], apex);
+          }
+        } else if constexpr (m == 0) {
           if (pr.x == 0 && pr.y == 0 && (SPLIT == 1 || h == 1)) {
 #pragma unroll
             for (int k = 0; k < Q2; ++k) {

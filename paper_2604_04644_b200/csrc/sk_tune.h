@@ -106,14 +106,15 @@ constexpr int kPersist[4][11] = {
     {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},  // tet
 };
 
-// pyr/tet ragged r <-> k sweeps: compile-time slice dispatch up to this
-// order (uniform table operands), L1 table reads above it (code size).
-// Prism: up to this order one item per (element, p, q) pair with L1 tables
-// instead of one per (element, q) with all p unrolled (balances the stage
-// across the CTA; the unrolled form idles most threads)
+// prism/pyr/tet ragged r <-> k sweeps: one item per (element, p, q) pair
+// with the slice dispatched to compile-time constants up to this order
+// (uniform table operands), L1 table reads above it (code size).  Prism
+// without dispatch: one item per (element, q), all p unrolled, up to
+// kPrismUniformMaxP.  Dispatch measured slower for Helmholtz at P >= 7 on
+// every shape and for prism at every order but 7 (+5 %) (c3_tune_helm)
 constexpr int kRaggedMaxP[3][4] = {
     {0, 0, 6, 5},  // Helmholtz / stiffness
-    {0, 0, 8, 8},  // mass
+    {0, 0, 9, 8},  // mass (pyr P=9: +12 %, c3_tune_mass)
     {0, 0, 8, 8},  // transforms
 };
 

@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--shapes", default="hex,prism,pyr,tet")
     ap.add_argument("--gbytes", default="1.0")
     ap.add_argument("--reps", default="8")
+    ap.add_argument("--geo", default="deformed")
     a = ap.parse_args()
     best = {}
     for v in a.variants.split(","):
@@ -32,7 +33,7 @@ def main():
         nt_, mb_ = kv.get("nt", 0), kv.get("mb", -1)
         env = dict(os.environ, SK200_LIB=lib)
         cmd = [sys.executable, os.path.join(ROOT, "tools", "sweep.py"), "--ops", a.ops, "--orders", a.orders, "--shapes", a.shapes,
-               "--gbytes", a.gbytes, "--reps", a.reps]
+               "--gbytes", a.gbytes, "--reps", a.reps, "--geo", a.geo]
         out = subprocess.run(cmd, env=env, capture_output=True, text=True)
         if out.returncode:
             print(json.dumps({"variant": v, "error": out.stderr[-2000:]}), flush=True)
