@@ -240,7 +240,7 @@ struct k_helm {
   double* dst = A.out + blockIdx.y * A.out_cstride;
   double* xs = sm + L::EB * PL;  // plane 1: coefficient tile staging
 
-  stage_f1<S, P, L, NT, TAo, CoefIn<L, NM>, false, ragged_dispatch(0, S, P), ragged_split(0, S, P)>(A.B, A.gtab, CoefIn<L, NM>{xs}, sm);
+  stage_f1<S, P, L, NT, TAo, CoefIn<L, NM>, false, ragged_dispatch(0, S, P), ragged_split(0, S, P), prism_warp_pairs(0, S, P)>(A.B, A.gtab, CoefIn<L, NM>{xs}, sm);
   __syncthreads();
   stage_f2<S, P, L, NT, TAo, TBo>(A.B, A.gtab, sm);
   __syncthreads();
@@ -409,7 +409,7 @@ struct k_helm {
   __syncthreads();
   stage_b2<S, P, L, NT, TAo, TBo>(A.B, A.gtab, sm);
   __syncthreads();
-  stage_b3<S, P, L, NT, TAo, CoefOut<L, NM>, false, ragged_dispatch(0, S, P), ragged_split(0, S, P)>(A.B, A.gtab, CoefOut<L, NM>{xs}, sm);
+  stage_b3<S, P, L, NT, TAo, CoefOut<L, NM>, false, ragged_dispatch(0, S, P), ragged_split(0, S, P), prism_warp_pairs(0, S, P)>(A.B, A.gtab, CoefOut<L, NM>{xs}, sm);
   __syncthreads();
   store_tile<L, NM, NT>(dst, c, xs);
   }
@@ -467,7 +467,7 @@ struct k_mass {
   const double* src = A.in + blockIdx.y * A.in_cstride;
   double* dst = A.out + blockIdx.y * A.out_cstride;
   double* xs = sm + L::EB * PL;  // plane 1 (TB): staging before F2 and after B2
-  stage_f1<S, P, L, NT, TAo, CoefIn<L, NM>, false, ragged_dispatch(1, S, P), ragged_split(1, S, P)>(A.B, A.gtab, CoefIn<L, NM>{xs}, sm);
+  stage_f1<S, P, L, NT, TAo, CoefIn<L, NM>, false, ragged_dispatch(1, S, P), ragged_split(1, S, P), prism_warp_pairs(1, S, P)>(A.B, A.gtab, CoefIn<L, NM>{xs}, sm);
   __syncthreads();
   stage_f2<S, P, L, NT, TAo, TBo>(A.B, A.gtab, sm);
   __syncthreads();
@@ -489,7 +489,7 @@ struct k_mass {
   if (tnext >= 0 && threadIdx.x < 32) prefetch_geo(A, tnext);
   stage_b2<S, P, L, NT, TAo, TBo>(A.B, A.gtab, sm);
   __syncthreads();
-  stage_b3<S, P, L, NT, TAo, CoefOut<L, NM>, false, ragged_dispatch(1, S, P), ragged_split(1, S, P)>(A.B, A.gtab, CoefOut<L, NM>{xs}, sm);
+  stage_b3<S, P, L, NT, TAo, CoefOut<L, NM>, false, ragged_dispatch(1, S, P), ragged_split(1, S, P), prism_warp_pairs(1, S, P)>(A.B, A.gtab, CoefOut<L, NM>{xs}, sm);
   __syncthreads();
   store_tile<L, NM, NT>(dst, c, xs);
   }
@@ -526,7 +526,7 @@ struct k_bwd {
   double* xs = sm + L::EB * PL;
   load_tile<L, NM, NT>(src, c, xs);
   __syncthreads();
-  stage_f1<S, P, L, NT, TAo, CoefIn<L, NM>, false, ragged_dispatch(2, S, P), ragged_split(2, S, P)>(A.B, A.gtab, CoefIn<L, NM>{xs}, sm);
+  stage_f1<S, P, L, NT, TAo, CoefIn<L, NM>, false, ragged_dispatch(2, S, P), ragged_split(2, S, P), prism_warp_pairs(2, S, P)>(A.B, A.gtab, CoefIn<L, NM>{xs}, sm);
   __syncthreads();
   stage_f2<S, P, L, NT, TAo, TBo>(A.B, A.gtab, sm);
   __syncthreads();
@@ -593,7 +593,7 @@ struct k_iprod {
   __syncthreads();
   stage_b2<S, P, L, NT, TAo, TBo>(A.B, A.gtab, sm);
   __syncthreads();
-  stage_b3<S, P, L, NT, TAo, CoefOut<L, NM>, false, ragged_dispatch(2, S, P), ragged_split(2, S, P)>(A.B, A.gtab, CoefOut<L, NM>{xs}, sm);
+  stage_b3<S, P, L, NT, TAo, CoefOut<L, NM>, false, ragged_dispatch(2, S, P), ragged_split(2, S, P), prism_warp_pairs(2, S, P)>(A.B, A.gtab, CoefOut<L, NM>{xs}, sm);
   __syncthreads();
   store_tile<L, NM, NT>(dst, c, xs);
   }
@@ -777,7 +777,7 @@ struct k_ipderiv {
   __syncthreads();
   stage_b2<S, P, L, NT, TAo, TBo>(A.B, A.gtab, sm);
   __syncthreads();
-  stage_b3<S, P, L, NT, TAo, CoefOut<L, NM>, false, ragged_dispatch(2, S, P), ragged_split(2, S, P)>(A.B, A.gtab, CoefOut<L, NM>{xs}, sm);
+  stage_b3<S, P, L, NT, TAo, CoefOut<L, NM>, false, ragged_dispatch(2, S, P), ragged_split(2, S, P), prism_warp_pairs(2, S, P)>(A.B, A.gtab, CoefOut<L, NM>{xs}, sm);
   __syncthreads();
   store_tile<L, NM, NT>(A.out, c, xs);
   }

@@ -35,6 +35,30 @@ constexpr int kTetDispatchMaxP = SK_TET_DISPATCH_MAXP;
 constexpr int kTetDispatchMaxP = 9;
 #endif
 constexpr int kPrismUniformMaxP = 8;
+
+// Prism r <-> k sweeps with warp-uniform slices: the slices p and P - p
+// (n = P1 - p and p + 1 columns, P1 + 1 together) go to one group of whole
+// warps whose lanes take the (element, q) lines, so every warp runs one
+// branch of the slice dispatch (no divergence, uniform table operands) and
+// the groups carry equal work.  f(pc, e, q) is called with the slice as a
+// compile-time constant.
+template <int P, class L, int NT, class F>
+__device__ __forceinline__ void prism_slice_pairs(F&& f) {
+  constexpr int P1 = P + 1, NPP = (P1 + 1) / 2, LN = L::EB * P1, WPG = (LN + 31) / 32;
+  for (int sl = threadIdx.x; sl < NPP * WPG * 32; sl += NT) {
+    const int g = sl / (WPG * 32), l = sl - g * (WPG * 32);
+    if (l < LN) {
+      const int q = l / L::EB, e = l - q * L::EB;
+      dispatch<0, NPP>(g, [&](auto gc) {
+        constexpr int pa = decltype(gc)::value, pb = P1 - 1 - pa;
+        f(std::integral_constant<int, pa>{}, e, q);
+        if constexpr (pb != pa) f(std::integral_constant<int, pb>{}, e, q);
+      });
+    }
+  }
+}
+// mode offset of the prism slice p: sum_{p' < p} P1 (P1 - p')
+__host__ __device__ constexpr int prism_slice_off(int P1, int p) { return P1 * (p * P1 - p * (p - 1) / 2); }
 // pyr/tet r <-> k sweeps (slice c2[max(p,q)] / c2[p+q] varies per item):
 // compile-time slice dispatch (RD = true) or L1 table reads; chosen per
 // operator class (sk_tune.h kRaggedMaxP)
@@ -348,7 +372,8 @@ __device__ __forceinline__ void line_a0t_eo(const FwdTab<S, P>& B, const double 
 // DER2: the dir-2 family is the derivative one (reference dmode == 2; the
 // caller passes the derivative FwdTab for hex/prism, the device buffer's DC2
 // slices are used for pyr/tet)
-template <int S, int P, class L, int NT, int TAo, class In, bool DER2 = false, bool RD = false, bool SPL = false>
+template <int S, int P, class L, int NT, int TAo, class In, bool DER2 = false, bool RD = false, bool SPL = false,
+          bool WP = false>
 __device__ __forceinline__ void stage_f1(const FwdTab<S, P>& B, const double* __restrict__ gtab, const In& xin,
                                          double* sm) {
   using Dm = Dims<S, P>;
@@ -413,6 +438,24 @@ __device__ __forceinline__ void stage_f1(const FwdTab<S, P>& B, const double* __
           }
         }
       });
+    });
+  } else if constexpr (S == PRISM && WP) {
+    prism_slice_pairs<P, L, NT>([&](auto pc, int e, int q) {
+      constexpr int p = decltype(pc)::value, n = P1 - p, co = wfam_off(Q2, P1, p);
+      constexpr int off = prism_slice_off(P1, p);
+      double x[n];
+#pragma unroll
+      for (int r = 0; r < n; ++r) x[r] = xin(e, off + q * n + r);
+      double u0q1 = 0.0;
+      if constexpr (p == 1) u0q1 = xin(e, q * P1 + 1);  // mode (0, q, 1): collapsed-edge share
+#pragma unroll
+      for (int k = 0; k < Q2; ++k) {
+        double s = B.c2[co + k * n] * x[0];
+#pragma unroll
+        for (int r = 1; r < n; ++r) s = fma(B.c2[co + k * n + r], x[r], s);
+        if constexpr (p == 1) s = fma(u0q1, B.c2[k * P1 + 1], s);
+        sm[L::at(e, TAo + (p * P1 + q) * S2 + k)] = s;
+      }
     });
   } else if constexpr (S == PRISM && P <= kPrismUniformMaxP && !RD) {
     // item = (e, q[, p parity]); p unrolled so c2[p] is uniform
@@ -716,7 +759,8 @@ __device__ __forceinline__ void stage_b2(const FwdTab<S, P>& B, const double* __
 // ---- B3: k -> r, produce coefficients ----------------------------------------
 // DER2: derivative dir-2 family (transposed dmode == 2); accumulation into
 // the output is the Out functor's business
-template <int S, int P, class L, int NT, int TAo, class Out, bool DER2 = false, bool RD = false, bool SPL = false>
+template <int S, int P, class L, int NT, int TAo, class Out, bool DER2 = false, bool RD = false, bool SPL = false,
+          bool WP = false>
 __device__ __forceinline__ void stage_b3(const FwdTab<S, P>& B, const double* __restrict__ gtab, const Out& out,
                                          const double* sm) {
   using Dm = Dims<S, P>;
@@ -790,6 +834,28 @@ __device__ __forceinline__ void stage_b3(const FwdTab<S, P>& B, const double* __
           }
         }
       });
+    });
+  } else if constexpr (S == PRISM && WP) {
+    prism_slice_pairs<P, L, NT>([&](auto pc, int e, int q) {
+      constexpr int p = decltype(pc)::value, n = P1 - p, co = wfam_off(Q2, P1, p);
+      constexpr int off = prism_slice_off(P1, p);
+      double x[Q2];
+#pragma unroll
+      for (int k = 0; k < Q2; ++k) x[k] = sm[L::at(e, TAo + (p * P1 + q) * S2 + k)];
+      double corr = 0.0;
+      if constexpr (p == 0) {
+        // modes (0,q,1) += sum_k c2[0][k][1] TA[1][q][k] (operators.py:312-317)
+#pragma unroll
+        for (int k = 0; k < Q2; ++k) corr = fma(B.c2[k * P1 + 1], sm[L::at(e, TAo + (1 * P1 + q) * S2 + k)], corr);
+      }
+#pragma unroll
+      for (int r = 0; r < n; ++r) {
+        double s = B.c2[co + r] * x[0];
+#pragma unroll
+        for (int k = 1; k < Q2; ++k) s = fma(B.c2[co + k * n + r], x[k], s);
+        if (p == 0 && r == 1) s += corr;
+        out(e, off + q * n + r, s);
+      }
     });
   } else if constexpr (S == PRISM && P <= kPrismUniformMaxP && !RD) {
     constexpr int SPLIT = SPL && 2 * L::EB * P1 <= NT ? 2 : 1;  // see stage_f1

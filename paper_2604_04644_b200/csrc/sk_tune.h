@@ -129,6 +129,16 @@ constexpr int kSplitMinP[3][4] = {
     {99, 99, 99, 99},  // transforms
 };
 
+// prism r <-> k sweeps with warp-uniform slice pairs (sk_stages.cuh
+// prism_slice_pairs) at these orders, per operator class: measured +3-4 %
+// Helmholtz/stiffness P=6/7, mass +9/+6/+4 % P=6/7/9, slower at P=8/10
+// (c5_tune_wp_*.jsonl)
+constexpr bool kPrismWP[3][11] = {
+    {0, 0, 0, 0, 0, 0, 1, 1, 0, 0, 0},
+    {0, 0, 0, 0, 0, 0, 1, 1, 0, 1, 0},
+    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},
+};
+
 // Overrides for tuning builds (-DSK_EB_FIXED=... etc.) apply to every class.
 #ifdef SK_EB_FIXED
 SK_HD constexpr int tuned_eb(int, int, int) { return SK_EB_FIXED; }
@@ -165,6 +175,12 @@ SK_HD constexpr bool ragged_dispatch(int cls, int S, int P) { return P <= kRagge
 SK_HD constexpr bool ragged_split(int, int, int P) { return P >= SK_SPLIT_MINP; }
 #else
 SK_HD constexpr bool ragged_split(int cls, int S, int P) { return P >= kSplitMinP[cls][S]; }
+#endif
+
+#ifdef SK_PRISM_WP
+SK_HD constexpr bool prism_warp_pairs(int, int S, int P) { return S == 1 && P >= SK_PRISM_WP; }
+#else
+SK_HD constexpr bool prism_warp_pairs(int cls, int S, int P) { return S == 1 && kPrismWP[cls][P]; }
 #endif
 
 }  // namespace sk
