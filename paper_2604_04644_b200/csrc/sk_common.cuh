@@ -77,6 +77,8 @@ struct Lay {
   // in the planes that are dead while it is live (plane 1 on, >= 2 planes)
   static constexpr int XSTR = EB >= 8 ? EB + 1 : EB;
   static constexpr int SMEM_DOUBLES = NPL * PLANE * EB;
+  // staged ragged-sweep tables after the planes (int4 pairs: 16-byte aligned)
+  static constexpr int TABOFF = (SMEM_DOUBLES + 1) / 2 * 2;
   static_assert(Dm::NM * XSTR <= (NPL - 1) * PLANE * EB, "coefficient staging does not fit");
   __device__ static __forceinline__ int at(int e, int idx) { return idx * EB + e; }
 };
@@ -152,10 +154,12 @@ struct DTab {
 template <int S, int P>
 struct GLayout {
   using Dm = Dims<S, P>;
+  // C2 and PAIRS lead: [0, DC2) is what the ragged r <-> k sweeps of the
+  // value operators read (copied to shared memory where kSmemTab says so)
   static constexpr int C2 = 0;                           // dir-2 family values
-  static constexpr int DC2 = C2 + Dm::Q2 * Dm::NTRI;     // dir-2 family derivatives
-  static constexpr int PAIRS = DC2 + Dm::Q2 * Dm::NTRI;  // NPAIR x 4 ints
-  static constexpr int REGK = PAIRS + 2 * Dm::NPAIR;     // [6][k][i*Q1+j]: refw,g00,g10,g11,g20,g21
+  static constexpr int PAIRS = C2 + (Dm::Q2 * Dm::NTRI + 1) / 2 * 2;  // NPAIR x 4 ints (16-byte aligned)
+  static constexpr int DC2 = PAIRS + 2 * Dm::NPAIR;      // dir-2 family derivatives
+  static constexpr int REGK = DC2 + Dm::Q2 * Dm::NTRI;   // [6][k][i*Q1+j]: refw,g00,g10,g11,g20,g21
   static constexpr int REFW = REGK + 6 * Dm::NQ;         // [i][j][k] refw
   static constexpr int B1 = REFW + Dm::NQ;               // tet dir-1 family values
   static constexpr int DB1 = B1 + Dm::Q1 * Dm::NTRI;     // tet dir-1 family derivatives

@@ -193,6 +193,14 @@ __global__ void __launch_bounds__(Op::NT, Op::MINB) k_persist(const __grid_const
   }
 }
 
+// copy [0, GLayout::DC2) of the device table buffer (ragged sweep slices and
+// pairs) to shared memory (kSmemTab configurations); the caller's barrier
+// after the tile load publishes it
+template <int S, int P, int NT>
+__device__ __forceinline__ void stage_tables(const double* __restrict__ gtab, double* st) {
+  for (int t = threadIdx.x; t < GLayout<S, P>::DC2; t += NT) st[t] = __ldg(gtab + t);
+}
+
 // ---------------------------------------------------------------------------
 // Helmholtz, collocated: 9 sweeps + coefficient tile staging, 10 CTA barriers
 template <int S, int P, class L, int NT_, int PW, int GEO, bool LAMW, int MINB_, bool C0 = false>
@@ -213,8 +221,10 @@ struct k_helm {
     const long long n = A.Epad - e0 < EB ? A.Epad - e0 : EB;
     prefetch_field<Dims<S, P>::NM>(A.in, A.in_cstride, gridDim.y, e0, n, A.Epad, A.W);
   }
+  static constexpr bool SMT = smem_tables(0, S, P);
+  static_assert(!(SMT && tuned_persist(0, S, P)), "the persistent driver does not stage the tables");
   static constexpr bool PERSIST = !C0;  // the register-staged next tile assumes the field layout
-  static constexpr bool GEO_PF_AT_START = kGeoPrefetch == 1;
+  static constexpr bool GEO_PF_AT_START = geo_prefetch(S, P) == 1;
   using Pre = TileRegs<L, Dims<S, P>::NM, NT_>;
   __device__ static void pre_load(const OpArgs<S, P>& A, long long t, Pre& p) {
     p.load(A.in + blockIdx.y * A.in_cstride, make_ctx<L::EB>(t, A.E, A.Epad, A.W));
@@ -227,6 +237,7 @@ struct k_helm {
       load_tile_c0<L, P, NT>(A.in, c, A.c0_nx, A.c0_ny, sm + L::EB * L::PLANE);
     else
       load_tile<L, Dm::NM, NT>(A.in + blockIdx.y * A.in_cstride, c, sm + L::EB * L::PLANE);
+    if constexpr (SMT) stage_tables<S, P, NT>(A.gtab, sm + L::TABOFF);
     __syncthreads();
     body(A, tile, sm, -1);
   }
@@ -240,11 +251,12 @@ struct k_helm {
   double* dst = A.out + blockIdx.y * A.out_cstride;
   double* xs = sm + L::EB * PL;  // plane 1: coefficient tile staging
 
-  stage_f1<S, P, L, NT, TAo, CoefIn<L, NM>, false, ragged_dispatch(0, S, P), ragged_split(0, S, P), prism_warp_pairs(0, S, P)>(A.B, A.gtab, CoefIn<L, NM>{xs}, sm);
+  const double* rt = SMT ? sm + L::TABOFF : A.gtab;  // ragged sweep tables
+  stage_f1<S, P, L, NT, TAo, CoefIn<L, NM>, false, ragged_dispatch(0, S, P), ragged_split(0, S, P), prism_warp_pairs(0, S, P), SMT>(A.B, rt, CoefIn<L, NM>{xs}, sm);
   __syncthreads();
   stage_f2<S, P, L, NT, TAo, TBo>(A.B, A.gtab, sm);
   __syncthreads();
-  if (kGeoPrefetch == 2 && tnext < 0 && threadIdx.x < 32) prefetch_geo(A, tile);
+  if (geo_prefetch(S, P) == 2 && tnext < 0 && threadIdx.x < 32) prefetch_geo(A, tile);
   // F3 + D0: u along i, v0 = D0 u
   items<L, Q1 * Q2, NT>([&](int e, int ps) {
     const int j = ps / Q2, k = ps - j * Q2;
@@ -409,7 +421,7 @@ struct k_helm {
   __syncthreads();
   stage_b2<S, P, L, NT, TAo, TBo>(A.B, A.gtab, sm);
   __syncthreads();
-  stage_b3<S, P, L, NT, TAo, CoefOut<L, NM>, false, ragged_dispatch(0, S, P), ragged_split(0, S, P), prism_warp_pairs(0, S, P)>(A.B, A.gtab, CoefOut<L, NM>{xs}, sm);
+  stage_b3<S, P, L, NT, TAo, CoefOut<L, NM>, false, ragged_dispatch(0, S, P), ragged_split(0, S, P), prism_warp_pairs(0, S, P), SMT>(A.B, rt, CoefOut<L, NM>{xs}, sm);
   __syncthreads();
   store_tile<L, NM, NT>(dst, c, xs);
   }
@@ -456,18 +468,21 @@ struct k_mass {
     using Dm = Dims<S, P>;
     const Ctx c = make_ctx<L::EB>(tile, A.E, A.Epad, A.W);
     load_tile<L, Dm::NM, NT>(A.in + blockIdx.y * A.in_cstride, c, sm + L::EB * L::PLANE);
+    if constexpr (SMT) stage_tables<S, P, NT>(A.gtab, sm + L::TABOFF);
     __syncthreads();
     body(A, tile, sm, -1);
   }
+  static constexpr bool SMT = smem_tables(1, S, P);
   __device__ static void body(const OpArgs<S, P>& A, long long tile, double* sm, long long tnext) {
   using Dm = Dims<S, P>;
   constexpr int P1 = Dm::P1, Q0 = Dm::Q0, Q1 = Dm::Q1, Q2 = Dm::Q2, S2 = L::S2, NM = Dm::NM;
   constexpr int PL = L::PLANE, TAo = 0, TBo = PL;
+  const double* rt = SMT ? sm + L::TABOFF : A.gtab;  // ragged sweep tables
   const Ctx c = make_ctx<L::EB>(tile, A.E, A.Epad, A.W);
   const double* src = A.in + blockIdx.y * A.in_cstride;
   double* dst = A.out + blockIdx.y * A.out_cstride;
   double* xs = sm + L::EB * PL;  // plane 1 (TB): staging before F2 and after B2
-  stage_f1<S, P, L, NT, TAo, CoefIn<L, NM>, false, ragged_dispatch(1, S, P), ragged_split(1, S, P), prism_warp_pairs(1, S, P)>(A.B, A.gtab, CoefIn<L, NM>{xs}, sm);
+  stage_f1<S, P, L, NT, TAo, CoefIn<L, NM>, false, ragged_dispatch(1, S, P), ragged_split(1, S, P), prism_warp_pairs(1, S, P), SMT>(A.B, rt, CoefIn<L, NM>{xs}, sm);
   __syncthreads();
   stage_f2<S, P, L, NT, TAo, TBo>(A.B, A.gtab, sm);
   __syncthreads();
@@ -489,7 +504,7 @@ struct k_mass {
   if (tnext >= 0 && threadIdx.x < 32) prefetch_geo(A, tnext);
   stage_b2<S, P, L, NT, TAo, TBo>(A.B, A.gtab, sm);
   __syncthreads();
-  stage_b3<S, P, L, NT, TAo, CoefOut<L, NM>, false, ragged_dispatch(1, S, P), ragged_split(1, S, P), prism_warp_pairs(1, S, P)>(A.B, A.gtab, CoefOut<L, NM>{xs}, sm);
+  stage_b3<S, P, L, NT, TAo, CoefOut<L, NM>, false, ragged_dispatch(1, S, P), ragged_split(1, S, P), prism_warp_pairs(1, S, P), SMT>(A.B, rt, CoefOut<L, NM>{xs}, sm);
   __syncthreads();
   store_tile<L, NM, NT>(dst, c, xs);
   }

@@ -57,6 +57,20 @@ __device__ __forceinline__ void prism_slice_pairs(F&& f) {
     }
   }
 }
+// table reads of the ragged r <-> k sweeps: through L1 from the device
+// table buffer, or plain shared-memory loads when the caller staged [0, DC2)
+// of it in shared memory (SMT)
+template <bool SMT>
+__device__ __forceinline__ double ldt(const double* p) {
+  if constexpr (SMT) return *p;
+  else return __ldg(p);
+}
+template <bool SMT>
+__device__ __forceinline__ int4 ldt(const int4* p) {
+  if constexpr (SMT) return *p;
+  else return __ldg(p);
+}
+
 // mode offset of the prism slice p: sum_{p' < p} P1 (P1 - p')
 __host__ __device__ constexpr int prism_slice_off(int P1, int p) { return P1 * (p * P1 - p * (p - 1) / 2); }
 // pyr/tet r <-> k sweeps (slice c2[max(p,q)] / c2[p+q] varies per item):
@@ -373,7 +387,7 @@ __device__ __forceinline__ void line_a0t_eo(const FwdTab<S, P>& B, const double 
 // caller passes the derivative FwdTab for hex/prism, the device buffer's DC2
 // slices are used for pyr/tet)
 template <int S, int P, class L, int NT, int TAo, class In, bool DER2 = false, bool RD = false, bool SPL = false,
-          bool WP = false>
+          bool WP = false, bool SMT = false>
 __device__ __forceinline__ void stage_f1(const FwdTab<S, P>& B, const double* __restrict__ gtab, const In& xin,
                                          double* sm) {
   using Dm = Dims<S, P>;
@@ -410,7 +424,7 @@ __device__ __forceinline__ void stage_f1(const FwdTab<S, P>& B, const double* __
     const int4* pairs = reinterpret_cast<const int4*>(gtab + GLayout<S, P>::PAIRS);
     items<L, Dm::NPAIR * SPLIT, NT>([&](int e, int ps2) {
       const int h = ps2 / Dm::NPAIR, ps = ps2 - h * Dm::NPAIR;
-      const int4 pr = __ldg(pairs + ps);  // p, q, mode offset, nr
+      const int4 pr = ldt<SMT>(pairs + ps);  // p, q, mode offset, nr
       dispatch<0, P1>(P1 - pr.w, [&](auto mc) {
         constexpr int m = decltype(mc)::value;
         constexpr int n = P1 - m;
@@ -496,7 +510,7 @@ __device__ __forceinline__ void stage_f1(const FwdTab<S, P>& B, const double* __
     const int4* pairs = reinterpret_cast<const int4*>(gtab + GLayout<S, P>::PAIRS);
     items<L, Dm::NPAIR * SPLIT, NT>([&](int e, int ps2) {
       const int h = ps2 / Dm::NPAIR, ps = ps2 - h * Dm::NPAIR;
-      const int4 pr = __ldg(pairs + ps);  // p, q, mode offset, nr
+      const int4 pr = ldt<SMT>(pairs + ps);  // p, q, mode offset, nr
       const int m = (S == TET) ? pr.x + pr.y : (S == PRISM) ? pr.x : cmax(pr.x, pr.y);
       const int n = P1 - m;
       const double* fam = gtab + (DER2 ? GLayout<S, P>::DC2 : GLayout<S, P>::C2);
@@ -512,9 +526,9 @@ __device__ __forceinline__ void stage_f1(const FwdTab<S, P>& B, const double* __
           double s = 0.0;
 #pragma unroll
           for (int r = 0; r < P1; ++r)
-            if (r < pr.w) s = fma(__ldg(tab + k * n + r), x[r], s);
+            if (r < pr.w) s = fma(ldt<SMT>(tab + k * n + r), x[r], s);
           if constexpr (S == PRISM) {
-            if (pr.x == 1) s = fma(u0q1, __ldg(fam + k * P1 + 1), s);
+            if (pr.x == 1) s = fma(u0q1, ldt<SMT>(fam + k * P1 + 1), s);
           }
           sm[L::at(e, TAo + (pr.x * P1 + pr.y) * S2 + k)] = s;
         }
@@ -523,7 +537,7 @@ __device__ __forceinline__ void stage_f1(const FwdTab<S, P>& B, const double* __
         // collapsed apex mode (0,0,1): Y[k] = c2[0][k][1] * uhat[0,0,1]
 #pragma unroll
         for (int k = 0; k < Q2; ++k)
-          if (SPLIT == 1 || (k * SPLIT) / Q2 == h) sm[L::at(e, TAo + P1 * P1 * S2 + k)] = __ldg(fam + k * P1 + 1) * x[1];
+          if (SPLIT == 1 || (k * SPLIT) / Q2 == h) sm[L::at(e, TAo + P1 * P1 * S2 + k)] = ldt<SMT>(fam + k * P1 + 1) * x[1];
       }
     });
   }
@@ -760,7 +774,7 @@ __device__ __forceinline__ void stage_b2(const FwdTab<S, P>& B, const double* __
 // DER2: derivative dir-2 family (transposed dmode == 2); accumulation into
 // the output is the Out functor's business
 template <int S, int P, class L, int NT, int TAo, class Out, bool DER2 = false, bool RD = false, bool SPL = false,
-          bool WP = false>
+          bool WP = false, bool SMT = false>
 __device__ __forceinline__ void stage_b3(const FwdTab<S, P>& B, const double* __restrict__ gtab, const Out& out,
                                          const double* sm) {
   using Dm = Dims<S, P>;
@@ -793,7 +807,7 @@ __device__ __forceinline__ void stage_b3(const FwdTab<S, P>& B, const double* __
     const int4* pairs = reinterpret_cast<const int4*>(gtab + GLayout<S, P>::PAIRS);
     items<L, Dm::NPAIR * SPLIT, NT>([&](int e, int ps2) {
       const int h = ps2 / Dm::NPAIR, ps = ps2 - h * Dm::NPAIR;
-      const int4 pr = __ldg(pairs + ps);
+      const int4 pr = ldt<SMT>(pairs + ps);
       double x[Q2];
 #pragma unroll
       for (int k = 0; k < Q2; ++k) x[k] = sm[L::at(e, TAo + (pr.x * P1 + pr.y) * S2 + k)];
@@ -898,7 +912,7 @@ __device__ __forceinline__ void stage_b3(const FwdTab<S, P>& B, const double* __
     const int4* pairs = reinterpret_cast<const int4*>(gtab + GLayout<S, P>::PAIRS);
     items<L, Dm::NPAIR * SPLIT, NT>([&](int e, int ps2) {
       const int h = ps2 / Dm::NPAIR, ps = ps2 - h * Dm::NPAIR;
-      const int4 pr = __ldg(pairs + ps);
+      const int4 pr = ldt<SMT>(pairs + ps);
       const int m = (S == TET) ? pr.x + pr.y : (S == PRISM) ? pr.x : cmax(pr.x, pr.y);
       const int n = P1 - m;
       const double* fam = gtab + (DER2 ? GLayout<S, P>::DC2 : GLayout<S, P>::C2);
@@ -917,21 +931,21 @@ __device__ __forceinline__ void stage_b3(const FwdTab<S, P>& B, const double* __
 #pragma unroll
         for (int k = 0; k < Q2; ++k) {
           const double y = sm[L::at(e, TAo + P1 * P1 * S2 + k)] + sm[L::at(e, TAo + (0 * P1 + 1) * S2 + k)];
-          apex = fma(__ldg(fam + k * P1 + 1), y, apex);
+          apex = fma(ldt<SMT>(fam + k * P1 + 1), y, apex);
         }
       }
       if (S == PRISM && pr.x == 0 && (SPLIT == 1 || h == 1)) {
         // modes (0,q,1) += sum_k c2[0][k][1] TA[1][q][k] (operators.py:312-317)
 #pragma unroll
         for (int k = 0; k < Q2; ++k)
-          apex = fma(__ldg(fam + k * P1 + 1), sm[L::at(e, TAo + (1 * P1 + pr.y) * S2 + k)], apex);
+          apex = fma(ldt<SMT>(fam + k * P1 + 1), sm[L::at(e, TAo + (1 * P1 + pr.y) * S2 + k)], apex);
       }
 #pragma unroll
       for (int r = 0; r < P1; ++r) {
         if (r < pr.w && (SPLIT == 1 || r % SPLIT == h)) {
           double s = 0.0;
 #pragma unroll
-          for (int k = 0; k < Q2; ++k) s = fma(__ldg(tab + k * n + r), x[k], s);
+          for (int k = 0; k < Q2; ++k) s = fma(ldt<SMT>(tab + k * n + r), x[k], s);
           if (r == 1) s += apex;
           out(e, pr.z + r, s);
         }

@@ -82,10 +82,19 @@ constexpr int kMinBCap[3][4][11] = {
 
 // Helmholtz geometry L2 prefetch of a tile: 1 = at tile start (bulk TMA
 // prefetch, SASS UBLKPF), 2 = after the F2 sweep, 0 = none
+// per shape x order; after F2 measured +1-7 % at P=6 (every shape), P=10
+// (hex, prism, pyr) and tet P=9, for Helmholtz and stiffness alike
+// (profiles/r01c/tune_geo_prefetch_pf2.jsonl); at tile start elsewhere
+constexpr int kGeoPF[4][11] = {
+    {1, 1, 1, 1, 1, 1, 2, 1, 1, 1, 2},  // hex
+    {1, 1, 1, 1, 1, 1, 2, 1, 1, 1, 2},  // prism
+    {1, 1, 1, 1, 1, 1, 2, 1, 1, 1, 2},  // pyr
+    {1, 1, 1, 1, 1, 1, 2, 1, 1, 2, 1},  // tet
+};
 #ifdef SK_GEO_PF
-constexpr int kGeoPrefetch = SK_GEO_PF;
+SK_HD constexpr int geo_prefetch(int, int) { return SK_GEO_PF; }
 #else
-constexpr int kGeoPrefetch = 1;
+SK_HD constexpr int geo_prefetch(int S, int P) { return kGeoPF[S][P]; }
 #endif
 
 // points per geometry-load chunk in the Helmholtz metric sweep (lines longer
@@ -175,6 +184,22 @@ SK_HD constexpr bool ragged_dispatch(int cls, int S, int P) { return P <= kRagge
 SK_HD constexpr bool ragged_split(int, int, int P) { return P >= SK_SPLIT_MINP; }
 #else
 SK_HD constexpr bool ragged_split(int cls, int S, int P) { return P >= kSplitMinP[cls][S]; }
+#endif
+
+// ragged r <-> k sweep tables ([0, GLayout::DC2): C2 slices and pairs)
+// staged in shared memory per CTA instead of read through L1, per operator
+// class (0 Helmholtz, 1 mass) x shape x order.  Enabled where Helmholtz and
+// stiffness (or mass) both gained >= 2 % (profiles/r01c/tune_smem_tables_*):
+// the ragged paths are L1-latency bound at these orders, the extra shared
+// memory costs no CTA per SM there
+constexpr bool kSmemTab[2][4][11] = {
+    {{0}, {0}, {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1}, {0, 0, 0, 0, 0, 1, 0, 0, 0, 1, 0}},
+    {{0}, {0}, {0, 0, 0, 0, 1, 1, 0, 0, 0, 0, 0}, {0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 1}},
+};
+#ifdef SK_SMT
+SK_HD constexpr bool smem_tables(int cls, int S, int P) { return cls < 2 && S >= 2 && P >= SK_SMT && (cls == 1 || !kPersist[S][P]); }
+#else
+SK_HD constexpr bool smem_tables(int cls, int S, int P) { return cls < 2 && kSmemTab[cls][S][P]; }
 #endif
 
 #ifdef SK_PRISM_WP
