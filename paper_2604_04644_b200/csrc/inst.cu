@@ -56,7 +56,7 @@ struct Cfg {
   static constexpr int CLS = OP == OP_HELM ? 0 : OP == OP_MASS ? 1 : 2;
   static constexpr int NT0 = ((EB * items / tuned_nt_div(CLS, S, P) + 31) / 32) * 32;
   static constexpr int NT = NT0 > 512 ? 512 : (NT0 < 64 ? 64 : NT0);
-  static constexpr int SMEM = (smem_tables(CLS, S, P) ? L::TABOFF + GLayout<S, P>::DC2 : L::SMEM_DOUBLES) * 8;
+  static constexpr int SMEM = (smem_tables(CLS, S, P) ? L::TABOFF + GLayout<S, P>::RAGGED : L::SMEM_DOUBLES) * 8;
   // __launch_bounds__ min blocks: 1, or the CTAs per SM that shared memory
   // allows (forces ptxas to fit the registers; tuned, as it can spill)
   static constexpr int MINB = tuned_minb(CLS, S, P) ? cmax(1, cmin(cmin(tuned_minb_cap(CLS, S, P), (220 * 1024) / (SMEM + 1024)), 2048 / NT))

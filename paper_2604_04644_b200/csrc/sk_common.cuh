@@ -154,12 +154,13 @@ struct DTab {
 template <int S, int P>
 struct GLayout {
   using Dm = Dims<S, P>;
-  // C2 and PAIRS lead: [0, DC2) is what the ragged r <-> k sweeps of the
-  // value operators read (copied to shared memory where kSmemTab says so)
+  // [0, RAGGED) is what the ragged r <-> k sweeps read (copied to shared
+  // memory where kSmemTab says so)
   static constexpr int C2 = 0;                           // dir-2 family values
-  static constexpr int PAIRS = C2 + (Dm::Q2 * Dm::NTRI + 1) / 2 * 2;  // NPAIR x 4 ints (16-byte aligned)
-  static constexpr int DC2 = PAIRS + 2 * Dm::NPAIR;      // dir-2 family derivatives
-  static constexpr int REGK = DC2 + Dm::Q2 * Dm::NTRI;   // [6][k][i*Q1+j]: refw,g00,g10,g11,g20,g21
+  static constexpr int DC2 = C2 + Dm::Q2 * Dm::NTRI;     // dir-2 family derivatives
+  static constexpr int PAIRS = DC2 + Dm::Q2 * Dm::NTRI;  // NPAIR x 4 ints (16-byte aligned)
+  static constexpr int RAGGED = PAIRS + 2 * Dm::NPAIR;
+  static constexpr int REGK = PAIRS + 2 * Dm::NPAIR;     // [6][k][i*Q1+j]: refw,g00,g10,g11,g20,g21
   static constexpr int REFW = REGK + 6 * Dm::NQ;         // [i][j][k] refw
   static constexpr int B1 = REFW + Dm::NQ;               // tet dir-1 family values
   static constexpr int DB1 = B1 + Dm::Q1 * Dm::NTRI;     // tet dir-1 family derivatives

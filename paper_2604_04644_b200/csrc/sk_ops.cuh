@@ -193,12 +193,12 @@ __global__ void __launch_bounds__(Op::NT, Op::MINB) k_persist(const __grid_const
   }
 }
 
-// copy [0, GLayout::DC2) of the device table buffer (ragged sweep slices and
+// copy [0, GLayout::RAGGED) of the device table buffer (ragged sweep slices and
 // pairs) to shared memory (kSmemTab configurations); the caller's barrier
 // after the tile load publishes it
 template <int S, int P, int NT>
 __device__ __forceinline__ void stage_tables(const double* __restrict__ gtab, double* st) {
-  for (int t = threadIdx.x; t < GLayout<S, P>::DC2; t += NT) st[t] = __ldg(gtab + t);
+  for (int t = threadIdx.x; t < GLayout<S, P>::RAGGED; t += NT) st[t] = __ldg(gtab + t);
 }
 
 // ---------------------------------------------------------------------------
@@ -251,8 +251,10 @@ struct k_helm {
   double* dst = A.out + blockIdx.y * A.out_cstride;
   double* xs = sm + L::EB * PL;  // plane 1: coefficient tile staging
 
-  const double* rt = SMT ? sm + L::TABOFF : A.gtab;  // ragged sweep tables
-  stage_f1<S, P, L, NT, TAo, CoefIn<L, NM>, false, ragged_dispatch(0, S, P), ragged_split(0, S, P), prism_warp_pairs(0, S, P), SMT>(A.B, rt, CoefIn<L, NM>{xs}, sm);
+  if constexpr (SMT)  // ragged sweep tables staged in shared memory by run()
+    stage_f1<S, P, L, NT, TAo, CoefIn<L, NM>, false, ragged_dispatch(0, S, P), ragged_split(0, S, P), prism_warp_pairs(0, S, P), true>(A.B, sm + L::TABOFF, CoefIn<L, NM>{xs}, sm);
+  else
+    stage_f1<S, P, L, NT, TAo, CoefIn<L, NM>, false, ragged_dispatch(0, S, P), ragged_split(0, S, P), prism_warp_pairs(0, S, P)>(A.B, A.gtab, CoefIn<L, NM>{xs}, sm);
   __syncthreads();
   stage_f2<S, P, L, NT, TAo, TBo>(A.B, A.gtab, sm);
   __syncthreads();
@@ -421,7 +423,10 @@ struct k_helm {
   __syncthreads();
   stage_b2<S, P, L, NT, TAo, TBo>(A.B, A.gtab, sm);
   __syncthreads();
-  stage_b3<S, P, L, NT, TAo, CoefOut<L, NM>, false, ragged_dispatch(0, S, P), ragged_split(0, S, P), prism_warp_pairs(0, S, P), SMT>(A.B, rt, CoefOut<L, NM>{xs}, sm);
+  if constexpr (SMT)
+    stage_b3<S, P, L, NT, TAo, CoefOut<L, NM>, false, ragged_dispatch(0, S, P), ragged_split(0, S, P), prism_warp_pairs(0, S, P), true>(A.B, sm + L::TABOFF, CoefOut<L, NM>{xs}, sm);
+  else
+    stage_b3<S, P, L, NT, TAo, CoefOut<L, NM>, false, ragged_dispatch(0, S, P), ragged_split(0, S, P), prism_warp_pairs(0, S, P)>(A.B, A.gtab, CoefOut<L, NM>{xs}, sm);
   __syncthreads();
   store_tile<L, NM, NT>(dst, c, xs);
   }
@@ -477,12 +482,14 @@ struct k_mass {
   using Dm = Dims<S, P>;
   constexpr int P1 = Dm::P1, Q0 = Dm::Q0, Q1 = Dm::Q1, Q2 = Dm::Q2, S2 = L::S2, NM = Dm::NM;
   constexpr int PL = L::PLANE, TAo = 0, TBo = PL;
-  const double* rt = SMT ? sm + L::TABOFF : A.gtab;  // ragged sweep tables
   const Ctx c = make_ctx<L::EB>(tile, A.E, A.Epad, A.W);
   const double* src = A.in + blockIdx.y * A.in_cstride;
   double* dst = A.out + blockIdx.y * A.out_cstride;
   double* xs = sm + L::EB * PL;  // plane 1 (TB): staging before F2 and after B2
-  stage_f1<S, P, L, NT, TAo, CoefIn<L, NM>, false, ragged_dispatch(1, S, P), ragged_split(1, S, P), prism_warp_pairs(1, S, P), SMT>(A.B, rt, CoefIn<L, NM>{xs}, sm);
+  if constexpr (SMT)  // ragged sweep tables staged in shared memory by run()
+    stage_f1<S, P, L, NT, TAo, CoefIn<L, NM>, false, ragged_dispatch(1, S, P), ragged_split(1, S, P), prism_warp_pairs(1, S, P), true>(A.B, sm + L::TABOFF, CoefIn<L, NM>{xs}, sm);
+  else
+    stage_f1<S, P, L, NT, TAo, CoefIn<L, NM>, false, ragged_dispatch(1, S, P), ragged_split(1, S, P), prism_warp_pairs(1, S, P)>(A.B, A.gtab, CoefIn<L, NM>{xs}, sm);
   __syncthreads();
   stage_f2<S, P, L, NT, TAo, TBo>(A.B, A.gtab, sm);
   __syncthreads();
@@ -504,7 +511,10 @@ struct k_mass {
   if (tnext >= 0 && threadIdx.x < 32) prefetch_geo(A, tnext);
   stage_b2<S, P, L, NT, TAo, TBo>(A.B, A.gtab, sm);
   __syncthreads();
-  stage_b3<S, P, L, NT, TAo, CoefOut<L, NM>, false, ragged_dispatch(1, S, P), ragged_split(1, S, P), prism_warp_pairs(1, S, P), SMT>(A.B, rt, CoefOut<L, NM>{xs}, sm);
+  if constexpr (SMT)
+    stage_b3<S, P, L, NT, TAo, CoefOut<L, NM>, false, ragged_dispatch(1, S, P), ragged_split(1, S, P), prism_warp_pairs(1, S, P), true>(A.B, sm + L::TABOFF, CoefOut<L, NM>{xs}, sm);
+  else
+    stage_b3<S, P, L, NT, TAo, CoefOut<L, NM>, false, ragged_dispatch(1, S, P), ragged_split(1, S, P), prism_warp_pairs(1, S, P)>(A.B, A.gtab, CoefOut<L, NM>{xs}, sm);
   __syncthreads();
   store_tile<L, NM, NT>(dst, c, xs);
   }

@@ -58,7 +58,7 @@ __device__ __forceinline__ void prism_slice_pairs(F&& f) {
   }
 }
 // table reads of the ragged r <-> k sweeps: through L1 from the device
-// table buffer, or plain shared-memory loads when the caller staged [0, DC2)
+// table buffer, or plain shared-memory loads when the caller staged [0, RAGGED)
 // of it in shared memory (SMT)
 template <bool SMT>
 __device__ __forceinline__ double ldt(const double* p) {

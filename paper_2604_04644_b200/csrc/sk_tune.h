@@ -186,14 +186,15 @@ SK_HD constexpr bool ragged_split(int, int, int P) { return P >= SK_SPLIT_MINP; 
 SK_HD constexpr bool ragged_split(int cls, int S, int P) { return P >= kSplitMinP[cls][S]; }
 #endif
 
-// ragged r <-> k sweep tables ([0, GLayout::DC2): C2 slices and pairs)
+// ragged r <-> k sweep tables ([0, GLayout::RAGGED): slices and pairs)
 // staged in shared memory per CTA instead of read through L1, per operator
 // class (0 Helmholtz, 1 mass) x shape x order.  Enabled where Helmholtz and
-// stiffness (or mass) both gained >= 2 % (profiles/r01c/tune_smem_tables_*):
+// stiffness (or mass) both gained >= 2 % (profiles/r01c/tune_smem_tables_*,
+// Helmholtz re-checked in ab_vs_ebf7fee.jsonl):
 // the ragged paths are L1-latency bound at these orders, the extra shared
 // memory costs no CTA per SM there
 constexpr bool kSmemTab[2][4][11] = {
-    {{0}, {0}, {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1}, {0, 0, 0, 0, 0, 1, 0, 0, 0, 1, 0}},
+    {{0}, {0}, {0}, {0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 0}},
     {{0}, {0}, {0, 0, 0, 0, 1, 1, 0, 0, 0, 0, 0}, {0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 1}},
 };
 #ifdef SK_SMT
