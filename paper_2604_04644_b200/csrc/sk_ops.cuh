@@ -224,7 +224,7 @@ struct k_helm {
   static constexpr bool SMT = smem_tables(0, S, P);
   static_assert(!(SMT && tuned_persist(0, S, P)), "the persistent driver does not stage the tables");
   static constexpr bool PERSIST = !C0;  // the register-staged next tile assumes the field layout
-  static constexpr bool GEO_PF_AT_START = geo_prefetch(S, P) == 1;
+  static constexpr bool GEO_PF_AT_START = geo_prefetch(S, P) & 1;
   using Pre = TileRegs<L, Dims<S, P>::NM, NT_>;
   __device__ static void pre_load(const OpArgs<S, P>& A, long long t, Pre& p) {
     p.load(A.in + blockIdx.y * A.in_cstride, make_ctx<L::EB>(t, A.E, A.Epad, A.W));
@@ -258,7 +258,7 @@ struct k_helm {
   __syncthreads();
   stage_f2<S, P, L, NT, TAo, TBo>(A.B, A.gtab, sm);
   __syncthreads();
-  if (geo_prefetch(S, P) == 2 && tnext < 0 && threadIdx.x < 32) prefetch_geo(A, tile);
+  if ((geo_prefetch(S, P) & 2) && tnext < 0 && threadIdx.x < 32) prefetch_geo(A, tile);
   // F3 + D0: u along i, v0 = D0 u
   items<L, Q1 * Q2, NT>([&](int e, int ps) {
     const int j = ps / Q2, k = ps - j * Q2;

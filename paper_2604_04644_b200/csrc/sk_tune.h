@@ -81,7 +81,7 @@ constexpr int kMinBCap[3][4][11] = {
 };
 
 // Helmholtz geometry L2 prefetch of a tile: 1 = at tile start (bulk TMA
-// prefetch, SASS UBLKPF), 2 = after the F2 sweep, 0 = none
+// prefetch, SASS UBLKPF), 2 = after the F2 sweep, 3 = both, 0 = none
 // per shape x order; after F2 measured +1-7 % at P=6 (every shape), P=10
 // (hex, prism, pyr) and tet P=9, for Helmholtz and stiffness alike
 // (profiles/r01c/tune_geo_prefetch_pf2.jsonl); at tile start elsewhere
