@@ -57,6 +57,15 @@ __device__ __forceinline__ void prism_slice_pairs(F&& f) {
     }
   }
 }
+// L1-table ragged sweeps: loop over the item's own run length at run time
+// (1) instead of the full unrolled P1 with predicated-off tails (0); same
+// accumulation order, bit-identical results
+#ifdef SK_RRL
+constexpr bool kRaggedRuntimeLoop = SK_RRL;
+#else
+constexpr bool kRaggedRuntimeLoop = false;
+#endif
+
 // table reads of the ragged r <-> k sweeps: through L1 from the device
 // table buffer, or plain shared-memory loads when the caller staged [0, RAGGED)
 // of it in shared memory (SMT)
@@ -515,6 +524,36 @@ __device__ __forceinline__ void stage_f1(const FwdTab<S, P>& B, const double* __
       const int n = P1 - m;
       const double* fam = gtab + (DER2 ? GLayout<S, P>::DC2 : GLayout<S, P>::C2);
       const double* tab = fam + wfam_off(Q2, P1, m);
+      if constexpr (kRaggedRuntimeLoop) {
+        double acc[Q2];
+#pragma unroll
+        for (int k = 0; k < Q2; ++k) acc[k] = 0.0;
+#pragma unroll 1
+        for (int r = 0; r < pr.w; ++r) {
+          const double xr = xin(e, pr.z + r);
+#pragma unroll
+          for (int k = 0; k < Q2; ++k)
+            if (SPLIT == 1 || (k * SPLIT) / Q2 == h) acc[k] = fma(ldt<SMT>(tab + k * n + r), xr, acc[k]);
+        }
+        const double u0q1 = (S == PRISM && pr.x == 1) ? xin(e, pr.y * P1 + 1) : 0.0;
+#pragma unroll
+        for (int k = 0; k < Q2; ++k) {
+          if (SPLIT == 1 || (k * SPLIT) / Q2 == h) {
+            double v = acc[k];
+            if constexpr (S == PRISM) {
+              if (pr.x == 1) v = fma(u0q1, ldt<SMT>(fam + k * P1 + 1), v);
+            }
+            sm[L::at(e, TAo + (pr.x * P1 + pr.y) * S2 + k)] = v;
+          }
+        }
+        if (S != PRISM && pr.x == 0 && pr.y == 0) {
+          const double x1 = xin(e, pr.z + 1);
+#pragma unroll
+          for (int k = 0; k < Q2; ++k)
+            if (SPLIT == 1 || (k * SPLIT) / Q2 == h) sm[L::at(e, TAo + P1 * P1 * S2 + k)] = ldt<SMT>(fam + k * P1 + 1) * x1;
+        }
+        return;
+      }
       double x[P1];
 #pragma unroll
       for (int r = 0; r < P1; ++r) x[r] = r < pr.w ? xin(e, pr.z + r) : 0.0;
@@ -601,11 +640,33 @@ __device__ __forceinline__ void stage_f2(const FwdTab<S, P>& B, const double* __
         const int p = ps / Q2, k = ps - p * Q2;
         const int n = P1 - p;
         const double* tab = fam + wfam_off(Q1, P1, p);
+        const double y = p <= 1 ? sm[L::at(e, TAo + P1 * P1 * S2 + k)] : 0.0;
+        const double x01 = p == 1 ? sm[L::at(e, TAo + (0 * P1 + 1) * S2 + k)] : 0.0;
+        if constexpr (kRaggedRuntimeLoop) {
+          double acc[Q1];
+#pragma unroll
+          for (int j = 0; j < Q1; ++j) acc[j] = 0.0;
+#pragma unroll 1
+          for (int q = 0; q < n; ++q) {
+            const double xq = sm[L::at(e, TAo + (p * P1 + q) * S2 + k)];
+#pragma unroll
+            for (int j = 0; j < Q1; ++j) acc[j] = fma(__ldg(tab + j * n + q), xq, acc[j]);
+          }
+#pragma unroll
+          for (int j = 0; j < Q1; ++j) {
+            double s = acc[j];
+            if (p == 1) {
+              s = fma(B.b1[j * P1 + 1], x01, s);
+              if constexpr (!DER1) s += y;
+            }
+            if (p == 0) s = fma(B.b1[j * P1 + 1], y, s);
+            sm[L::at(e, TBo + (p * Q1 + j) * S2 + k)] = s;
+          }
+          return;
+        }
         double x[P1];
 #pragma unroll
         for (int q = 0; q < P1; ++q) x[q] = q < n ? sm[L::at(e, TAo + (p * P1 + q) * S2 + k)] : 0.0;
-        const double y = p <= 1 ? sm[L::at(e, TAo + P1 * P1 * S2 + k)] : 0.0;
-        const double x01 = p == 1 ? sm[L::at(e, TAo + (0 * P1 + 1) * S2 + k)] : 0.0;
 #pragma unroll
         for (int j = 0; j < Q1; ++j) {
           double s = 0.0;
@@ -711,14 +772,25 @@ __device__ __forceinline__ void stage_b2(const FwdTab<S, P>& B, const double* __
         double x[Q1];
 #pragma unroll
         for (int j = 0; j < Q1; ++j) x[j] = sm[L::at(e, TBo + (p * Q1 + j) * S2 + k)];
-#pragma unroll
-        for (int q = 0; q < P1; ++q) {
-          if (q < n) {
+        if constexpr (kRaggedRuntimeLoop) {
+#pragma unroll 1
+          for (int q = 0; q < n; ++q) {
             double s = 0.0;
 #pragma unroll
             for (int j = 0; j < Q1; ++j) s = fma(__ldg(tab + j * n + q), x[j], s);
             double& t = sm[L::at(e, TAo + (p * P1 + q) * S2 + k)];
             t = ACC ? t + s : s;
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < P1; ++q) {
+            if (q < n) {
+              double s = 0.0;
+#pragma unroll
+              for (int j = 0; j < Q1; ++j) s = fma(__ldg(tab + j * n + q), x[j], s);
+              double& t = sm[L::at(e, TAo + (p * P1 + q) * S2 + k)];
+              t = ACC ? t + s : s;
+            }
           }
         }
         if (p == 1) {
@@ -939,6 +1011,19 @@ __device__ __forceinline__ void stage_b3(const FwdTab<S, P>& B, const double* __
 #pragma unroll
         for (int k = 0; k < Q2; ++k)
           apex = fma(ldt<SMT>(fam + k * P1 + 1), sm[L::at(e, TAo + (1 * P1 + pr.y) * S2 + k)], apex);
+      }
+      if constexpr (kRaggedRuntimeLoop) {
+#pragma unroll 1
+        for (int r = 0; r < pr.w; ++r) {
+          if (SPLIT == 1 || r % SPLIT == h) {
+            double s = 0.0;
+#pragma unroll
+            for (int k = 0; k < Q2; ++k) s = fma(ldt<SMT>(tab + k * n + r), x[k], s);
+            if (r == 1) s += apex;
+            out(e, pr.z + r, s);
+          }
+        }
+        return;
       }
 #pragma unroll
       for (int r = 0; r < P1; ++r) {
