@@ -358,11 +358,10 @@ int sk_apply_streamed(const sk_basis* b, int op, int geo, int64_t E, int W, int 
   if (st) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream), sh = nullptr, sd = nullptr;
   if ((st = copy_streams(&sh, &sd))) return st;
-  // chunks start on a multiple of the interleave width, the tile width and
-  // the payload lane width (= tile width), so every chunk is a sub-block
-  int64_t cfg[3];
-  b->ops->config(kop, cfg);
-  const long long eb = cfg[0] > 0 ? cfg[0] : 1;
+  // chunks start on a multiple of the interleave width, the tile widths and
+  // the payload lane widths (all powers of two <= 16, kRegPW = 16), so every
+  // chunk is a sub-block
+  const long long eb = 16;
   const long long unit = (long long)W / gcd_ll(W, eb) * eb;
   if (chunk <= 0) chunk = (Epad + 15) / 16;
   if (chunk < 4096) chunk = 4096;

@@ -41,13 +41,16 @@ struct Mode {
   static constexpr int EBW = tuned_eb(1, S, P) > 0 ? fit(tuned_eb(1, S, P), 200 * 1024) : fit(16, 100 * 1024);
   // payload lane width of each payload kind = tile width of its consumers
   SK_HD static constexpr int pw(int kind) { return kind == 1 ? EBW : EBH; }
+  // regular-geometry collocated Helmholtz tile width (its payload lane
+  // width is kRegPW, independent of the tile)
+  static constexpr int EBHR = tuned_eb_regular(S, P) > 0 ? fit(tuned_eb_regular(S, P), 200 * 1024) : EBH;
   SK_HD static constexpr int eb(int op) { return (op == OP_HELM || op == OP_HELM_NC || op == OP_PDERIV) ? EBH : EBW; }
 };
 
-template <int S, int P, int OP>
+template <int S, int P, int OP, bool REG = false>
 struct Cfg {
   using Dm = Dims<S, P>;
-  static constexpr int EB = Mode<S, P>::eb(OP);
+  static constexpr int EB = REG ? Mode<S, P>::EBHR : Mode<S, P>::eb(OP);
   static constexpr int PW = EB;
   static constexpr int planes = OP == OP_HELM_NC ? 5 : (OP == OP_HELM || OP == OP_PDERIV || OP == OP_IPDERIV) ? 3 : 2;
   static constexpr int items = cmax(cmax(cmax(Dm::Q1 * Dm::Q2, Dm::Q0 * Dm::Q2), cmax(Dm::Q0 * Dm::Q1, Dm::P1 * Dm::P1)),
@@ -244,9 +247,8 @@ static void ensure_smem(K kernel, int bytes) {
   if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
 
-template <int S, int P, int OP, class Op, class Args>
+template <int S, int P, int OP, class Op, class C = Cfg<S, P, OP>, class Args>
 static int go(const Args& a, const LaunchReq& r, int gy, void* stream) {
-  using C = Cfg<S, P, OP>;
   static_assert(C::EB == C::PW, "tiles must align with payload lanes");
   constexpr bool persist = Op::PERSIST && tuned_persist(C::CLS, S, P);
   auto kern = [] {
@@ -347,8 +349,9 @@ int launch(int op, const LaunchReq& r, void* stream) {
         if (r.lam != 0.0) return go<S, P, OP_HELM, k_helm<S, P, typename C::L, C::NT, C::PW, GEO_DEFORMED, true, C::MINB>>(a, r, r.ncomp, stream);
         return go<S, P, OP_HELM, k_helm<S, P, typename C::L, C::NT, C::PW, GEO_DEFORMED, false, C::MINB>>(a, r, r.ncomp, stream);
       }
-      if (r.lam != 0.0) return go<S, P, OP_HELM, k_helm<S, P, typename C::L, C::NT, C::PW, GEO_REGULAR, true, C::MINB>>(a, r, r.ncomp, stream);
-      return go<S, P, OP_HELM, k_helm<S, P, typename C::L, C::NT, C::PW, GEO_REGULAR, false, C::MINB>>(a, r, r.ncomp, stream);
+      using CR = Cfg<S, P, OP_HELM, true>;  // regular geometry: own tile width
+      if (r.lam != 0.0) return go<S, P, OP_HELM, k_helm<S, P, typename CR::L, CR::NT, CR::PW, GEO_REGULAR, true, CR::MINB>, CR>(a, r, r.ncomp, stream);
+      return go<S, P, OP_HELM, k_helm<S, P, typename CR::L, CR::NT, CR::PW, GEO_REGULAR, false, CR::MINB>, CR>(a, r, r.ncomp, stream);
     }
 #endif
 #if !defined(SK_ONLY_OP) || SK_ONLY_OP == 1
@@ -415,7 +418,8 @@ long long payload_doubles(int kind, int geo) {
 
 template <int S, int P>
 long long payload_elements(int kind, long long E) {
-  const long long PW = Mode<S, P>::pw(kind);
+  // kind 0: room for either lane width (deformed PW, regular kRegPW; PW | 16)
+  const long long PW = kind == 0 ? kRegPW : Mode<S, P>::pw(kind);
   return (E + PW - 1) / PW * PW;
 }
 
@@ -496,15 +500,17 @@ __global__ void k_pack_regular(int kind, long long E, const double* __restrict__
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < E; e += (long long)gridDim.x * blockDim.x) {
     const double* d = dxi + e * 9;
     if (kind == 0 || kind == 3) {
-      double* o = pay + pay_base<PW>(e, 8, 1);
+      // kind 0 (collocated Helmholtz) uses the fixed regular lane width
+      const int W0 = kind == 0 ? kRegPW : PW;
+      double* o = pay + (kind == 0 ? pay_base<kRegPW>(e, 8, 1) : pay_base<PW>(e, 8, 1));
       const int mi[6] = {0, 0, 0, 1, 1, 2}, ni[6] = {0, 1, 2, 1, 2, 2};
       for (int c = 0; c < 6; ++c) {
         const int a = mi[c], b = ni[c];
         const double s = fma(d[a * 3 + 2], d[b * 3 + 2], fma(d[a * 3 + 1], d[b * 3 + 1], d[a * 3] * d[b * 3]));
-        o[c * PW] = s * jac[e];
+        o[c * W0] = s * jac[e];
       }
-      o[6 * PW] = jac[e];
-      o[7 * PW] = 0.0;
+      o[6 * W0] = jac[e];
+      o[7 * W0] = 0.0;
     } else if (kind == 1) {
       pay[pay_base<PWW>(e, 1, 1)] = jac[e];
     } else {

@@ -10,6 +10,9 @@
 namespace sk {
 
 enum : int { GEO_REGULAR = 0, GEO_DEFORMED = 1 };
+// lane width of the regular-geometry Helmholtz payload (8 doubles per
+// element): fixed, so the regular kernel's tile width is tuned on its own
+constexpr int kRegPW = 16;
 
 __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
 __host__ __device__ constexpr int cmin(int a, int b) { return a < b ? a : b; }

@@ -321,10 +321,11 @@ struct k_helm {
       }
     } else {
       // affine: Lam per element, G and reference weights per point
-      const double* ge = A.pay + pay_base<PW>(live ? eg : 0, 8, 1);
-      const double l00 = __ldg(ge + 0 * PW), l01 = __ldg(ge + 1 * PW), l02 = __ldg(ge + 2 * PW),
-                   l11 = __ldg(ge + 3 * PW), l12 = __ldg(ge + 4 * PW), l22 = __ldg(ge + 5 * PW),
-                   jac = __ldg(ge + 6 * PW);
+      constexpr int RW = kRegPW;
+      const double* ge = A.pay + pay_base<RW>(live ? eg : 0, 8, 1);
+      const double l00 = __ldg(ge + 0 * RW), l01 = __ldg(ge + 1 * RW), l02 = __ldg(ge + 2 * RW),
+                   l11 = __ldg(ge + 3 * RW), l12 = __ldg(ge + 4 * RW), l22 = __ldg(ge + 5 * RW),
+                   jac = __ldg(ge + 6 * RW);
       // G and the reference weights factor over the tensor directions: the
       // (i, j) factors come from a small per-line table, the k factors are
       // uniform parameter-space constants (no per-point loads)

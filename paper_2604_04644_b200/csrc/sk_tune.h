@@ -31,6 +31,17 @@ constexpr int kTunedEB[2][4][11] = {
      {0, 16, 16, 16, 16, 8, 8, 16, 16, 8, 8}},
 };
 
+// regular-geometry collocated Helmholtz / stiffness tile width (0 = the
+// deformed table's); its payload has a fixed lane width (kRegPW), so the
+// tile is tuned on its own (profiles/r01c/tune_regular_eb.jsonl)
+constexpr int kTunedEBReg[4][11] = {
+    // P: 0  1  2  3  4  5  6  7  8  9  10
+    {0, 0, 0, 0, 0, 0, 4, 4, 4, 0, 0},  // hex
+    {0, 0, 0, 8, 0, 16, 8, 8, 4, 0, 0},  // prism
+    {0, 0, 0, 0, 0, 0, 8, 0, 0, 0, 0},  // pyr
+    {0, 0, 0, 0, 0, 0, 8, 0, 0, 0, 0},  // tet
+};
+
 // threads per CTA = EB x (largest sweep item count) / divisor
 constexpr int kTunedNTDiv[3][4][11] = {
     {{1, 1, 1, 2, 1, 1, 1, 1, 1, 1, 1},
@@ -153,6 +164,11 @@ constexpr bool kPrismWP[3][11] = {
 SK_HD constexpr int tuned_eb(int, int, int) { return SK_EB_FIXED; }
 #else
 SK_HD constexpr int tuned_eb(int fam, int S, int P) { return kTunedEB[fam][S][P]; }
+#endif
+#ifdef SK_EB_FIXED
+SK_HD constexpr int tuned_eb_regular(int, int) { return SK_EB_FIXED; }
+#else
+SK_HD constexpr int tuned_eb_regular(int S, int P) { return kTunedEBReg[S][P]; }
 #endif
 #ifdef SK_NT_DIV
 SK_HD constexpr int tuned_nt_div(int, int, int) { return SK_NT_DIV; }
