@@ -33,12 +33,12 @@ constexpr int kTunedEB[2][4][11] = {
 
 // regular-geometry collocated Helmholtz / stiffness tile width (0 = the
 // deformed table's); its payload has a fixed lane width (kRegPW), so the
-// tile is tuned on its own (profiles/r01c/tune_regular_eb.jsonl)
+// tile is tuned on its own (profiles/r01c/tune_regular_eb*.jsonl)
 constexpr int kTunedEBReg[4][11] = {
     // P: 0  1  2  3  4  5  6  7  8  9  10
-    {0, 0, 0, 0, 0, 0, 4, 4, 4, 0, 0},  // hex
-    {0, 0, 0, 8, 0, 16, 8, 8, 4, 0, 0},  // prism
-    {0, 0, 0, 0, 0, 0, 8, 0, 0, 0, 0},  // pyr
+    {0, 0, 0, 0, 0, 0, 4, 4, 2, 0, 0},  // hex
+    {0, 0, 0, 8, 0, 16, 8, 1, 4, 0, 2},  // prism
+    {0, 0, 0, 0, 0, 0, 8, 0, 0, 0, 2},  // pyr
     {0, 0, 0, 0, 0, 0, 8, 0, 0, 0, 0},  // tet
 };
 
