@@ -57,7 +57,7 @@ struct Cfg {
                                     cmax(Dm::NPAIR, Dm::P1 * Dm::Q2));
   using L = Lay<S, P, planes, EB>;
   static constexpr int CLS = OP == OP_HELM ? 0 : OP == OP_MASS ? 1 : 2;
-  static constexpr int NT0 = ((EB * items / tuned_nt_div(CLS, S, P) + 31) / 32) * 32;
+  static constexpr int NT0 = ((EB * items / (REG ? tuned_nt_div_regular(S, P) : tuned_nt_div(CLS, S, P)) + 31) / 32) * 32;
   static constexpr int NT = NT0 > 512 ? 512 : (NT0 < 64 ? 64 : NT0);
   static constexpr int SMEM = (smem_tables(CLS, S, P) ? L::TABOFF + GLayout<S, P>::RAGGED : L::SMEM_DOUBLES) * 8;
   // __launch_bounds__ min blocks: 1, or the CTAs per SM that shared memory

@@ -42,6 +42,16 @@ constexpr int kTunedEBReg[4][11] = {
     {0, 0, 0, 0, 0, 0, 8, 0, 0, 0, 0},  // tet
 };
 
+// regular-geometry thread divisor (0 = the class table's): two items per
+// thread measured +9-17 % at hex P=1, prism P=3/4, tet P=3
+// (profiles/r01c/tune_regular_nt.jsonl)
+constexpr int kTunedNTDivReg[4][11] = {
+    {0, 2, 0, 0, 0, 0, 0, 0, 0, 0, 0},  // hex
+    {0, 0, 0, 2, 2, 0, 0, 0, 0, 0, 0},  // prism
+    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},  // pyr
+    {0, 0, 0, 2, 0, 0, 0, 0, 0, 0, 0},  // tet
+};
+
 // threads per CTA = EB x (largest sweep item count) / divisor
 constexpr int kTunedNTDiv[3][4][11] = {
     {{1, 1, 1, 2, 1, 1, 1, 1, 1, 1, 1},
@@ -174,6 +184,11 @@ SK_HD constexpr int tuned_eb_regular(int S, int P) { return kTunedEBReg[S][P]; }
 SK_HD constexpr int tuned_nt_div(int, int, int) { return SK_NT_DIV; }
 #else
 SK_HD constexpr int tuned_nt_div(int cls, int S, int P) { return kTunedNTDiv[cls][S][P]; }
+#endif
+#ifdef SK_NT_DIV
+SK_HD constexpr int tuned_nt_div_regular(int, int) { return SK_NT_DIV; }
+#else
+SK_HD constexpr int tuned_nt_div_regular(int S, int P) { return kTunedNTDivReg[S][P] > 0 ? kTunedNTDivReg[S][P] : kTunedNTDiv[0][S][P]; }
 #endif
 #ifdef SK_MINB
 SK_HD constexpr int tuned_minb(int, int, int) { return SK_MINB; }
