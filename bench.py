@@ -1,17 +1,30 @@
-"""Benchmark: Helmholtz apply throughput (GDOF/s) on B200, BASELINE config 2.
+"""Benchmark: Helmholtz apply throughput (GDOF/s) on B200.
 
-Workload (BASELINE.json configs[1]): Helmholtz operator (collocated, lam=1)
-on a synthetic deformed tetrahedral mesh, P=4, 2^20 elements per GPU, FP64,
-inputs resident in HBM (8.96 GB of geometry per apply >> 126 MB L2, so no
-flush is needed between steps).  One process per GPU; every rank owns a
+Default workload (BASELINE.json configs[1]): Helmholtz operator (collocated,
+lam=1) on a synthetic deformed tetrahedral mesh, P=4, 2^20 elements per GPU,
+FP64, inputs resident in HBM (9.4 GB of traffic per apply >> 126 MB L2, so
+no flush is needed between steps).  One process per GPU; every rank owns a
 contiguous element range of the same seeded mesh (weak scaling, no
 collective in the timed region); time = max over ranks of CUDA-event time.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl sk|reference]
+The same JSON line carries ``per_shape_P`` -- the BASELINE metric itself
+("Helmholtz apply GDOF/s per shape vs P; % of roofline"): every shape at
+P=2..10 (deformed, plus regular), and mass / stiffness on prism and pyr at
+P=2..8 (configs[2]); each cell >= 1 GB of algorithmic traffic per apply,
+with its roofline fraction, a sampled-element parity error against the CPU
+oracle and the SM clocks sampled while it ran.
 
-``--impl reference`` times the reference algorithm on the host cores (the
-numpy oracle restatement of speckern's sum-factorised operators; the
-reference is pure Python, so there is no compiled reference to time).
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl sk|reference]
+                  [--workload tet4|hex4|mixed6|c0hex] [--sweep auto|on|off]
+
+``--gpus N`` (N > 1) without a torchrun environment re-launches itself under
+``torch.distributed.run`` with N ranks on 127.0.0.1.
+
+``--impl reference`` times the reference's own CPU implementation on the
+host cores: the unmodified ``speckern`` package installed in
+``baseline/_ref`` (``apply_operator(HELMHOLTZ_COLL, block, SUM_FAC, lam)``,
+one worker process per core), or -- when it is not installed -- the numpy
+oracle restatement of the same algorithm.
 """
 
 from __future__ import annotations
@@ -23,26 +36,34 @@ os.environ.setdefault("OMP_NUM_THREADS", "1")
 
 import argparse  # noqa: E402
 import json  # noqa: E402
+import socket  # noqa: E402
 import statistics  # noqa: E402
 import subprocess  # noqa: E402
 import sys  # noqa: E402
+import threading  # noqa: E402
 import time  # noqa: E402
 
 import numpy as np  # noqa: E402
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
 
 SHAPE, ORDER, E_PER_GPU, LAM, SEED = "tet", 4, 1 << 20, 1.0, 0
 METRIC = "Helmholtz apply GDOF/s (tet, P=4, deformed, FP64)"
 UNIT = "GDOF/s"
-
+SHAPES = ("hex", "prism", "pyr", "tet")
 
 WORKLOADS = {
     # BASELINE configs[1]: Helmholtz, tet, P=4, ~10^6 deformed elements per GPU
     "tet4": {"blocks": [("tet", 4, 1 << 20)],
              "metric": METRIC,
              "name": "helmholtz_coll tet P=4 deformed, 2^20 elements per GPU (BASELINE configs[1])"},
+    # BASELINE configs[0]: Helmholtz, hex, P=4, 10^3 deformed elements (an
+    # L2-resident latency figure: L2 flushed before every timed apply)
+    "hex4": {"blocks": [("hex", 4, 1000)],
+             "metric": "Helmholtz apply GDOF/s (hex, P=4, 10^3 deformed elements, cold L2, FP64)",
+             "name": "helmholtz_coll hex P=4 deformed, 1000 elements per GPU (BASELINE configs[0])"},
     # BASELINE configs[3]: mixed hex/prism/pyr/tet Helmholtz, P=6, sharded
     "mixed6": {"blocks": [("hex", 6, 1 << 17), ("prism", 6, 1 << 17), ("pyr", 6, 1 << 17), ("tet", 6, 1 << 17)],
                "metric": "Helmholtz apply GDOF/s (mixed hex/prism/pyr/tet, P=6, deformed, FP64)",
@@ -65,6 +86,23 @@ def _peaks():
         return {"hbm_gbs": 6650.0}, "fallback"
 
 
+def _fp64_peak():
+    """Measured FP64 peak on B200 (TFLOP/s): the higher of the DFMA-chain and
+    DMMA microbenchmarks (profiles/fp64_peak.json, profiles/r01b/dmma_peak.json)."""
+    vals = []
+    try:
+        with open(os.path.join(ROOT, "profiles", "fp64_peak.json")) as fh:
+            vals.append(float(json.load(fh)["fp64_tflops"]))
+    except (OSError, ValueError, KeyError):
+        pass
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01b", "dmma_peak.json")) as fh:
+            vals.extend(float(v) for v in json.load(fh)["dmma_tflops"].values())
+    except (OSError, ValueError, KeyError):
+        pass
+    return max(vals) if vals else 37.0
+
+
 def _config(wl, spec, ws):
     step_bytes = 0
     for shape, P, e in spec:
@@ -72,70 +110,125 @@ def _config(wl, spec, ws):
 
         q = qcounts(shape, P)
         step_bytes += 8 * (2 * mode_count(shape, P) + 7 * q[0] * q[1] * q[2]) * e
+    l2 = (f"inputs > L2 ({step_bytes / 1e9:.2f} GB per step per GPU), no flush" if step_bytes > 4 * 126e6
+          else f"inputs ({step_bytes / 1e6:.1f} MB) fit in L2: 256 MB L2 flush before every timed apply")
     return {
         "workload": wl["name"],
         "blocks": [{"shape": s, "order": P, "elements_per_gpu": e} for s, P, e in spec],
         "elements_total": sum(e for _, _, e in spec) * ws,
         "lam": LAM,
         "geometry": "deformed (seeded sinusoidal, reference geometry.py:275-300)",
-        "l2": f"inputs > L2 ({step_bytes / 1e9:.2f} GB per step per GPU), no flush",
+        "l2": l2,
         "parallelism": f"elements sharded contiguously over {ws} GPU(s), no collective",
     }
 
 
+# ---------------------------------------------------------------------------
+# clocks: NVML sampled from a thread every ~5 ms for the whole run, so even a
+# 30-ms timed region carries samples; summaries are taken per time window
+
+_REASONS = {  # nvmlClocksEventReason* bits
+    0x8: "hw_slowdown",
+    0x40: "hw_thermal_slowdown",
+    0x20: "sw_thermal_slowdown",
+    0x4: "sw_power_cap",
+    0x80: "hw_power_brake_slowdown",
+}
+
+
 class Clocks:
-    """nvidia-smi sampler running during the timed region."""
+    """Background SM-clock / throttle-reason sampler (NVML; nvidia-smi when
+    NVML is unavailable)."""
 
-    Q = (
-        "clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-        "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
-    )
+    def __init__(self, dev: int, period_s: float = 0.005):
+        self.dev, self.period = dev, period_s
+        self.samples: list = []  # (t, sm_mhz, reasons_mask)
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._thr = None
+        self._proc = None
 
-    def __init__(self, dev: int):
-        self.dev = dev
-        self.p = None
-
-    def __enter__(self):
+    def start(self):
         try:
-            self.p = subprocess.Popen(
-                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-i", str(self.dev), "-lms", "50"],
-                stdout=subprocess.PIPE,
-                stderr=subprocess.DEVNULL,
-                text=True,
-            )
-        except OSError:
-            self.p = None
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self._nvml_index())
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+
+            def loop():
+                while not self._stop.is_set():
+                    try:
+                        sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                        rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        self.samples.append((time.perf_counter(), float(sm), int(rs)))
+                    except Exception:  # noqa: BLE001 - sampling must never break the bench
+                        pass
+                    self._stop.wait(self.period)
+
+            self._thr = threading.Thread(target=loop, daemon=True)
+            self._thr.start()
+        except Exception:  # noqa: BLE001
+            self._start_smi()
         return self
 
-    def __exit__(self, *exc):
-        self.lines = []
-        if self.p is not None:
-            self.p.terminate()
+    def _nvml_index(self) -> int:
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        if vis:
             try:
-                out, _ = self.p.communicate(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.p.kill()
-                out, _ = self.p.communicate()
-            self.lines = [ln for ln in out.splitlines() if ln.strip()]
-
-    def summary(self):
-        sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            f = [x.strip() for x in ln.split(",")]
-            try:
-                sm.append(float(f[0]))
-                mx = max(mx, float(f[1]))
+                return int(vis.split(",")[self.dev])
             except (ValueError, IndexError):
-                continue
-            for name, v in zip(names, f[2:]):
-                if v.lower() == "active":
-                    reasons.add(name)
+                return self.dev
+        return self.dev
+
+    def _start_smi(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self._proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits", "-i", str(self._nvml_index()),
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self._proc = None
+
+        def reader():
+            names = [0x8, 0x40, 0x20, 0x4]
+            for ln in self._proc.stdout:
+                f = [x.strip() for x in ln.split(",")]
+                try:
+                    sm, mx = float(f[0]), float(f[1])
+                except (ValueError, IndexError):
+                    continue
+                self.max_mhz = mx
+                mask = 0
+                for bit, v in zip(names, f[2:]):
+                    if v.lower() == "active":
+                        mask |= bit
+                self.samples.append((time.perf_counter(), sm, mask))
+
+        if self._proc is not None:
+            self._thr = threading.Thread(target=reader, daemon=True)
+            self._thr.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._proc is not None:
+            self._proc.terminate()
+        if self._thr is not None:
+            self._thr.join(timeout=2)
+
+    def summary(self, t0: float | None = None, t1: float | None = None, pad: float = 0.0):
+        sel = [s for s in list(self.samples)
+               if (t0 is None or s[0] >= t0 - pad) and (t1 is None or s[0] <= t1 + pad)]
+        mask = 0
+        for s in sel:
+            mask |= s[2]
         return {
-            "sm_mhz": statistics.median(sm) if sm else None,
-            "sm_max_mhz": mx or None,
-            "reasons": sorted(reasons),
-            "samples": len(sm),
+            "sm_mhz": statistics.median(s[1] for s in sel) if sel else None,
+            "sm_min_mhz": min(s[1] for s in sel) if sel else None,
+            "sm_max_mhz": self.max_mhz,
+            "reasons": sorted(n for b, n in _REASONS.items() if mask & b),
+            "samples": len(sel),
         }
 
 
@@ -146,21 +239,54 @@ def _dist():
     return ws, rank, local
 
 
+def _relaunch(args) -> int:
+    """--gpus N > 1 outside torchrun: run this script under
+    torch.distributed.run with N ranks (one per GPU) and return its status."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (the reference arm and the cpu_baseline leg)
+
 _CPU_STATE: dict = {}
 
 
-def _cpu_init(counter, per_core, blocks):
-    """Worker initialiser: claim a distinct contiguous slice of one block of
-    the workload (blocks round-robin over workers) and build it with the
-    oracle (geometry, coefficients, lam payload)."""
-    import oracle as O
-    from oracle.geom import deformed_coords, payload_lam
+def _ref_available() -> bool:
+    return os.path.isdir(os.path.join(REF_DIR, "speckern"))
 
+
+def _cpu_init(counter, per_core, blocks, kind):
+    """Worker initialiser: build one block of the workload (blocks round-robin
+    over workers).  kind "reference": the unmodified speckern from
+    baseline/_ref (make_field + bench-style seeded coefficients,
+    speckern/bench.py:167-172); kind "port": the oracle restatement on a
+    distinct contiguous slice of the same seeded mesh."""
     with counter.get_lock():
         idx = counter.value
         counter.value += 1
     k = idx % len(blocks)
     shape, P = blocks[k]
+    if kind == "reference":
+        sys.path.insert(0, REF_DIR)
+        from speckern.field_block import make_field
+        from speckern.geometry import GeometryClass
+        from speckern.operators import OperatorKind, Strategy
+        from speckern.shapes import Shape
+
+        fld = make_field(Shape[shape.upper()], P, GeometryClass.DEFORMED, per_core, seed=SEED + k)
+        blk = fld.blocks[0]
+        rng = np.random.default_rng([SEED, list(Shape).index(Shape[shape.upper()]), P, 1])
+        blk.set_elements(np.ascontiguousarray(rng.uniform(-1.0, 1.0, (per_core, blk.n_data)).T)[None])
+        _CPU_STATE["ref"] = (blk, OperatorKind.HELMHOLTZ_COLL, Strategy.SUM_FAC)
+        return
+    import oracle as O
+    from oracle.geom import deformed_coords, payload_lam
+
     first, n = (idx // len(blocks)) * per_core, per_core
     el = O.element(shape, P)
     geo = O.deformed_geometry_from_coords(el, deformed_coords(el, O.deformation_params(n, SEED + k, first=first)))
@@ -170,7 +296,14 @@ def _cpu_init(counter, per_core, blocks):
 
 
 def _cpu_task(reps):
-    """Apply the reference Helmholtz to this worker's slice ``reps`` times."""
+    """Apply the reference Helmholtz to this worker's block ``reps`` times."""
+    if "ref" in _CPU_STATE:
+        from speckern.operators import apply_operator
+
+        blk, kind, strat = _CPU_STATE["ref"]
+        for _ in range(reps):
+            apply_operator(kind, blk, strat, LAM)
+        return blk.basis.n_modes * blk.n_elements * reps
     import oracle as O
 
     el, geo, x, lp = _CPU_STATE["slice"]
@@ -180,18 +313,21 @@ def _cpu_task(reps):
 
 
 class CpuReference:
-    """The reference algorithm (numpy oracle restatement of speckern's
-    sum-factorised Helmholtz, operators.py:670-699) on the host cores: one
-    worker process per core, each on its own contiguous element slice of the
-    workload (numpy is GIL-bound at these matrix sizes, so threads do not
-    scale).  Throughput = DOF / parent wall time of one pass over all slices."""
+    """The reference Helmholtz (speckern.operators.apply_operator
+    HELMHOLTZ_COLL / SUM_FAC, operators.py:670-699, 724-746) on the host
+    cores: one worker process per core, each applying it to its own block of
+    the workload (numpy is GIL-bound at these matrix sizes, so threads do not
+    scale).  Throughput = DOF / parent wall time of one pass over all
+    workers."""
 
-    def __init__(self, cores: int, per_core: int = 4096, blocks=((SHAPE, ORDER),)):
+    def __init__(self, cores: int, per_core: int = 4096, blocks=((SHAPE, ORDER),), kind: str | None = None):
         import multiprocessing as mp
 
         ctx = mp.get_context("spawn")
+        self.kind = kind or ("reference" if _ref_available() else "port")
         self.cores, self.per_core = cores, per_core
-        self.pool = ctx.Pool(cores, initializer=_cpu_init, initargs=(ctx.Value("i", 0), per_core, tuple(blocks)))
+        self.pool = ctx.Pool(cores, initializer=_cpu_init,
+                             initargs=(ctx.Value("i", 0), per_core, tuple(blocks), self.kind))
         self.reps = 1
         self.run(1)  # warm up every worker
 
@@ -210,16 +346,20 @@ class CpuReference:
         self.pool.join()
 
 
+def _per_core(spec) -> int:
+    per_core = int(os.environ.get("SK_BENCH_CPU_PER_CORE", "2048"))
+    if any(P >= 6 for _, P, _ in spec):
+        per_core = max(1, per_core // 8)
+    return per_core
+
+
 def run_reference(args, ws, rank):
     if rank != 0:
         return
     wl = WORKLOADS[args.workload]
     spec = [(s, P, args.elements or e) for s, P, e in wl["blocks"]]
     cores = os.cpu_count() or 1
-    per_core = int(os.environ.get("SK_BENCH_CPU_PER_CORE", "4096"))
-    if any(P >= 6 for _, P, _ in spec):
-        per_core = max(1, per_core // 8)
-    ref = CpuReference(cores, per_core, [(s, P) for s, P, _ in spec])
+    ref = CpuReference(cores, min(_per_core(spec), max(e for _, _, e in spec)), [(s, P) for s, P, _ in spec])
     step_s = max(0.3, min(3.0, 150.0 / max(1, args.steps + args.warmup)))
     reps = ref.calibrate(step_s)
     for _ in range(args.warmup):
@@ -231,6 +371,8 @@ def run_reference(args, ws, rank):
     ref.close()
     value = statistics.median(vals)
     n_sample = ref.per_core * cores
+    what = ("unmodified speckern (baseline/_ref) apply_operator(HELMHOLTZ_COLL, SUM_FAC)" if ref.kind == "reference"
+            else "oracle port of speckern's sum-factorised Helmholtz")
     line = {
         "impl": "reference",
         "metric": wl["metric"],
@@ -249,12 +391,159 @@ def run_reference(args, ws, rank):
             "value": value,
             "unit": UNIT,
             "cores": cores,
-            "kind": "port",
-            "sample": f"{n_sample} elements ({ref.per_core} per core process) x {reps} passes per step, median of {args.steps} steps",
+            "kind": ref.kind,
+            "sample": f"{what}: {n_sample} elements ({ref.per_core} per core process) x {reps} passes per step, "
+                      f"median of {args.steps} steps",
         },
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# per (shape, P) sweep: the BASELINE metric table
+
+SWEEP_BYTES = 1.2e9  # algorithmic bytes per apply per cell (>= 1 GB, >> L2)
+POOL = 1 << 16  # reference-seeded elements per pool, tiled to the cell size
+
+
+def _cells(quick: bool):
+    orders = (2, 4, 6, 8, 10) if quick else tuple(range(2, 11))
+    out = []
+    for s in SHAPES:
+        for P in orders:
+            out.append(("helm_deformed", "helm", True, s, P))
+    for s in SHAPES:
+        for P in orders:
+            out.append(("helm_regular", "helm", False, s, P))
+    for tab, op in (("mass_deformed", "mass"), ("stiff_deformed", "stiff")):
+        for s in ("prism", "pyr"):
+            for P in (orders if quick else range(2, 9)):
+                if P <= 8:
+                    out.append((tab, op, True, s, P))
+    return out
+
+
+def run_sweep(args, ws, rank, dist, clk, quick=False):
+    """Every cell: a block of >= 1 GB algorithmic traffic per apply built from
+    a tiled pool of seeded elements, timed over >= 0.15 s of back-to-back
+    applies with CUDA events (max over ranks), parity of 6 sampled elements
+    against the CPU oracle on identical inputs, clocks over the cell's
+    window."""
+    import torch
+
+    import oracle as O
+    import paper_2604_04644_b200 as sk
+    from oracle.geom import deformed_coords
+    from paper_2604_04644_b200.geometry import synthetic_affine_vertices, synthetic_deformation_params
+
+    peaks, _ = _peaks()
+    hbm, fp64 = peaks.get("hbm_gbs", 6650.0), _fp64_peak()
+    kinds = {"helm": (sk.OperatorKind.HELMHOLTZ_COLL, 1.0), "stiff": (sk.OperatorKind.HELMHOLTZ_COLL, 0.0),
+             "mass": (sk.OperatorKind.MASS, 1.0)}
+    params = synthetic_deformation_params(POOL, SEED)
+    verts = {}
+    rng = np.random.default_rng(1234 + rank)
+    res = []
+    for tab, op, deformed, s, P in _cells(quick):
+        kind, lam = kinds[op]
+        shp = sk.Shape(s)
+        b = sk.build_shape_basis(shp, P)
+        bel = sk.operator_bytes(kind, shp, P, deformed, lam)
+        if deformed:
+            E = max(POOL, int(SWEEP_BYTES / bel))
+            reps_e = -(-E // POOL)
+            fac = sk.GeometricFactors(sk.GeometryClass.DEFORMED, shp, E, params=np.tile(params, (reps_e, 1))[:E], basis=b)
+        else:
+            # regular geometry is FP64-bound (7 doubles per element): size by work
+            E = int(min(1 << 21, max(POOL, 4e10 / sk.operator_flops(kind, shp, P))))
+            if s not in verts:
+                verts[s] = synthetic_affine_vertices(shp, POOL, SEED)
+            pool = sk.make_affine_block(shp, verts[s])
+            reps_e = -(-E // POOL)
+            fac = sk.GeometricFactors(sk.GeometryClass.REGULAR, shp, E,
+                                      dxi_dx=np.tile(pool.dxi_dx, (reps_e, 1, 1))[:E],
+                                      jac=np.tile(pool.jac, reps_e)[:E])
+        blk = sk.Block(b, fac, sk.FieldState.COEFF, 1, 1)
+        xd = blk.device(sk.AccessQualifier.WRITE_ONLY)
+        gen = torch.Generator(device=xd.device)
+        gen.manual_seed(P * 100 + SHAPES.index(s))
+        xd.uniform_(-1.0, 1.0, generator=gen)
+        out = blk.like(sk.FieldState.COEFF)
+        if op == "mass":
+            fn = lambda: sk.mass_apply(blk, out=out)  # noqa: E731
+        else:
+            fn = lambda: sk.helmholtz_apply(blk, lam, out=out)  # noqa: E731
+        fn()
+        torch.cuda.synchronize()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record()
+        fn()
+        t1.record()
+        torch.cuda.synchronize()
+        est = max(t0.elapsed_time(t1) / 1e3, 1e-6)
+        reps = int(min(400, max(5, 0.15 / est)))
+        if dist:
+            rt = torch.tensor([reps], device="cuda")
+            dist.all_reduce(rt, op=dist.ReduceOp.MAX)
+            reps = int(rt.item())
+            dist.barrier()
+        torch.cuda.synchronize()
+        w0 = time.perf_counter()
+        t0.record()
+        for _ in range(reps):
+            fn()
+        t1.record()
+        torch.cuda.synchronize()
+        w1 = time.perf_counter()
+        ms = t0.elapsed_time(t1) / reps
+        # parity on sampled elements, identical inputs, CPU oracle
+        err = None
+        if rank == 0:
+            idx = sorted({0, 1, E // 2, E - 2, E - 1, int(rng.integers(0, E))})
+            el = O.element(s, P)
+            nm = b.n_modes
+            xs = xd.view(E, nm)[idx].cpu().numpy().T
+            ys = out.device(sk.AccessQualifier.READ_ONLY).view(E, nm)[idx].cpu().numpy().T
+            if deformed:
+                prm = params[[i % POOL for i in idx]]
+                geo = O.deformed_geometry_from_coords(el, deformed_coords(el, prm))
+            else:
+                geo = O.affine_geometry(s, verts[s][[i % POOL for i in idx]])
+            ref = O.mass(el, geo, xs) if op == "mass" else O.helmholtz_coll(el, geo, xs, lam)
+            err = O.rel_diff(ys, ref)
+        del blk, out, fac, xd
+        torch.cuda.empty_cache()
+        res.append((tab, s, P, E, ms, err, clk.summary(w0, w1) if clk else None, kind, lam, deformed))
+    # max over ranks of every cell's time (weak scaling: each rank ran its own block)
+    times = torch.tensor([r[4] for r in res], dtype=torch.float64, device="cuda")
+    if dist:
+        dist.all_reduce(times, op=dist.ReduceOp.MAX)
+    tables: dict = {}
+    info: dict = {}
+    for r, ms in zip(res, times.tolist()):
+        tab, s, P, E, _, err, ck, kind, lam, deformed = r
+        shp = sk.Shape(s)
+        nm = sk.mode_count(shp, P)
+        bel = sk.operator_bytes(kind, shp, P, deformed, lam)
+        fl = sk.operator_flops(kind, shp, P)
+        gdof = ws * nm * E / (ms / 1e3) / 1e9
+        roof_hbm = ws * hbm * 1e9 / bel * nm / 1e9
+        roof_fp = ws * fp64 * 1e12 / fl * nm / 1e9
+        roof = min(roof_hbm, roof_fp)
+        frac = gdof / roof
+        row = [P, float(f"{gdof:.4g}"), round(frac, 3), None if err is None else float(f"{err:.1e}"),
+               None if not ck or ck["sm_mhz"] is None else round(ck["sm_mhz"])]
+        tables.setdefault(tab, {}).setdefault(s, []).append(row)
+        meta = info.setdefault(tab, {"bound": set(), "throttle": set(), "max_parity": 0.0})
+        meta["bound"].add("hbm" if roof_hbm <= roof_fp else "fp64")
+        meta["throttle"].update(ck["reasons"] if ck else [])
+        meta["max_parity"] = max(meta["max_parity"], err or 0.0)
+    for tab, meta in info.items():
+        tables[tab]["bound"] = sorted(meta["bound"])
+        tables[tab]["throttle"] = sorted(meta["throttle"])
+        tables[tab]["max_parity"] = float(f"{meta['max_parity']:.1e}")
+    return tables, fp64
 
 
 def run_device(args, ws, rank, local):
@@ -270,11 +559,15 @@ def run_device(args, ws, rank, local):
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        chk = torch.ones(1, device="cuda")
+        dist.all_reduce(chk)  # communicator up: comm_nranks == world size
+        assert int(chk.item()) == ws, "NCCL communicator does not span every rank"
     dev = torch.cuda.current_device()
+    clk = Clocks(dev).start()  # sampling from before the warm-up on
     wl = WORKLOADS[args.workload]
     spec = [(s, P, args.elements or e) for s, P, e in wl["blocks"]]
     if args.workload == "c0hex":
-        return run_c0(args, ws, rank, dist, dev, wl)
+        return run_c0(args, ws, rank, dist, dev, wl, clk)
 
     # every rank owns a contiguous slice of each block of the seeded mesh
     # (weak scaling: elements per GPU fixed); block k uses seed SEED + k
@@ -292,9 +585,13 @@ def run_device(args, ws, rank, local):
     torch.cuda.synchronize()
     stream = torch.cuda.current_stream()
     nb = len(blocks)
+    cold = args.workload == "hex4"  # L2-resident workload: flush L2 before every timed apply
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda") if cold else None
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(nb + 1)] for _ in range(args.steps)]
 
     def step(marks=None):
+        if flush is not None:
+            flush.zero_()
         for b, (blk, out) in enumerate(zip(blocks, outs)):
             if marks is not None:
                 marks[b].record(stream)
@@ -309,18 +606,21 @@ def run_device(args, ws, rank, local):
         dist.barrier()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     n0 = _lib.launch_count()
-    with Clocks(dev) as clk:
-        torch.cuda.synchronize()
-        t0.record(stream)
-        for i in range(args.steps):
-            step(ev[i])
-        t1.record(stream)
-        torch.cuda.synchronize()
+    torch.cuda.synchronize()
+    w0 = time.perf_counter()
+    t0.record(stream)
+    for i in range(args.steps):
+        step(ev[i])
+    t1.record(stream)
+    torch.cuda.synchronize()
+    w1 = time.perf_counter()
     launches = _lib.launch_count() - n0
     if dist:
         dist.barrier()
     ms = t0.elapsed_time(t1)
     per_block_ms = [sum(ev[i][b].elapsed_time(ev[i][b + 1]) for i in range(args.steps)) / args.steps for b in range(nb)]
+    if cold:  # the apply itself (cold L2), not the flush kernel
+        ms = sum(per_block_ms) * args.steps
     tmax = torch.tensor([ms], dtype=torch.float64, device="cuda")
     if dist:
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
@@ -328,6 +628,30 @@ def run_device(args, ws, rank, local):
     ndof_rank = sum(b.basis.n_modes * b.n_elements for b in blocks)
     ndof = ndof_rank * ws
     value = ndof * args.steps / (ms_max / 1e3) / 1e9
+    main_clocks = clk.summary(w0, w1)
+
+    warm_us = None
+    if cold:
+        # L2-warm latency of the same apply, CUDA-graph captured back to back
+        g = torch.cuda.CUDAGraph()
+        s2 = torch.cuda.Stream()
+        s2.wait_stream(stream)
+        with torch.cuda.stream(s2):
+            for _ in range(3):
+                sk.helmholtz_apply(blocks[0], LAM, out=outs[0])
+            with torch.cuda.graph(g, stream=s2):
+                for _ in range(20):
+                    sk.helmholtz_apply(blocks[0], LAM, out=outs[0])
+        torch.cuda.synchronize()
+        g.replay()
+        torch.cuda.synchronize()
+        a, c = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(10):
+            g.replay()
+        c.record()
+        torch.cuda.synchronize()
+        warm_us = a.elapsed_time(c) / 200 * 1e3
 
     # e2e through the public API with host buffers: H2D of the step's
     # coefficients (pinned), apply, D2H of the result, every step
@@ -340,14 +664,14 @@ def run_device(args, ws, rank, local):
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
-    w0 = time.perf_counter()
+    e0 = time.perf_counter()
     for _ in range(e2e_steps):
         for blk, out in zip(blocks, outs):
             blk.host(sk.AccessQualifier.READ_WRITE)  # host copy is now the live one
             sk.helmholtz_apply(blk, LAM, out=out)  # -> H2D transfer + kernel
             out.host()  # -> D2H transfer of the result
     torch.cuda.synchronize()
-    we = torch.tensor([time.perf_counter() - w0], dtype=torch.float64, device="cuda")
+    we = torch.tensor([time.perf_counter() - e0], dtype=torch.float64, device="cuda")
     if dist:
         dist.all_reduce(we, op=dist.ReduceOp.MAX)
     e2e_val = ndof * e2e_steps / float(we.item()) / 1e9
@@ -355,6 +679,7 @@ def run_device(args, ws, rank, local):
     # roofline of the dominant kernel: algorithmic bytes per launch / its
     # average duration (CUDA events on the launching stream)
     peaks, src = _peaks()
+    hbm = peaks.get("hbm_gbs", 6650.0)
     dom = int(np.argmax(per_block_ms))
     db = blocks[dom]
     bytes_per_launch = sk.operator_bytes(sk.OperatorKind.HELMHOLTZ_COLL, db.shape, db.basis.order, True, LAM) * db.n_elements
@@ -363,7 +688,7 @@ def run_device(args, ws, rank, local):
                      for b in blocks)
     traffic = None
     prof = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(prof):
+    if os.path.exists(prof) and not cold:
         try:
             with open(prof) as fh:
                 per_el = json.load(fh).get(f"{db.shape.value}_P{db.basis.order}_helm_per_element_bytes")
@@ -371,13 +696,33 @@ def run_device(args, ws, rank, local):
         except (OSError, ValueError):
             traffic = None
 
-    if rank == 0:
+    # the BASELINE metric table (every shape x P), default workload only
+    sweep = args.sweep == "on" or (args.sweep == "auto" and args.workload == "tet4")
+    tables = fp64 = None
+    if sweep:
+        sw0 = time.perf_counter()
+        tables, fp64 = run_sweep(args, ws, rank, dist, clk, quick=args.sweep_quick)
+        sweep_s = time.perf_counter() - sw0
+
+    cpu = None
+    if rank == 0 and ws == 1:
         cores = os.cpu_count() or 1
-        ref = CpuReference(cores, 4096 if max(P for _, P, _ in spec) < 6 else 512, [(s, P) for s, P, _ in spec])
+        ref = CpuReference(cores, min(_per_core(spec), max(e for _, _, e in spec)), [(s, P) for s, P, _ in spec])
         reps = ref.calibrate(10.0)
         dofs, dt = ref.run(reps)
         ref.close()
-        cpu_v = dofs / dt / 1e9
+        what = ("unmodified speckern (baseline/_ref) apply_operator(HELMHOLTZ_COLL, SUM_FAC)"
+                if ref.kind == "reference" else "oracle port of speckern's sum-factorised Helmholtz")
+        cpu = {
+            "value": dofs / dt / 1e9,
+            "unit": UNIT,
+            "cores": cores,
+            "kind": ref.kind,
+            "sample": f"{what}: {ref.per_core * cores} elements of the workload ({cores} processes x "
+                      f"{ref.per_core}, blocks round-robin) x {reps} passes: {dofs / 1e6:.0f} MDOF in {dt:.1f} s",
+        }
+    clk.stop()
+    if rank == 0:
         cfg = _config(wl, spec, ws)
         line = {
             "metric": wl["metric"],
@@ -396,36 +741,45 @@ def run_device(args, ws, rank, local):
             "roofline": {
                 "bound": "hbm",
                 "achieved": achieved,
-                "peak": peaks.get("hbm_gbs", 6650.0),
+                "peak": hbm,
                 "unit": "GB/s",
-                "frac": achieved / peaks.get("hbm_gbs", 6650.0),
+                "frac": achieved / hbm,
                 "traffic": traffic,
                 "peak_source": src,
                 "bytes_per_launch": bytes_per_launch,
                 "kernel": f"helmholtz {db.shape.value} P={db.basis.order}",
-                "step_frac": step_bytes / (ms / 1e3 / args.steps) / 1e9 / peaks.get("hbm_gbs", 6650.0),
+                "step_frac": step_bytes / (ms / 1e3 / args.steps) / 1e9 / hbm,
             },
-            "cpu_baseline": {
-                "value": cpu_v,
-                "unit": UNIT,
-                "cores": cores,
-                "kind": "port",
-                "sample": f"{ref.per_core * cores} elements of the workload ({cores} processes x {ref.per_core}, "
-                          f"blocks round-robin) x {reps} passes: {dofs / 1e6:.0f} MDOF in {dt:.1f} s",
-            },
+            "cpu_baseline": cpu,
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
-            "clocks": clk.summary(),
+            "clocks": main_clocks,
+            "comm": {"backend": "nccl" if dist else None, "world": ws, "collectives_in_timed_region": 0},
         }
         if nb > 1:
             line["per_block_ms"] = {f"{b.shape.value}": m for b, m in zip(blocks, per_block_ms)}
+        if warm_us is not None:
+            line["latency_us"] = {"cold_l2": ms_max / args.steps * 1e3, "warm_l2_graph": warm_us}
+        if tables is not None:
+            line["per_shape_P"] = {
+                "columns": ["P", "gdof_s", "roofline_frac", "parity_maxrel", "sm_mhz"],
+                "roofline": f"min(HBM {hbm:.0f} GB/s x N_P / bytes_el, FP64 {fp64:.1f} TF x N_P / flops_el), "
+                            "bytes_el = 8(2N_P + 7N_Q) (6N_Q stiffness, N_Q mass; 7 / 6 / 1 regular), "
+                            "flops_el = reference operator_flops",
+                "parity": "6 sampled elements per cell vs CPU oracle, max-normalised (speckern bench.py:192-194)",
+                "cells": f"deformed: max({POOL}, {SWEEP_BYTES / 1e9:.1f} GB / bytes_el) elements per apply; regular: "
+                         f"min(2^21, max({POOL}, 4e10 / flops_el)); tiled pool of {POOL} seeded elements; "
+                         "time = CUDA events over >= 0.15 s of back-to-back applies",
+                "seconds": round(sweep_s, 1),
+                **tables,
+            }
         print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()
         dist.destroy_process_group()
 
 
-def run_c0(args, ws, rank, dist, dev, wl):
+def run_c0(args, ws, rank, dist, dev, wl, clk):
     """Assembled C0 Helmholtz: gather -> elemental kernel -> scatter -> NCCL
     exchange of the two shared DOF layers, all inside the timed region."""
     import torch
@@ -446,13 +800,14 @@ def run_c0(args, ws, rank, dist, dev, wl):
     stream = torch.cuda.current_stream()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     n0 = _lib.launch_count()
-    with Clocks(dev) as clk:
-        torch.cuda.synchronize()
-        t0.record(stream)
-        for _ in range(args.steps):
-            mesh.helmholtz(x, LAM)
-        t1.record(stream)
-        torch.cuda.synchronize()
+    torch.cuda.synchronize()
+    w0 = time.perf_counter()
+    t0.record(stream)
+    for _ in range(args.steps):
+        mesh.helmholtz(x, LAM)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    w1 = time.perf_counter()
     launches = _lib.launch_count() - n0
     ms = t0.elapsed_time(t1)
     tmax = torch.tensor([ms], dtype=torch.float64, device="cuda")
@@ -466,11 +821,11 @@ def run_c0(args, ws, rank, dist, dev, wl):
     yh = torch.empty_like(xh).pin_memory()
     e2e_steps = max(3, min(args.steps, 10))
     torch.cuda.synchronize()
-    w0 = time.perf_counter()
+    e0 = time.perf_counter()
     for _ in range(e2e_steps):
         yh.copy_(mesh.helmholtz(xh.to("cuda", non_blocking=True), LAM))
     torch.cuda.synchronize()
-    we = torch.tensor([time.perf_counter() - w0], dtype=torch.float64, device="cuda")
+    we = torch.tensor([time.perf_counter() - e0], dtype=torch.float64, device="cuda")
     if dist:
         dist.all_reduce(we, op=dist.ReduceOp.MAX)
     e2e_val = n_global * e2e_steps / float(we.item()) / 1e9
@@ -480,6 +835,7 @@ def run_c0(args, ws, rank, dist, dev, wl):
     bel = sk.operator_bytes(sk.OperatorKind.HELMHOLTZ_COLL, sk.Shape.HEX, P, True, LAM)
     step_bytes = bel * mesh.E + 2 * 8 * mesh.n_dofs
     achieved = step_bytes / (ms / 1e3 / args.steps) / 1e9
+    clk.stop()
     if rank == 0:
         line = {
             "metric": wl["metric"],
@@ -504,7 +860,9 @@ def run_c0(args, ws, rank, dist, dev, wl):
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": 8 * mesh.n_dofs,
                     "d2h_bytes_per_step": 8 * mesh.n_dofs},
             "gpu_launches": launches,
-            "clocks": clk.summary(),
+            "clocks": clk.summary(w0, w1),
+            "comm": {"backend": "nccl" if dist else None, "world": ws,
+                     "collectives_in_timed_region": "2 P2P send/recv per interface per step" if ws > 1 else 0},
         }
         print(json.dumps(line), flush=True)
     if dist:
@@ -513,13 +871,12 @@ def run_c0(args, ws, rank, dist, dev, wl):
 
 
 def run_reference_sweep(args):
-    """Reference CPU path (oracle port of speckern's sum-factorised Helmholtz,
-    all host cores) per shape x order: one JSON line each, to sit beside the
-    device sweep (tools/sweep.py).  Bounded samples (~2 s per case)."""
+    """Reference CPU path per shape x order: one JSON line each, to sit beside
+    the device sweep.  Bounded samples (~2 s per case)."""
     cores = os.cpu_count() or 1
-    for shape in ("hex", "prism", "pyr", "tet"):
-        for P in range(1, 11):
-            per_core = max(8, int(2048 * (5.0 / (P + 1)) ** 3))
+    for shape in SHAPES:
+        for P in range(2, 11):
+            per_core = max(8, int(1024 * (5.0 / (P + 1)) ** 3))
             ref = CpuReference(cores, per_core, [(shape, P)])
             reps = ref.calibrate(1.5)
             vals = []
@@ -528,22 +885,31 @@ def run_reference_sweep(args):
                 vals.append(dof / dt / 1e9)
             ref.close()
             print(json.dumps({"impl": "reference", "op": "helm", "shape": shape, "P": P,
-                              "gdof_s": statistics.median(vals), "cores": cores, "kind": "port",
+                              "gdof_s": statistics.median(vals), "cores": cores, "kind": ref.kind,
                               "sample": f"{per_core * cores} elements x {reps} passes, median of 3"}), flush=True)
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["sk", "reference"], default="sk")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="tet4")
     ap.add_argument("--elements", type=int, default=0, help="override elements per block per GPU")
-    ap.add_argument("--sweep", action="store_true", help="with --impl reference: CPU GDOF/s per shape x order")
+    ap.add_argument("--sweep", choices=["auto", "on", "off"], default="auto",
+                    help="per (shape, P) table in the JSON line (auto: default workload only)")
+    ap.add_argument("--sweep-quick", action="store_true", help="P in {2,4,6,8,10} only")
+    ap.add_argument("--ref-sweep", action="store_true", help="with --impl reference: CPU GDOF/s per shape x order")
     args = ap.parse_args()
+    if args.gpus < 1:
+        raise SystemExit("--gpus must be >= 1")
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(_relaunch(args))
     ws, rank, local = _dist()
-    if args.impl == "reference" and args.sweep:
+    if ws != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={ws}: launch one rank per GPU")
+    if args.impl == "reference" and args.ref_sweep:
         if rank == 0:
             run_reference_sweep(args)
         return

@@ -150,6 +150,17 @@ int sk_c0_scatter(int order, int nx, int ny, int64_t nz_local, const double* loc
 int sk_helmholtz_apply_c0(const sk_basis* b, int geo_class, int nx, int ny, int64_t nz_local, const double* x,
                           const double* hpay, double lam, double* out, void* stream);
 
+/* ---- device memory (for callers without CUDA runtime bindings) --------------
+ * The MemoryRegion DEVICE space of a reference Block (field_block.py:67-149)
+ * held by a binding that loads only this library (integration/speckern_sk200.py).
+ * Copies are stream-ordered (pass NULL for the legacy default stream);
+ * sk_stream_synchronize waits for the stream. */
+int sk_device_alloc(int64_t bytes, void** ptr);
+int sk_device_free(void* ptr);
+int sk_copy_h2d(void* dst, const void* src, int64_t bytes, void* stream);
+int sk_copy_d2h(void* dst, const void* src, int64_t bytes, void* stream);
+int sk_stream_synchronize(void* stream);
+
 /* ---- diagnostics ------------------------------------------------------------ */
 /* Number of kernel launches this thread issued through the library. */
 int64_t sk_launch_count(void);
@@ -159,6 +170,10 @@ const char* sk_last_error(void);
  * CTA, out[1]=threads per CTA, out[2]=dynamic shared bytes. op: 0 helmholtz,
  * 1 mass, 2 bwd, 3 iprod, 4 physderiv, 5 iprod_deriv, 6 helmholtz noncoll. */
 int sk_launch_config(const sk_basis* b, int op, int64_t out[3]);
+/* Same, for a geometry class (the regular collocated Helmholtz is tuned
+ * with its own tile width and thread count); sk_launch_config reports the
+ * deformed configuration. */
+int sk_launch_config_geo(const sk_basis* b, int op, int geo_class, int64_t out[3]);
 
 #ifdef __cplusplus
 }

@@ -48,9 +48,15 @@ SIGNATURES = {
     "sk_c0_gather": (_I, [_I, _I, _I, _L, _P, _I, _P, _P]),
     "sk_c0_scatter": (_I, [_I, _I, _I, _L, _P, _I, _P, _P]),
     "sk_helmholtz_apply_c0": (_I, [_P, _I, _I, _I, _L, _P, _P, _D, _P, _P]),
+    "sk_device_alloc": (_I, [_L, ctypes.POINTER(_P)]),
+    "sk_device_free": (_I, [_P]),
+    "sk_copy_h2d": (_I, [_P, _P, _L, _P]),
+    "sk_copy_d2h": (_I, [_P, _P, _L, _P]),
+    "sk_stream_synchronize": (_I, [_P]),
     "sk_launch_count": (_L, []),
     "sk_last_error": (ctypes.c_char_p, []),
     "sk_launch_config": (_I, [_P, _I, _PL]),
+    "sk_launch_config_geo": (_I, [_P, _I, _I, _PL]),
 }
 
 _lib = None

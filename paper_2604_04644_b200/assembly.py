@@ -45,7 +45,23 @@ def exchange_interfaces(y, layer: int, group=None) -> None:
     if world == 1:
         return
     rank = dist.get_rank(group)
-    lo, hi = y[:layer], y[-layer:]
+    if y.is_cuda and dist.get_backend(group) == "gloo":
+        # gloo point-to-point moves host tensors: exchange host copies of the
+        # two boundary layers and add the neighbours' sums back on the device
+        h = torch.cat([y[:layer], y[-layer:]]).cpu()
+        lo_h, hi_h = h[:layer].clone(), h[layer:].clone()
+        _exchange(lo_h, hi_h, rank, world, group)
+        y[:layer] = lo_h.to(y.device)
+        y[-layer:] = hi_h.to(y.device)
+        return
+    _exchange(y[:layer], y[-layer:], rank, world, group)
+
+
+def _exchange(lo, hi, rank: int, world: int, group) -> None:
+    """lo += lower neighbour's hi layer, hi += upper neighbour's lo layer."""
+    import torch
+    import torch.distributed as dist
+
     recv_lo = torch.empty_like(lo) if rank > 0 else None
     recv_hi = torch.empty_like(hi) if rank < world - 1 else None
     ops = []
@@ -72,6 +88,10 @@ class C0HexMesh:
     def __init__(self, nx: int, ny: int, nz: int, order: int, amp: float = 0.05, rank: int = 0, world: int = 1):
         import torch
 
+        if nz < world:
+            # an empty slab would leave its scatter output unwritten, and the
+            # one-hop exchange cannot sum a layer shared by ranks r-1 and r+1
+            raise ValueError(f"need at least one element layer per rank: nz={nz} < world={world}")
         self.nx, self.ny, self.nz, self.P, self.amp = nx, ny, nz, order, amp
         self.z0, self.nzl = partition(nz, world, rank)
         self.first = self.z0 * nx * ny

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -11,6 +12,7 @@
 #include <vector>
 
 #include "../../include/sk200.h"
+#include "sk_tune.h"
 #include "sk_opset.hpp"
 
 namespace sk {
@@ -55,6 +57,10 @@ struct sk_basis {
   // device copies of gtab, one per device, created on first use
   std::mutex mu;
   std::vector<double*> gtab_dev;
+  // DMMA StdMat mass fragments (sk_dense.cuh), one per device, built on
+  // first use from the dense B the bwd_trans kernel produces
+  std::mutex dmu;
+  std::vector<double*> dense_dev;
 };
 
 namespace {
@@ -96,6 +102,72 @@ const double* device_gtab(sk_basis* b, int* status) {
   return b->gtab_dev[dev];
 }
 
+int run(sk_basis* b, int op, int geo, long long E, int W, int ncomp, const double* in, double* out,
+        const double* pay, double lam, long long in_n, long long out_n, void* stream, const double* dense = nullptr);
+
+// Dense basis matrix B[q][m] (= bwd_trans of the unit coefficient vectors,
+// so it is the sum-factorised kernel's own B) -> DMMA fragment tables on
+// this device (built once, cached on the basis).
+const double* device_dense(sk_basis* b, void* stream, int* status) {
+  *status = SK_OK;
+  const int nd = b->ops->dense_doubles;
+  if (nd <= 0) {
+    *status = fail(SK_ERR_UNSUPPORTED, "no dense mass kernel for this order");
+    return nullptr;
+  }
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) {
+    *status = cuda_status(e, "cudaGetDevice");
+    return nullptr;
+  }
+  std::lock_guard<std::mutex> lk(b->dmu);
+  if ((int)b->dense_dev.size() <= dev) b->dense_dev.resize(dev + 1, nullptr);
+  if (b->dense_dev[dev]) return b->dense_dev[dev];
+  const int nm = b->hb.nm, nq = b->hb.nq;
+  std::vector<double> eye((size_t)nm * nm, 0.0), bt((size_t)nm * nq), B((size_t)nq * nm), frag((size_t)nd);
+  for (int m = 0; m < nm; ++m) eye[(size_t)m * nm + m] = 1.0;
+  double *d_in = nullptr, *d_out = nullptr, *d_frag = nullptr;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  e = cudaMalloc(&d_in, sizeof(double) * eye.size());
+  if (e == cudaSuccess) e = cudaMalloc(&d_out, sizeof(double) * bt.size());
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_in, eye.data(), sizeof(double) * eye.size(), cudaMemcpyHostToDevice, s);
+  int st = SK_OK;
+  if (e == cudaSuccess) st = run(b, sk::OP_BWD, 0, nm, 1, 1, d_in, d_out, nullptr, 0.0, nm, nq, stream);
+  if (e == cudaSuccess && st == SK_OK)
+    e = cudaMemcpyAsync(bt.data(), d_out, sizeof(double) * bt.size(), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess && st == SK_OK) e = cudaStreamSynchronize(s);
+  cudaFree(d_in);
+  cudaFree(d_out);
+  if (st != SK_OK || e != cudaSuccess) {
+    *status = st != SK_OK ? st : cuda_status(e, "dense basis matrix");
+    return nullptr;
+  }
+  for (int m = 0; m < nm; ++m)
+    for (int q = 0; q < nq; ++q) B[(size_t)q * nm + m] = bt[(size_t)m * nq + q];
+  b->ops->fill_dense(B.data(), b->hb.refw.data(), frag.data());
+  e = cudaMalloc(&d_frag, sizeof(double) * frag.size());
+  if (e == cudaSuccess) e = cudaMemcpy(d_frag, frag.data(), sizeof(double) * frag.size(), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    cudaFree(d_frag);
+    *status = cuda_status(e, "dense fragment upload");
+    return nullptr;
+  }
+  b->dense_dev[dev] = d_frag;
+  return d_frag;
+}
+
+// StdMat (DMMA) or sum-factorised mass for this basis and geometry class:
+// the tuned table, overridden by SK_MASS_DENSE=0/1
+bool use_dense_mass(const sk_basis* b, int geo) {
+  if (b->ops->dense_doubles <= 0) return false;
+  if (const char* v = std::getenv("SK_MASS_DENSE")) {
+    if (v[0] == '0') return false;
+    if (v[0] == '1') return true;
+  }
+  return sk::kDenseMass[geo == SK_GEO_DEFORMED ? 1 : 0][b->hb.shape][b->hb.P];
+}
+
 int check_layout(long long E, int W, int ncomp) {
   if (E < 0) return fail(SK_ERR_ARG, "element count must be nonnegative");
   if (W < 1) return fail(SK_ERR_ARG, "interleave width must be at least 1");
@@ -106,7 +178,7 @@ int check_layout(long long E, int W, int ncomp) {
 long long padded(long long E, int W) { return ((E + W - 1) / W) * (long long)W; }
 
 int run(sk_basis* b, int op, int geo, long long E, int W, int ncomp, const double* in, double* out,
-        const double* pay, double lam, long long in_n, long long out_n, void* stream) {
+        const double* pay, double lam, long long in_n, long long out_n, void* stream, const double* dense) {
   int st = SK_OK;
   const double* g = device_gtab(b, &st);
   if (st) return st;
@@ -126,6 +198,7 @@ int run(sk_basis* b, int op, int geo, long long E, int W, int ncomp, const doubl
   r.ncomp = ncomp;
   r.geo = geo;
   r.lam = lam;
+  r.dense = dense;
   if (r.Epad == 0) return SK_OK;
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cuda_status(b->ops->launch(op, r, stream), "kernel launch");
@@ -165,6 +238,8 @@ int sk_basis_create(int shape, int order, sk_basis** out) {
 int sk_basis_destroy(sk_basis* b) {
   if (!b) return SK_OK;
   for (double* p : b->gtab_dev)
+    if (p) cudaFree(p);
+  for (double* p : b->dense_dev)
     if (p) cudaFree(p);
   delete b;
   return SK_OK;
@@ -296,8 +371,14 @@ int sk_mass_apply(const sk_basis* b, int geo, int64_t E, int W, int ncomp, const
   if (!b || (E > 0 && (!uhat || !wpay || !out))) return fail(SK_ERR_ARG, "null argument");
   if (geo != SK_GEO_REGULAR && geo != SK_GEO_DEFORMED) return fail(SK_ERR_ARG, "bad geometry class");
   if (int st = check_layout(E, W, ncomp)) return st;
-  return run(const_cast<sk_basis*>(b), sk::OP_MASS, geo, E, W, ncomp, uhat, out, wpay, 0.0, b->hb.nm, b->hb.nm,
-             stream);
+  sk_basis* bb = const_cast<sk_basis*>(b);
+  const double* dense = nullptr;
+  if (E > 0 && use_dense_mass(bb, geo)) {
+    int st = SK_OK;
+    dense = device_dense(bb, stream, &st);
+    if (st) return st;
+  }
+  return run(bb, sk::OP_MASS, geo, E, W, ncomp, uhat, out, wpay, 0.0, b->hb.nm, b->hb.nm, stream, dense);
 }
 
 int sk_helmholtz_apply(const sk_basis* b, int geo, int form, int64_t E, int W, int ncomp, const double* uhat,
@@ -395,6 +476,13 @@ int sk_apply_streamed(const sk_basis* b, int op, int geo, int64_t E, int W, int 
   r.ncomp = ncomp;
   r.geo = geo;
   r.lam = op == SK_STREAM_MASS ? 0.0 : lam;
+  if (kop == sk::OP_MASS && use_dense_mass(b, geo)) {
+    r.dense = device_dense(const_cast<sk_basis*>(b), stream, &st);
+    if (st) {
+      cleanup();
+      return st;
+    }
+  }
   for (int i = 0; i < nchunk && e == cudaSuccess; ++i) {
     const long long e0 = (long long)i * chunk, e1 = std::min<long long>(Epad, e0 + chunk);
     const size_t bytes = sizeof(double) * (size_t)((e1 - e0) * nm);
@@ -467,9 +555,43 @@ extern "C" {
 
 const char* sk_last_error(void) { return g_err.c_str(); }
 
+// ---- device memory helpers: a caller binding only this library (no CUDA
+// runtime bindings of its own) can hold the MemoryRegion DEVICE space
+int sk_device_alloc(int64_t bytes, void** ptr) {
+  if (!ptr || bytes < 0) return fail(SK_ERR_ARG, "bad argument");
+  *ptr = nullptr;
+  if (bytes == 0) return SK_OK;
+  return cuda_status(cudaMalloc(ptr, (size_t)bytes), "cudaMalloc");
+}
+
+int sk_device_free(void* ptr) { return ptr ? cuda_status(cudaFree(ptr), "cudaFree") : SK_OK; }
+
+int sk_copy_h2d(void* dst, const void* src, int64_t bytes, void* stream) {
+  if (bytes < 0 || (bytes > 0 && (!dst || !src))) return fail(SK_ERR_ARG, "bad argument");
+  if (bytes == 0) return SK_OK;
+  return cuda_status(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyHostToDevice, static_cast<cudaStream_t>(stream)),
+                     "cudaMemcpyAsync H2D");
+}
+
+int sk_copy_d2h(void* dst, const void* src, int64_t bytes, void* stream) {
+  if (bytes < 0 || (bytes > 0 && (!dst || !src))) return fail(SK_ERR_ARG, "bad argument");
+  if (bytes == 0) return SK_OK;
+  return cuda_status(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDeviceToHost, static_cast<cudaStream_t>(stream)),
+                     "cudaMemcpyAsync D2H");
+}
+
+int sk_stream_synchronize(void* stream) {
+  return cuda_status(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)), "cudaStreamSynchronize");
+}
+
 int sk_launch_config(const sk_basis* b, int op, int64_t out[3]) {
+  return sk_launch_config_geo(b, op, SK_GEO_DEFORMED, out);
+}
+
+int sk_launch_config_geo(const sk_basis* b, int op, int geo_class, int64_t out[3]) {
   if (!b || !out || op < 0 || op >= sk::OP_COUNT) return fail(SK_ERR_ARG, "bad argument");
-  b->ops->config(op, out);
+  if (geo_class != SK_GEO_REGULAR && geo_class != SK_GEO_DEFORMED) return fail(SK_ERR_ARG, "bad geometry class");
+  b->ops->config(op, geo_class, out);  // SK_GEO_* == sk::GEO_* (0 regular, 1 deformed)
   return SK_OK;
 }
 

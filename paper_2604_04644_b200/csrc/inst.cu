@@ -11,6 +11,7 @@
 #include <cstring>
 #include <mutex>
 
+#include "sk_dense.cuh"
 #include "sk_ops.cuh"
 #include "sk_opset.hpp"
 #include "sk_tune.h"
@@ -283,6 +284,46 @@ static int go(const Args& a, const LaunchReq& r, int gy, void* stream) {
   return (int)cudaGetLastError();
 }
 
+// StdMat mass on DMMA (sk_dense.cuh): persistent warps over 8-element groups
+template <int S, int P, int PW>
+int launch_dense(const LaunchReq& r, void* stream) {
+  DenseArgs a;
+  a.frag = r.dense;
+  a.in = r.in;
+  a.out = r.out;
+  a.pay = r.pay;
+  a.E = r.E;
+  a.Epad = r.Epad;
+  a.in_cstride = r.in_cs;
+  a.out_cstride = r.out_cs;
+  a.W = r.W;
+  using X = DenseDims<S, P>;
+  const long long groups = (r.Epad + 7) / 8;
+  if (groups == 0) return 0;
+  auto kern = r.geo == GEO_DEFORMED ? k_mass_dense<S, P, PW, GEO_DEFORMED> : k_mass_dense<S, P, PW, GEO_REGULAR>;
+  const int smem = (r.geo == GEO_DEFORMED ? X::F1 + X::F2 : X::FR) * 8;
+  static std::once_flag once;
+  static int per_sm[2] = {1, 1}, sms = 148;
+  std::call_once(once, [&] {
+    for (int g = 0; g < 2; ++g) {
+      auto k = g ? k_mass_dense<S, P, PW, GEO_DEFORMED> : k_mass_dense<S, P, PW, GEO_REGULAR>;
+      const int sb = (g ? X::F1 + X::F2 : X::FR) * 8;
+      ensure_smem(k, sb);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[g], k, kDenseThreads, sb);
+      if (per_sm[g] < 1) per_sm[g] = 1;
+    }
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  });
+  const int gy = r.ncomp > 0 ? r.ncomp : 1;
+  const long long resident = (long long)per_sm[r.geo == GEO_DEFORMED] * sms / gy;
+  const long long need = (groups + kDenseThreads / 32 - 1) / (kDenseThreads / 32);
+  long long grid = need < resident ? need : (resident > 0 ? resident : 1);
+  kern<<<dim3((unsigned)grid, (unsigned)gy), kDenseThreads, smem, static_cast<cudaStream_t>(stream)>>>(a);
+  return (int)cudaGetLastError();
+}
+
 template <int S, int P>
 int launch_nc(const LaunchReq& r, void* stream) {
   NcArgs<S, P> a;
@@ -357,6 +398,10 @@ int launch(int op, const LaunchReq& r, void* stream) {
 #if !defined(SK_ONLY_OP) || SK_ONLY_OP == 1
     case OP_MASS: {
       using C = Cfg<S, P, OP_MASS>;
+      if (r.dense) {
+        if constexpr (P <= kDenseMaxP) return launch_dense<S, P, C::PW>(r, stream);
+        return (int)cudaErrorInvalidValue;
+      }
       if (def) return go<S, P, OP_MASS, k_mass<S, P, typename C::L, C::NT, C::PW, GEO_DEFORMED, C::MINB>>(a, r, r.ncomp, stream);
       return go<S, P, OP_MASS, k_mass<S, P, typename C::L, C::NT, C::PW, GEO_REGULAR, C::MINB>>(a, r, r.ncomp, stream);
     }
@@ -387,7 +432,13 @@ int launch(int op, const LaunchReq& r, void* stream) {
 }
 
 template <int S, int P>
-void config(int op, int64_t out[3]) {
+void config(int op, int geo, int64_t out[3]) {
+  if (op == OP_HELM && geo == GEO_REGULAR) {  // the regular collocated Helmholtz has its own tile
+    out[0] = Cfg<S, P, OP_HELM, true>::EB;
+    out[1] = Cfg<S, P, OP_HELM, true>::NT;
+    out[2] = Cfg<S, P, OP_HELM, true>::SMEM;
+    return;
+  }
   switch (op) {
 #define SK_CFG(OPV)                    \
   case OPV:                            \
@@ -665,7 +716,9 @@ const OpSet* opset_impl() {
                             &payload_doubles<S, P>,
                             &payload_elements<S, P>,
                             &pack<S, P>,
-                            &geometry<S, P>};
+                            &geometry<S, P>,
+                            P <= kDenseMaxP ? DenseDims<S, P>::DOUBLES : 0,
+                            &fill_dense_frags<S, P>};
   return &ops;
 }
 

@@ -1,0 +1,171 @@
+// StdMat mass on the FP64 tensor cores (DMMA, mma.sync.m8n8k4.f64): the
+// reference's dense strategy (_stdmat_apply with the dense basis matrix,
+// speckern/operators.py:398-405; bmat shapes.py:491-492) as element-batched
+// GEMMs, for the low orders where the paper found StdMat fastest for simplex
+// mass.
+//
+// Deformed:  out_e = B^T diag(wJ_e) B uhat_e, per warp a group of 8 elements:
+//   GEMM1  U^T (8 x NQ) = Uhat^T (8 x NM) . B^T (NM x NQ)    A = Uhat^T (global)
+//   V^T = U^T o W^T (wJ from the W payload, per element and point)
+//   GEMM2  out^T (8 x NM) = V^T (8 x NQ) . B (NQ x NM)         A = V^T (registers)
+// processed point tile by point tile (8 points): GEMM1's accumulator of a
+// tile becomes GEMM2's A operand of two k-steps through four quad shuffles,
+// so U never leaves registers.
+// Regular:   out_e = |J|_e M_ref uhat_e with M_ref = B^T diag(refw) B (one
+//   NM x NM matrix per basis): one GEMM, 2 NM^2 multiply-adds per element.
+//
+// B / M_ref operand fragments live in shared memory in fragment order
+// (one conflict-free 8-byte load per lane per DMMA); the fragments are built
+// once per basis and device (abi.cu device_dense) from the dense B that the
+// sum-factorised bwd_trans kernel produces on unit coefficient vectors.
+// Persistent CTAs: every warp strides over 8-element groups, no CTA barrier
+// after the fragment copy.
+#pragma once
+
+#include <vector>
+
+#include "sk_common.cuh"
+
+namespace sk {
+
+template <int S, int P>
+struct DenseDims {
+  using Dm = Dims<S, P>;
+  static constexpr int NQ = Dm::NQ, NM = Dm::NM;
+  static constexpr int NQP = (NQ + 7) / 8 * 8;   // points, padded to the 8-row tiles
+  static constexpr int NMP4 = (NM + 3) / 4 * 4;  // modes as a k dimension
+  static constexpr int NMP8 = (NM + 7) / 8 * 8;  // modes as an n dimension
+  static constexpr int NT = NQP / 8;             // point tiles
+  static constexpr int KS1 = NMP4 / 4;           // GEMM1 k-steps
+  static constexpr int MT = NMP8 / 8;            // output mode tiles
+  static constexpr int F1 = NT * KS1 * 32;       // GEMM1 B fragments: B^T[k = m][n = q]
+  static constexpr int F2 = 2 * NT * MT * 32;    // GEMM2 B fragments: B[k = q][n = m]
+  static constexpr int FR = KS1 * MT * 32;       // regular: M_ref[k][n]
+  static constexpr int DOUBLES = F1 + F2 + FR;
+};
+
+// host: fragment tables from the dense B (NQ x NM row-major) and refw
+template <int S, int P>
+void fill_dense_frags(const double* B, const double* refw, double* f) {
+  using X = DenseDims<S, P>;
+  auto b = [&](int q, int m) { return (q < X::NQ && m < X::NM) ? B[q * X::NM + m] : 0.0; };
+  double* f1 = f;
+  double* f2 = f + X::F1;
+  double* fr = f + X::F1 + X::F2;
+  for (int nt = 0; nt < X::NT; ++nt)
+    for (int ks = 0; ks < X::KS1; ++ks)
+      for (int l = 0; l < 32; ++l) f1[(nt * X::KS1 + ks) * 32 + l] = b(8 * nt + (l >> 2), 4 * ks + (l & 3));
+  for (int ks = 0; ks < 2 * X::NT; ++ks)
+    for (int mt = 0; mt < X::MT; ++mt)
+      for (int l = 0; l < 32; ++l) f2[(ks * X::MT + mt) * 32 + l] = b(4 * ks + (l & 3), 8 * mt + (l >> 2));
+  // M_ref = B^T diag(refw) B
+  std::vector<double> M((size_t)X::NM * X::NM, 0.0);
+  for (int i = 0; i < X::NM; ++i)
+    for (int j = 0; j < X::NM; ++j) {
+      double s = 0.0;
+      for (int q = 0; q < X::NQ; ++q) s += B[q * X::NM + i] * refw[q] * B[q * X::NM + j];
+      M[(size_t)i * X::NM + j] = s;
+    }
+  for (int ks = 0; ks < X::KS1; ++ks)
+    for (int mt = 0; mt < X::MT; ++mt)
+      for (int l = 0; l < 32; ++l) {
+        const int k = 4 * ks + (l & 3), n = 8 * mt + (l >> 2);
+        fr[(ks * X::MT + mt) * 32 + l] = (k < X::NM && n < X::NM) ? M[(size_t)k * X::NM + n] : 0.0;
+      }
+}
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+struct DenseArgs {
+  const double* __restrict__ frag;  // DenseDims::DOUBLES (device)
+  const double* __restrict__ in;
+  double* __restrict__ out;
+  const double* __restrict__ pay;   // W payload (deformed wJ per point / regular |J|)
+  long long E, Epad, in_cstride, out_cstride;
+  int W;
+};
+
+constexpr int kDenseThreads = 256;
+
+template <int S, int P, int PW, int GEO>
+__global__ void __launch_bounds__(kDenseThreads) k_mass_dense(const __grid_constant__ DenseArgs A) {
+  using X = DenseDims<S, P>;
+  constexpr int NQ = X::NQ, NM = X::NM, KS1 = X::KS1, MT = X::MT;
+  extern __shared__ double sfr[];
+  // fragments this geometry class reads: GEMM1 + GEMM2 (deformed) or M_ref
+  constexpr int OFF = GEO == GEO_DEFORMED ? 0 : X::F1 + X::F2;
+  constexpr int NF = GEO == GEO_DEFORMED ? X::F1 + X::F2 : X::FR;
+  for (int i = threadIdx.x; i < NF / 2; i += kDenseThreads)
+    reinterpret_cast<double2*>(sfr)[i] = __ldg(reinterpret_cast<const double2*>(A.frag + OFF) + i);
+  __syncthreads();
+  const double* f1 = sfr;
+  const double* f2 = sfr + X::F1;
+  const int lane = threadIdx.x & 31, t = lane & 3, r = lane >> 2;
+  const long long warps = (long long)gridDim.x * (kDenseThreads / 32);
+  const double* src = A.in + blockIdx.y * A.in_cstride;
+  double* dst = A.out + blockIdx.y * A.out_cstride;
+  const long long ngroups = (A.Epad + 7) / 8;
+  for (long long g = blockIdx.x * (kDenseThreads / 32) + (threadIdx.x >> 5); g < ngroups; g += warps) {
+    const long long e = g * 8 + r;  // this lane's element (A-operand row = C row)
+    const bool live = e < A.E;
+    const long long base = lane_base(live ? e : 0, NM, A.W);
+    double a[KS1];
+#pragma unroll
+    for (int ks = 0; ks < KS1; ++ks) {
+      const int m = 4 * ks + t;
+      a[ks] = (live && m < NM) ? __ldcs(src + base + (long long)m * A.W) : 0.0;
+    }
+    double c[MT][2];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) c[mt][0] = c[mt][1] = 0.0;
+    if constexpr (GEO == GEO_DEFORMED) {
+      const double* wp = A.pay + pay_base<PW>(live ? e : 0, 1, NQ);
+      const int s1 = (lane & ~3) | (t >> 1), s2 = s1 + 2;
+#pragma unroll
+      for (int nt = 0; nt < X::NT; ++nt) {
+        double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < KS1; ++ks) dmma(d0, d1, a[ks], f1[(nt * KS1 + ks) * 32 + lane]);
+        const int q0 = 8 * nt + 2 * t;
+        const double w0 = (live && q0 < NQ) ? __ldcs(wp + (long long)q0 * PW) : 0.0;
+        const double w1 = (live && q0 + 1 < NQ) ? __ldcs(wp + (long long)(q0 + 1) * PW) : 0.0;
+        const double v0 = d0 * w0, v1 = d1 * w1;
+        // V^T[r][8nt + t] and V^T[r][8nt + 4 + t] from the quad's accumulators
+        const double x0 = __shfl_sync(0xffffffffu, v0, s1), x1 = __shfl_sync(0xffffffffu, v1, s1);
+        const double y0 = __shfl_sync(0xffffffffu, v0, s2), y1 = __shfl_sync(0xffffffffu, v1, s2);
+        const double alo = (t & 1) ? x1 : x0, ahi = (t & 1) ? y1 : y0;
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          dmma(c[mt][0], c[mt][1], alo, f2[((2 * nt) * MT + mt) * 32 + lane]);
+          dmma(c[mt][0], c[mt][1], ahi, f2[((2 * nt + 1) * MT + mt) * 32 + lane]);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int ks = 0; ks < KS1; ++ks) dmma(c[mt][0], c[mt][1], a[ks], sfr[(ks * MT + mt) * 32 + lane]);
+      const double jac = live ? __ldg(A.pay + pay_base<PW>(e, 1, 1)) : 0.0;
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        c[mt][0] *= jac;
+        c[mt][1] *= jac;
+      }
+    }
+    if (e < A.Epad) {
+      const long long ob = lane_base(e, NM, A.W);
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        const int m = 8 * mt + 2 * t;
+        if (m < NM) __stcs(dst + ob + (long long)m * A.W, live ? c[mt][0] : 0.0);
+        if (m + 1 < NM) __stcs(dst + ob + (long long)(m + 1) * A.W, live ? c[mt][1] : 0.0);
+      }
+    }
+  }
+}
+
+}  // namespace sk

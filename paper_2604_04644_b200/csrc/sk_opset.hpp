@@ -23,6 +23,7 @@ struct LaunchReq {
   int W, ncomp, geo;
   double lam;
   int c0_nx = 0, c0_ny = 0;  // > 0: assembled C0 hex slab, `in` is the global DOF vector
+  const double* dense = nullptr;  // mass only: DMMA StdMat fragments (sk_dense.cuh) -> dense kernel
 };
 
 struct OpSet {
@@ -33,7 +34,7 @@ struct OpSet {
   void (*fill_gtab)(const HostBasis& hb, double* gtab_host);
   // returns a cudaError_t value (0 = success)
   int (*launch)(int op, const LaunchReq& r, void* stream);
-  void (*config)(int op, int64_t out[3]);
+  void (*config)(int op, int geo, int64_t out[3]);  // geo: GEO_REGULAR / GEO_DEFORMED
   // payload kinds: 0 HELMHOLTZ (k-major), 1 W, 2 DERIV, 3 HELMHOLTZ (standard order)
   long long (*payload_doubles)(int kind, int geo);  // per element
   long long (*payload_elements)(int kind, long long E);  // elements incl. lane padding
@@ -44,6 +45,11 @@ struct OpSet {
   // (kind < 0: none).  Counts nonpositive-Jacobian points into *bad (device).
   int (*geometry)(int mode, long long E, const double* src, double* dxi, double* jac, int kind,
                   double* pay, unsigned long long* bad, const double* gtab, void* stream);
+  // dense (StdMat, DMMA) mass: fragment table size in doubles (0: not
+  // instantiated for this order) and its host fill from the dense basis
+  // matrix B (NQ x NM row-major) and the reference weights
+  int dense_doubles;
+  void (*fill_dense)(const double* B, const double* refw, double* frags);
 };
 
 template <int S, int P>

@@ -169,6 +169,16 @@ constexpr bool kPrismWP[3][11] = {
     {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},
 };
 
+// Mass by the StdMat strategy on the FP64 tensor cores (sk_dense.cuh)
+// instead of sum factorisation, per geometry class (0 regular, 1 deformed)
+// x shape x order; instantiated up to kDenseMaxP.  Run-time override:
+// SK_MASS_DENSE=0 (never) / 1 (wherever instantiated).
+constexpr int kDenseMaxP = 4;
+constexpr bool kDenseMass[2][4][11] = {
+    {{0}, {0}, {0}, {0}},
+    {{0}, {0}, {0}, {0}},
+};
+
 // Overrides for tuning builds (-DSK_EB_FIXED=... etc.) apply to every class.
 #ifdef SK_EB_FIXED
 SK_HD constexpr int tuned_eb(int, int, int) { return SK_EB_FIXED; }

@@ -80,8 +80,9 @@ class GeometricFactors:
     ``dxi_dx[..., i, j] = d xi_i / d x_j``: (E, 3, 3) regular, (E, NQ, 3, 3)
     deformed; ``jac``: |J| (E,) regular, w|J| (E, NQ) deformed.  Deformed
     factors may be held lazily as deformation parameters (``params``, E x 12)
-    and materialised on demand.  Device payloads are cached per (kind,
-    device) and are independent of the block's interleave width.
+    and materialised on demand.  Device payloads are cached per (basis
+    shape, order, kind, device) and are independent of the block's
+    interleave width.
     """
 
     def __init__(
@@ -147,7 +148,9 @@ class GeometricFactors:
         replaces Block.payload (field_block.py:309-363)."""
         torch = _torch()
         dev = torch.cuda.current_device()
-        key = (kind, dev)
+        # the payload layout (lane width, point count) depends on the basis:
+        # one regular GeometricFactors may serve bases of several orders
+        key = (basis.shape, basis.order, kind, dev)
         if key in self._payloads:
             return self._payloads[key]
         lib = _lib.load()

@@ -179,9 +179,12 @@ class ShapeBasis:
     def modes(self) -> tuple[tuple[int, ...], ...]:
         return tuple(tuple(int(v) for v in m) for m in self.table("modes").reshape(-1, 3))
 
-    def launch_config(self, op: int) -> tuple[int, int, int]:
+    def launch_config(self, op: int, deformed: bool = True) -> tuple[int, int, int]:
+        """(elements per CTA, threads per CTA, dynamic shared bytes) of the
+        kernel an operator launches for this basis and geometry class."""
         out = (ctypes.c_int64 * 3)()
-        _lib.check(_lib.load().sk_launch_config(self.handle, op, out), "sk_launch_config")
+        geo = _lib.SK_GEO_DEFORMED if deformed else _lib.SK_GEO_REGULAR
+        _lib.check(_lib.load().sk_launch_config_geo(self.handle, op, geo, out), "sk_launch_config_geo")
         return int(out[0]), int(out[1]), int(out[2])
 
 

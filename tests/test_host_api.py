@@ -151,4 +151,15 @@ def test_bench_reference_arm_contract():
     for key in ("metric", "value", "unit", "impl", "cpu_baseline", "e2e", "config", "higher_is_better"):
         assert key in line
     assert line["impl"] == "reference" and line["value"] > 0
-    assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
+    # the unmodified reference (baseline/_ref) when installed, else the oracle port
+    want = "reference" if os.path.isdir(os.path.join(ROOT, "baseline", "_ref", "speckern")) else "port"
+    assert line["cpu_baseline"]["kind"] == want and line["cpu_baseline"]["cores"] >= 1
+
+
+def test_bench_rank_count_must_match_gpus():
+    """--gpus N inside a launcher that started a different rank count fails
+    loudly instead of reporting the wrong n_gpus."""
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "1"],
+                         capture_output=True, text=True, env=env, timeout=120)
+    assert out.returncode != 0 and "WORLD_SIZE=1" in out.stderr

@@ -120,6 +120,50 @@ def test_oracle_ragged_tiles(sk, shape, P, width):
 
 
 @pytest.mark.parametrize("shape", SHAPES)
+@pytest.mark.parametrize("P", [1, 3, 5, 6, 8, 10])
+def test_regular_multi_tile_every_order(sk, shape, P):
+    """Regular-geometry collocated Helmholtz / stiffness on several CTA tiles
+    at the orders whose regular launch table (tile width, thread divisor)
+    differs from the deformed one: every element against the oracle."""
+    n = 301
+    el = O.element(shape, P)
+    blk = _block(sk, shape, P, False, n, 11, 1)
+    geo = O.synthetic_geometry(el, False, n, seed=11)
+    x = O.bench_coeffs(O.SHAPE_INDEX[shape], P, el.nm, n, seed=11)
+    blk.set_elements(x[None])
+    eb, nt, _ = blk.basis.launch_config(0, deformed=False)
+    assert n > 4 * eb  # several tiles
+    for lam in (0.0, 1.7):
+        got = sk.helmholtz_apply(blk, lam).get_elements()[0]
+        assert _err(got, O.helmholtz_coll(el, geo, x, lam)) <= TOL, (lam, eb, nt)
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+def test_regular_factors_shared_by_two_orders(sk, shape):
+    """One regular GeometricFactors serving bases of two orders (the
+    reference's affine factors do not depend on the order): each order gets
+    its own payload (lane widths differ), results match the oracle."""
+    n = 40
+    from paper_2604_04644_b200.geometry import synthetic_affine_vertices
+
+    verts = synthetic_affine_vertices(sk.Shape(shape), n, 4)
+    fac = sk.make_affine_block(sk.Shape(shape), verts)
+    geo = O.affine_geometry(shape, verts)
+    for P in (1, 3, 2):
+        el = O.element(shape, P)
+        b = sk.build_shape_basis(sk.Shape(shape), P)
+        blk = sk.Block(b, fac, sk.FieldState.COEFF, 1, 1)
+        x = O.bench_coeffs(O.SHAPE_INDEX[shape], P, el.nm, n, seed=P)
+        blk.set_elements(x[None])
+        assert _err(sk.helmholtz_apply_noncoll(blk, 1.0).get_elements()[0], O.helmholtz_noncoll(el, geo, x, 1.0)) <= TOL
+        assert _err(sk.helmholtz_apply(blk, 1.0).get_elements()[0], O.helmholtz_coll(el, geo, x, 1.0)) <= TOL
+        pb = blk.like(sk.FieldState.PHYS)
+        y = np.random.default_rng(P).uniform(-1, 1, (el.nq, n))
+        pb.set_elements(y[None])
+        assert _err(sk.phys_deriv(pb).get_elements(), O.phys_deriv(el, geo, y)) <= TOL
+
+
+@pytest.mark.parametrize("shape", SHAPES)
 def test_padding_lanes_stay_zero(sk, shape):
     """Padded lanes of the lane-major layout are written as zeros
     (reference acceptance criterion 9)."""
@@ -245,3 +289,46 @@ def test_persistent_tiles_at_scale(sk, shape, P, n, width):
     blk.device()
     got = sk.helmholtz_apply(blk, 0.7).get_elements()[0]
     assert _err(got, O.helmholtz_coll(el, geo, x, 0.7)) <= TOL
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+@pytest.mark.parametrize("P", [1, 2, 3, 4])
+@pytest.mark.parametrize("width", [1, 8])
+def test_dense_dmma_mass(sk, monkeypatch, shape, P, width):
+    """StdMat mass on the FP64 tensor cores (sk_dense.cuh, forced with
+    SK_MASS_DENSE=1) against the oracle's sum-factorised mass on every
+    element: ragged 8-element groups, interleave widths, two components,
+    both geometry classes (regular: |J| M_ref)."""
+    monkeypatch.setenv("SK_MASS_DENSE", "1")
+    n = 157
+    el = O.element(shape, P)
+    for deformed in (False, True):
+        blk = _block(sk, shape, P, deformed, n, 9, width, ncomp=2)
+        geo = O.synthetic_geometry(el, deformed, n, seed=9)
+        x = np.random.default_rng(P).uniform(-1, 1, (2, el.nm, n))
+        blk.set_elements(x)
+        got = sk.mass_apply(blk)
+        for c in range(2):
+            assert _err(got.get_elements()[c], O.mass(el, geo, x[c])) <= TOL, (deformed, c)
+        # padded lanes of the last group stay zero
+        h = got.host().reshape(2, -1, el.nm, width)
+        if n % width:
+            assert not np.any(h[:, -1, :, n % width:])
+
+
+def test_dense_mass_streamed_and_forced_off(sk, monkeypatch):
+    """The streamed host path takes the dense kernel too; SK_MASS_DENSE=0
+    (sum factorisation) gives the same result to 1e-12."""
+    from paper_2604_04644_b200 import operators as ops
+
+    b = sk.build_shape_basis(sk.Shape.TET, 2)
+    n = ops.STREAM_MIN_BYTES // (8 * b.n_modes) + 333
+    fac = sk.make_synthetic_factors(b, sk.GeometryClass.DEFORMED, n, seed=2)
+    x = np.random.default_rng(1).uniform(-1, 1, (1, b.n_modes, n))
+    res = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("SK_MASS_DENSE", flag)
+        blk = sk.Block(b, fac, sk.FieldState.COEFF, 1, 1)
+        blk.set_elements(x)
+        res[flag] = sk.mass_apply(blk).get_elements()
+    assert _err(res["1"], res["0"]) <= TOL

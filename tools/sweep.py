@@ -92,7 +92,7 @@ def main():
         sec = t0.elapsed_time(t1) / 1e3 / a.reps
         gdof = b.n_modes * E / sec / 1e9
         flops = sk.operator_flops(kind, sk.Shape(s), P) * E
-        cfg = b.launch_config({"mass": 1, "helmnc": 6}.get(op, 0))
+        cfg = b.launch_config({"mass": 1, "helmnc": 6}.get(op, 0), deformed)
         rec = {
             "op": op, "shape": s, "P": P, "geo": a.geo, "elements": E, "ms": sec * 1e3, "gdof_s": gdof,
             "hbm_gbs": bel * E / sec / 1e9, "hbm_frac": bel * E / sec / 1e9 / hbm,
