@@ -113,6 +113,18 @@ int sk_mass_apply(const sk_basis* b, int geo_class, int64_t E, int W, int ncomp,
 int sk_helmholtz_apply(const sk_basis* b, int geo_class, int form, int64_t E, int W, int ncomp,
                        const double* uhat, const double* hpay, double lam, double* out, void* stream);
 
+/* Staged collocated Helmholtz (deformed geometry): the fused kernel split
+ * into BwdTrans -> quadrature-point kernel (collocation sweeps, metric,
+ * transposed sweeps, lam W u) -> unweighted B^T, run over element chunks so
+ * the two NQ-sized intermediates stay L2-resident.  Same payload and
+ * results as sk_helmholtz_apply(SK_FORM_COLL); the fused-vs-staged choice per
+ * (shape, order) is made from measurements.  work: device
+ * buffer of 2 * chunk * n_points doubles; chunk: elements per chunk, a
+ * positive multiple of lcm(16, W). */
+int sk_helmholtz_apply_staged(const sk_basis* b, int geo_class, int64_t E, int W, int ncomp, const double* uhat,
+                              const double* hpay, double lam, double* out, double* work, int64_t chunk,
+                              void* stream);
+
 /* ---- host-buffer applies with transfer/compute overlap ----------------------
  * The reference's callers hold their blocks in host memory (field_block.py:
  * 67-149 MemoryRegion HOST space).  sk_apply_streamed runs a coefficient ->

@@ -160,7 +160,7 @@ const double* device_dense(sk_basis* b, void* stream, int* status) {
 // StdMat (DMMA) or sum-factorised mass for this basis and geometry class:
 // the tuned table, overridden by SK_MASS_DENSE=0/1
 bool use_dense_mass(const sk_basis* b, int geo) {
-  if (b->ops->dense_doubles <= 0) return false;
+  if (b->ops->dense_doubles <= 0 || !(b->ops->dense_mask & (geo == SK_GEO_DEFORMED ? 2 : 1))) return false;
   if (const char* v = std::getenv("SK_MASS_DENSE")) {
     if (v[0] == '0') return false;
     if (v[0] == '1') return true;
@@ -390,6 +390,68 @@ int sk_helmholtz_apply(const sk_basis* b, int geo, int form, int64_t E, int W, i
   if (int st = check_layout(E, W, ncomp)) return st;
   return run(const_cast<sk_basis*>(b), form == SK_FORM_NONCOLL ? sk::OP_HELM_NC : sk::OP_HELM, geo, E, W, ncomp, uhat,
              out, hpay, lam, b->hb.nm, b->hb.nm, stream);
+}
+
+int sk_helmholtz_apply_staged(const sk_basis* b, int geo, int64_t E, int W, int ncomp, const double* uhat,
+                              const double* hpay, double lam, double* out, double* work, int64_t chunk,
+                              void* stream) {
+  if (!b || (E > 0 && (!uhat || !hpay || !out || !work))) return fail(SK_ERR_ARG, "null argument");
+  if (geo != SK_GEO_DEFORMED) return fail(SK_ERR_UNSUPPORTED, "the staged variant is built for deformed geometry");
+  if (!(lam >= 0.0)) return fail(SK_ERR_ARG, "reaction coefficient must be nonnegative");
+  if (int st = check_layout(E, W, ncomp)) return st;
+  // chunks start on a multiple of the interleave width and of 16 (tile and
+  // payload lane widths divide 16)
+  long long unit = 16;
+  while (unit % W) unit += 16;
+  if (chunk < unit || chunk % unit) return fail(SK_ERR_ARG, "chunk must be a positive multiple of lcm(16, W)");
+  const long long Epad = padded(E, W);
+  if (Epad == 0) return SK_OK;
+  int st = SK_OK;
+  sk_basis* bb = const_cast<sk_basis*>(b);
+  const double* g = device_gtab(bb, &st);
+  if (st) return st;
+  const long long nm = b->hb.nm, nq = b->hb.nq, per_el = b->ops->payload_doubles(SK_PAYLOAD_HELMHOLTZ, geo);
+  double* w0 = work;
+  double* w1 = work + chunk * nq;
+  sk::LaunchReq r;
+  r.fwd = b->fwd_vals.data();
+  r.fwd_d = b->fwd_ders.data();
+  r.dtab = b->dtab.data();
+  r.gtab = g;
+  r.W = W;
+  r.ncomp = 1;
+  r.geo = geo;
+  r.lam = lam;
+  for (int c = 0; c < ncomp; ++c) {
+    for (long long e0 = 0; e0 < Epad; e0 += chunk) {
+      const long long e1 = std::min<long long>(Epad, e0 + chunk);
+      r.E = std::max<long long>(0, std::min<long long>(E, e1) - e0);
+      r.Epad = e1 - e0;
+      // BwdTrans -> u
+      r.in = uhat + c * Epad * nm + e0 * nm;
+      r.out = w0;
+      r.pay = nullptr;
+      r.in_cs = r.Epad * nm;
+      r.out_cs = r.Epad * nq;
+      g_launches.fetch_add(3, std::memory_order_relaxed);
+      int e = b->ops->launch(sk::OP_BWD, r, stream);
+      // quadrature-point Helmholtz -> u'
+      r.in = w0;
+      r.out = w1;
+      r.pay = hpay + e0 * per_el;  // chunks start on a payload lane group
+      r.in_cs = r.out_cs = r.Epad * nq;
+      if (e == 0) e = b->ops->launch(sk::OP_QP, r, stream);
+      // B^T -> out
+      r.in = w1;
+      r.out = out + c * Epad * nm + e0 * nm;
+      r.pay = nullptr;
+      r.in_cs = r.Epad * nq;
+      r.out_cs = r.Epad * nm;
+      if (e == 0) e = b->ops->launch(sk::OP_BT, r, stream);
+      if (e) return cuda_status(e, "staged kernel launch");
+    }
+  }
+  return SK_OK;
 }
 
 namespace {

@@ -45,7 +45,7 @@ struct Mode {
   // regular-geometry collocated Helmholtz tile width (its payload lane
   // width is kRegPW, independent of the tile)
   static constexpr int EBHR = tuned_eb_regular(S, P) > 0 ? fit(tuned_eb_regular(S, P), 200 * 1024) : EBH;
-  SK_HD static constexpr int eb(int op) { return (op == OP_HELM || op == OP_HELM_NC || op == OP_PDERIV) ? EBH : EBW; }
+  SK_HD static constexpr int eb(int op) { return (op == OP_HELM || op == OP_HELM_NC || op == OP_PDERIV || op == OP_QP) ? EBH : EBW; }
 };
 
 template <int S, int P, int OP, bool REG = false>
@@ -53,14 +53,20 @@ struct Cfg {
   using Dm = Dims<S, P>;
   static constexpr int EB = REG ? Mode<S, P>::EBHR : Mode<S, P>::eb(OP);
   static constexpr int PW = EB;
-  static constexpr int planes = OP == OP_HELM_NC ? 5 : (OP == OP_HELM || OP == OP_PDERIV || OP == OP_IPDERIV) ? 3 : 2;
+  static constexpr int planes = OP == OP_HELM_NC ? 5 : (OP == OP_HELM || OP == OP_PDERIV || OP == OP_IPDERIV || OP == OP_QP) ? 3 : 2;
   static constexpr int items = cmax(cmax(cmax(Dm::Q1 * Dm::Q2, Dm::Q0 * Dm::Q2), cmax(Dm::Q0 * Dm::Q1, Dm::P1 * Dm::P1)),
                                     cmax(Dm::NPAIR, Dm::P1 * Dm::Q2));
   using L = Lay<S, P, planes, EB>;
-  static constexpr int CLS = OP == OP_HELM ? 0 : OP == OP_MASS ? 1 : 2;
+  static constexpr int CLS = (OP == OP_HELM || OP == OP_QP) ? 0 : OP == OP_MASS ? 1 : 2;
   static constexpr int NT0 = ((EB * items / (REG ? tuned_nt_div_regular(S, P) : tuned_nt_div(CLS, S, P)) + 31) / 32) * 32;
   static constexpr int NT = NT0 > 512 ? 512 : (NT0 < 64 ? 64 : NT0);
-  static constexpr int SMEM = (smem_tables(CLS, S, P) ? L::TABOFF + GLayout<S, P>::RAGGED : L::SMEM_DOUBLES) * 8;
+  // deformed Helmholtz: TMA geometry ring after the planes (sk_tune.h kGeoRing)
+  static constexpr int RING = (OP == OP_HELM && !REG && geo_ring(S, P) > 0 && EB * Dm::Q0 * Dm::Q1 <= NT &&
+                               (Dm::Q0 * Dm::Q1 * EB) % 2 == 0 && !tuned_persist(0, S, P))
+                                  ? geo_ring(S, P)
+                                  : 0;
+  static constexpr int SMEM0 = (smem_tables(CLS, S, P) ? L::TABOFF + GLayout<S, P>::RAGGED : L::SMEM_DOUBLES) * 8;
+  static constexpr int SMEM = RING ? (SMEM0 + 15) / 16 * 16 + RING * (7 * Dm::Q0 * Dm::Q1 * EB * 8 + 16) : SMEM0;
   // __launch_bounds__ min blocks: 1, or the CTAs per SM that shared memory
   // allows (forces ptxas to fit the registers; tuned, as it can spill)
   static constexpr int MINB = tuned_minb(CLS, S, P) ? cmax(1, cmin(cmin(tuned_minb_cap(CLS, S, P), (220 * 1024) / (SMEM + 1024)), 2048 / NT))
@@ -285,6 +291,36 @@ static int go(const Args& a, const LaunchReq& r, int gy, void* stream) {
 }
 
 // StdMat mass on DMMA (sk_dense.cuh): persistent warps over 8-element groups
+template <int S, int P, int PW, int GEO>
+int launch_dense_geo(const DenseArgs& a, int ncomp, void* stream) {
+  using X = DenseDims<S, P>;
+  constexpr int BIT = GEO == GEO_DEFORMED ? 2 : 1;
+  if constexpr (!(X::MASK & BIT)) {
+    return (int)cudaErrorInvalidValue;  // fragments would not fit in shared memory: never selected
+  } else {
+    constexpr int smem = (GEO == GEO_DEFORMED ? X::F1 + X::F2 : X::FR) * 8;
+    auto kern = k_mass_dense<S, P, PW, GEO>;
+    static std::once_flag once;
+    static int per_sm = 1, sms = 148;
+    std::call_once(once, [&] {
+      ensure_smem(kern, smem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kDenseThreads, smem);
+      if (per_sm < 1) per_sm = 1;
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    });
+    const long long groups = (a.Epad + 7) / 8;
+    if (groups == 0) return 0;
+    const int gy = ncomp > 0 ? ncomp : 1;
+    const long long resident = (long long)per_sm * sms / gy;
+    const long long need = (groups + kDenseThreads / 32 - 1) / (kDenseThreads / 32);
+    const long long grid = need < resident ? need : (resident > 0 ? resident : 1);
+    kern<<<dim3((unsigned)grid, (unsigned)gy), kDenseThreads, smem, static_cast<cudaStream_t>(stream)>>>(a);
+    return (int)cudaGetLastError();
+  }
+}
+
 template <int S, int P, int PW>
 int launch_dense(const LaunchReq& r, void* stream) {
   DenseArgs a;
@@ -297,31 +333,8 @@ int launch_dense(const LaunchReq& r, void* stream) {
   a.in_cstride = r.in_cs;
   a.out_cstride = r.out_cs;
   a.W = r.W;
-  using X = DenseDims<S, P>;
-  const long long groups = (r.Epad + 7) / 8;
-  if (groups == 0) return 0;
-  auto kern = r.geo == GEO_DEFORMED ? k_mass_dense<S, P, PW, GEO_DEFORMED> : k_mass_dense<S, P, PW, GEO_REGULAR>;
-  const int smem = (r.geo == GEO_DEFORMED ? X::F1 + X::F2 : X::FR) * 8;
-  static std::once_flag once;
-  static int per_sm[2] = {1, 1}, sms = 148;
-  std::call_once(once, [&] {
-    for (int g = 0; g < 2; ++g) {
-      auto k = g ? k_mass_dense<S, P, PW, GEO_DEFORMED> : k_mass_dense<S, P, PW, GEO_REGULAR>;
-      const int sb = (g ? X::F1 + X::F2 : X::FR) * 8;
-      ensure_smem(k, sb);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[g], k, kDenseThreads, sb);
-      if (per_sm[g] < 1) per_sm[g] = 1;
-    }
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  });
-  const int gy = r.ncomp > 0 ? r.ncomp : 1;
-  const long long resident = (long long)per_sm[r.geo == GEO_DEFORMED] * sms / gy;
-  const long long need = (groups + kDenseThreads / 32 - 1) / (kDenseThreads / 32);
-  long long grid = need < resident ? need : (resident > 0 ? resident : 1);
-  kern<<<dim3((unsigned)grid, (unsigned)gy), kDenseThreads, smem, static_cast<cudaStream_t>(stream)>>>(a);
-  return (int)cudaGetLastError();
+  if (r.geo == GEO_DEFORMED) return launch_dense_geo<S, P, PW, GEO_DEFORMED>(a, r.ncomp, stream);
+  return launch_dense_geo<S, P, PW, GEO_REGULAR>(a, r.ncomp, stream);
 }
 
 template <int S, int P>
@@ -387,8 +400,8 @@ int launch(int op, const LaunchReq& r, void* stream) {
         return (int)cudaErrorInvalidValue;
       }
       if (def) {
-        if (r.lam != 0.0) return go<S, P, OP_HELM, k_helm<S, P, typename C::L, C::NT, C::PW, GEO_DEFORMED, true, C::MINB>>(a, r, r.ncomp, stream);
-        return go<S, P, OP_HELM, k_helm<S, P, typename C::L, C::NT, C::PW, GEO_DEFORMED, false, C::MINB>>(a, r, r.ncomp, stream);
+        if (r.lam != 0.0) return go<S, P, OP_HELM, k_helm<S, P, typename C::L, C::NT, C::PW, GEO_DEFORMED, true, C::MINB, false, C::RING>>(a, r, r.ncomp, stream);
+        return go<S, P, OP_HELM, k_helm<S, P, typename C::L, C::NT, C::PW, GEO_DEFORMED, false, C::MINB, false, C::RING>>(a, r, r.ncomp, stream);
       }
       using CR = Cfg<S, P, OP_HELM, true>;  // regular geometry: own tile width
       if (r.lam != 0.0) return go<S, P, OP_HELM, k_helm<S, P, typename CR::L, CR::NT, CR::PW, GEO_REGULAR, true, CR::MINB>, CR>(a, r, r.ncomp, stream);
@@ -415,6 +428,16 @@ int launch(int op, const LaunchReq& r, void* stream) {
       using C = Cfg<S, P, OP_IPROD>;
       if (def) return go<S, P, OP_IPROD, k_iprod<S, P, typename C::L, C::NT, C::PW, GEO_DEFORMED, C::MINB>>(a, r, r.ncomp, stream);
       return go<S, P, OP_IPROD, k_iprod<S, P, typename C::L, C::NT, C::PW, GEO_REGULAR, C::MINB>>(a, r, r.ncomp, stream);
+    }
+    case OP_QP: {  // staged Helmholtz, quadrature-point kernel (deformed)
+      using C = Cfg<S, P, OP_QP>;
+      if (!def) return (int)cudaErrorInvalidValue;
+      if (r.lam != 0.0) return go<S, P, OP_QP, k_qp<S, P, typename C::L, C::NT, C::PW, GEO_DEFORMED, true, C::MINB>>(a, r, r.ncomp, stream);
+      return go<S, P, OP_QP, k_qp<S, P, typename C::L, C::NT, C::PW, GEO_DEFORMED, false, C::MINB>>(a, r, r.ncomp, stream);
+    }
+    case OP_BT: {  // staged Helmholtz, unweighted B^T
+      using C = Cfg<S, P, OP_BT>;
+      return go<S, P, OP_BT, k_iprod<S, P, typename C::L, C::NT, C::PW, GEO_UNIT, C::MINB>>(a, r, r.ncomp, stream);
     }
     case OP_PDERIV: {
       using C = Cfg<S, P, OP_PDERIV>;
@@ -453,6 +476,8 @@ void config(int op, int geo, int64_t out[3]) {
     SK_CFG(OP_PDERIV)
     SK_CFG(OP_IPDERIV)
     SK_CFG(OP_HELM_NC)
+    SK_CFG(OP_QP)
+    SK_CFG(OP_BT)
 #undef SK_CFG
   }
   out[0] = out[1] = out[2] = 0;
@@ -718,6 +743,7 @@ const OpSet* opset_impl() {
                             &pack<S, P>,
                             &geometry<S, P>,
                             P <= kDenseMaxP ? DenseDims<S, P>::DOUBLES : 0,
+                            P <= kDenseMaxP ? DenseDims<S, P>::MASK : 0,
                             &fill_dense_frags<S, P>};
   return &ops;
 }

@@ -9,7 +9,8 @@
 
 namespace sk {
 
-enum : int { GEO_REGULAR = 0, GEO_DEFORMED = 1 };
+enum : int { GEO_REGULAR = 0, GEO_DEFORMED = 1,
+             GEO_UNIT = 2 };  // no weight (the staged Helmholtz's final B^T)
 // lane width of the regular-geometry Helmholtz payload (8 doubles per
 // element): fixed, so the regular kernel's tile width is tuned on its own
 constexpr int kRegPW = 16;
@@ -212,6 +213,41 @@ __device__ __forceinline__ void dispatch(int v, F&& f) {
       dispatch<I + 1, N>(v, f);
     }
   }
+}
+
+// ---- mbarrier / TMA bulk-copy helpers (shared::cta barriers, 1D bulk copies)
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+// make barrier initialisation visible to the async (TMA) proxy
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+  unsigned ok = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+// global -> shared bulk copy (TMA, SASS UBLKCP) completing on barrier b;
+// 16-byte aligned addresses, size a multiple of 16
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(b))
+               : "memory");
 }
 
 // passes of a sweep's item loop unrolled together (independent items give

@@ -42,6 +42,9 @@ struct DenseDims {
   static constexpr int F2 = 2 * NT * MT * 32;    // GEMM2 B fragments: B[k = q][n = m]
   static constexpr int FR = KS1 * MT * 32;       // regular: M_ref[k][n]
   static constexpr int DOUBLES = F1 + F2 + FR;
+  // a geometry class's kernel exists when its fragments fit in 100 KB of
+  // shared memory (two CTAs per SM); bit 0 regular, bit 1 deformed
+  static constexpr int MASK = (FR * 8 <= 100 * 1024 ? 1 : 0) | ((F1 + F2) * 8 <= 100 * 1024 ? 2 : 0);
 };
 
 // host: fragment tables from the dense B (NQ x NM row-major) and refw

@@ -203,11 +203,36 @@ __device__ __forceinline__ void stage_tables(const double* __restrict__ gtab, do
 
 // ---------------------------------------------------------------------------
 // Helmholtz, collocated: 9 sweeps + coefficient tile staging, 10 CTA barriers
-template <int S, int P, class L, int NT_, int PW, int GEO, bool LAMW, int MINB_, bool C0 = false>
+template <int S, int P, class L, int NT_, int PW, int GEO, bool LAMW, int MINB_, bool C0 = false, int RING = 0>
 struct k_helm {
   static constexpr int NT = NT_;
   static constexpr int EB = L::EB;
   static constexpr int MINB = MINB_;
+  // TMA geometry ring (RING > 0 slots, sk_tune.h kGeoRing): slot s holds one
+  // k-slice [C][Q0*Q1][PW] of the tile's payload, after the work planes
+  // (and staged tables); then RING "full" and RING "empty" mbarriers
+  static constexpr int RING_C = LAMW ? 7 : 6;
+  static constexpr int RING_N = Dims<S, P>::Q0 * Dims<S, P>::Q1 * PW;  // doubles per component slice
+  static constexpr int RING_SLOT = RING_C * RING_N;
+  static constexpr int RING_OFF =
+      ((smem_tables(0, S, P) ? L::TABOFF + GLayout<S, P>::RAGGED : L::SMEM_DOUBLES) + 1) / 2 * 2;
+  static constexpr int RING_WARPS = (EB * Dims<S, P>::Q0 * Dims<S, P>::Q1 + 31) / 32;
+  static_assert(RING == 0 || (GEO == GEO_DEFORMED && !C0 && EB == PW && RING_N % 2 == 0 &&
+                              EB * Dims<S, P>::Q0 * Dims<S, P>::Q1 <= NT_),
+                "geometry ring: deformed, one metric-sweep item per thread, 16-byte slices");
+  __device__ static unsigned long long* ring_bars(double* sm) {
+    return reinterpret_cast<unsigned long long*>(sm + RING_OFF + RING * RING_SLOT);
+  }
+  // thread 0: TMA bulk copies of k-slice k of this tile's payload into slot s
+  __device__ static void ring_issue(const OpArgs<S, P>& A, long long tile, int k, int s, double* sm) {
+    constexpr long long NQ = Dims<S, P>::NQ;
+    unsigned long long* bars = ring_bars(sm);
+    const double* src = A.pay + pay_base<PW>(tile * EB, 7, (int)NQ) + (long long)k * RING_N;
+    double* dst = sm + RING_OFF + s * RING_SLOT;
+    mbar_expect_tx(&bars[s], RING_SLOT * 8);
+#pragma unroll
+    for (int cc = 0; cc < RING_C; ++cc) bulk_g2s(dst + cc * RING_N, src + cc * NQ * PW, RING_N * 8, &bars[s]);
+  }
   __device__ static void prefetch_geo(const OpArgs<S, P>& A, long long t) {
     const long long e0 = t * EB;
     const long long n = A.E - e0 < EB ? A.E - e0 : EB;
@@ -233,6 +258,20 @@ struct k_helm {
   __device__ static void run(const OpArgs<S, P>& A, long long tile, double* sm) {
     using Dm = Dims<S, P>;
     const Ctx c = make_ctx<L::EB>(tile, A.E, A.Epad, A.W);
+    if constexpr (RING > 0) {
+      // first slices in flight before the coefficient load: they land
+      // during the F and M1 sweeps
+      if (threadIdx.x == 0) {
+        unsigned long long* bars = ring_bars(sm);
+        for (int s = 0; s < RING; ++s) {
+          mbar_init(&bars[s], 1);
+          mbar_init(&bars[RING + s], RING_WARPS);
+        }
+        mbar_fence_init();
+        if (c.e0 < c.E)
+          for (int s = 0; s < RING && s < Dims<S, P>::Q2; ++s) ring_issue(A, tile, s, s, sm);
+      }
+    }
     if constexpr (C0)
       load_tile_c0<L, P, NT>(A.in, c, A.c0_nx, A.c0_ny, sm + L::EB * L::PLANE);
     else
@@ -241,39 +280,16 @@ struct k_helm {
     __syncthreads();
     body(A, tile, sm, -1);
   }
-  __device__ static void body(const OpArgs<S, P>& A, long long tile, double* sm, long long tnext) {
+  // M1 .. M3: the quadrature-point part of the collocated pipeline (u, v0
+  // in planes UO / V0O on entry; U = lam W u + D1^T w1 + D2^T w2 and the
+  // metric-weighted w0 in V0O on exit), shared by the fused kernel and the
+  // staged quadrature-point kernel (k_qp)
+  __device__ static __forceinline__ void middle(const OpArgs<S, P>& A, const Ctx& c, double* sm, long long tile,
+                                                long long tnext) {
   using Dm = Dims<S, P>;
-  constexpr int P1 = Dm::P1, Q0 = Dm::Q0, Q1 = Dm::Q1, Q2 = Dm::Q2, S2 = L::S2;
-  constexpr int NQ = Dm::NQ, NM = Dm::NM, PL = L::PLANE;
-  constexpr int UO = 0, V0O = PL, V1O = 2 * PL, TAo = 0, TBo = 2 * PL;
-  const Ctx c = make_ctx<L::EB>(tile, A.E, A.Epad, A.W);
-  const double* src = A.in + blockIdx.y * A.in_cstride;
-  double* dst = A.out + blockIdx.y * A.out_cstride;
-  double* xs = sm + L::EB * PL;  // plane 1: coefficient tile staging
-
-  if constexpr (SMT)  // ragged sweep tables staged in shared memory by run()
-    stage_f1<S, P, L, NT, TAo, CoefIn<L, NM>, false, ragged_dispatch(0, S, P), ragged_split(0, S, P), prism_warp_pairs(0, S, P), true>(A.B, sm + L::TABOFF, CoefIn<L, NM>{xs}, sm);
-  else
-    stage_f1<S, P, L, NT, TAo, CoefIn<L, NM>, false, ragged_dispatch(0, S, P), ragged_split(0, S, P), prism_warp_pairs(0, S, P)>(A.B, A.gtab, CoefIn<L, NM>{xs}, sm);
-  __syncthreads();
-  stage_f2<S, P, L, NT, TAo, TBo>(A.B, A.gtab, sm);
-  __syncthreads();
-  if ((geo_prefetch(S, P) & 2) && tnext < 0 && threadIdx.x < 32) prefetch_geo(A, tile);
-  // F3 + D0: u along i, v0 = D0 u
-  items<L, Q1 * Q2, NT>([&](int e, int ps) {
-    const int j = ps / Q2, k = ps - j * Q2;
-    double x[P1], u[Q0], v[Q0];
-#pragma unroll
-    for (int p = 0; p < P1; ++p) x[p] = sm[L::at(e, TBo + (p * Q1 + j) * S2 + k)];
-    line_a0_eo<S, P>(A.B, x, u);
-    line_dd<S, P, 0>(A.D, u, v);
-#pragma unroll
-    for (int i = 0; i < Q0; ++i) {
-      sm[L::at(e, UO + (i * Q1 + j) * S2 + k)] = u[i];
-      sm[L::at(e, V0O + (i * Q1 + j) * S2 + k)] = v[i];
-    }
-  });
-  __syncthreads();
+  constexpr int Q0 = Dm::Q0, Q1 = Dm::Q1, Q2 = Dm::Q2, S2 = L::S2;
+  constexpr int NQ = Dm::NQ, PL = L::PLANE;
+  constexpr int UO = 0, V0O = PL, V1O = 2 * PL;
   // M1: v1 = D1 u along j
   items<L, Q0 * Q2, NT>([&](int e, int ps) {
     const int i = ps / Q2, k = ps - i * Q2;
@@ -294,7 +310,43 @@ struct k_helm {
 #pragma unroll
     for (int k = 0; k < Q2; ++k) u[k] = sm[L::at(e, UO + row + k)];
     line_dd<S, P, 2>(A.D, u, w2);  // w2 holds v2 until overwritten per point
-    if constexpr (GEO == GEO_DEFORMED) {
+    if constexpr (RING > 0) {
+      // geometry from the TMA ring: wait for slice k, read it from shared
+      // memory, release the slot (one arrival per warp); thread 0 refills it
+      // with slice k + RING once every warp has released it
+      unsigned long long* bars = ring_bars(sm);
+      const double* ring = sm + RING_OFF;
+      const bool tile_live = c.e0 < c.E;  // uniform: an all-padding tile issued no copies
+      const unsigned amask = __activemask();
+      const bool leader = (int)(threadIdx.x & 31) == __ffs(amask) - 1;
+#pragma unroll
+      for (int k = 0; k < Q2; ++k) {
+        const int s = k % RING;
+        const unsigned ph = (k / RING) & 1;
+        if (tile_live) mbar_wait(&bars[s], ph);
+        const double* gk = ring + s * RING_SLOT + ps * PW + e;
+        const double l00 = live ? gk[0 * RING_N] : 0.0, l01 = live ? gk[1 * RING_N] : 0.0,
+                     l02 = live ? gk[2 * RING_N] : 0.0, l11 = live ? gk[3 * RING_N] : 0.0,
+                     l12 = live ? gk[4 * RING_N] : 0.0, l22 = live ? gk[5 * RING_N] : 0.0;
+        double wj = 0.0;
+        if constexpr (LAMW) wj = live ? gk[6 * RING_N] : 0.0;
+        if (tile_live) {
+          __syncwarp(amask);
+          if (leader) mbar_arrive(&bars[RING + s]);
+          if (threadIdx.x == 0 && k + RING < Q2) {
+            mbar_wait(&bars[RING + s], ph);
+            ring_issue(A, tile, k + RING, s, sm);
+          }
+        }
+        const double v0 = sm[L::at(e, V0O + row + k)], v1 = sm[L::at(e, V1O + row + k)], v2 = w2[k];
+        const double a0 = fma(l02, v2, fma(l01, v1, l00 * v0));
+        const double a1 = fma(l12, v2, fma(l11, v1, l01 * v0));
+        w2[k] = fma(l22, v2, fma(l12, v1, l02 * v0));
+        sm[L::at(e, V0O + row + k)] = a0;
+        sm[L::at(e, V1O + row + k)] = a1;
+        z[k] = LAMW ? (A.lam * wj) * u[k] : 0.0;
+      }
+    } else if constexpr (GEO == GEO_DEFORMED) {
       const double* g = A.pay + pay_base<PW>(live ? eg : 0, 7, NQ) + (long long)ps * PW;
       // points in chunks of CH: a compiler fence between chunks keeps ptxas
       // from hoisting all 7*Q2 geometry loads (register pressure at high P)
@@ -407,6 +459,41 @@ struct k_helm {
     for (int j = 0; j < Q1; ++j) sm[L::at(e, UO + (i * Q1 + j) * S2 + k)] = r[j];
   });
   __syncthreads();
+  }
+  __device__ static void body(const OpArgs<S, P>& A, long long tile, double* sm, long long tnext) {
+  using Dm = Dims<S, P>;
+  constexpr int P1 = Dm::P1, Q0 = Dm::Q0, Q1 = Dm::Q1, Q2 = Dm::Q2, S2 = L::S2;
+  constexpr int NM = Dm::NM, PL = L::PLANE;
+  constexpr int UO = 0, V0O = PL, TAo = 0, TBo = 2 * PL;
+  const Ctx c = make_ctx<L::EB>(tile, A.E, A.Epad, A.W);
+  const double* src = A.in + blockIdx.y * A.in_cstride;
+  double* dst = A.out + blockIdx.y * A.out_cstride;
+  double* xs = sm + L::EB * PL;  // plane 1: coefficient tile staging
+
+  if constexpr (SMT)  // ragged sweep tables staged in shared memory by run()
+    stage_f1<S, P, L, NT, TAo, CoefIn<L, NM>, false, ragged_dispatch(0, S, P), ragged_split(0, S, P), prism_warp_pairs(0, S, P), true>(A.B, sm + L::TABOFF, CoefIn<L, NM>{xs}, sm);
+  else
+    stage_f1<S, P, L, NT, TAo, CoefIn<L, NM>, false, ragged_dispatch(0, S, P), ragged_split(0, S, P), prism_warp_pairs(0, S, P)>(A.B, A.gtab, CoefIn<L, NM>{xs}, sm);
+  __syncthreads();
+  stage_f2<S, P, L, NT, TAo, TBo>(A.B, A.gtab, sm);
+  __syncthreads();
+  if ((geo_prefetch(S, P) & 2) && tnext < 0 && threadIdx.x < 32) prefetch_geo(A, tile);
+  // F3 + D0: u along i, v0 = D0 u
+  items<L, Q1 * Q2, NT>([&](int e, int ps) {
+    const int j = ps / Q2, k = ps - j * Q2;
+    double x[P1], u[Q0], v[Q0];
+#pragma unroll
+    for (int p = 0; p < P1; ++p) x[p] = sm[L::at(e, TBo + (p * Q1 + j) * S2 + k)];
+    line_a0_eo<S, P>(A.B, x, u);
+    line_dd<S, P, 0>(A.D, u, v);
+#pragma unroll
+    for (int i = 0; i < Q0; ++i) {
+      sm[L::at(e, UO + (i * Q1 + j) * S2 + k)] = u[i];
+      sm[L::at(e, V0O + (i * Q1 + j) * S2 + k)] = v[i];
+    }
+  });
+  __syncthreads();
+  middle(A, c, sm, tile, tnext);
   // B1: r = U + D0^T w0 along i, then B^T along dir 0
   items<L, Q1 * Q2, NT>([&](int e, int ps) {
     const int j = ps / Q2, k = ps - j * Q2;
@@ -433,10 +520,78 @@ struct k_helm {
   }
 };
 
+// ---------------------------------------------------------------------------
+// Staged collocated Helmholtz, quadrature-point kernel (the fused kernel
+// split after BwdTrans and before the final B^T): u (NQ values per
+// element, lane-major work buffer written by k_bwd) ->
+// u' = lam W u + sum_m D_m^T (G^T Lam G) D_m u (k_helm::middle, the same
+// sweeps and metric as the fused kernel), written for the unweighted B^T
+// (k_iprod<GEO_UNIT>).  Only the middle sweeps' three planes are live, the
+// coefficient-space stages run in their own two-plane kernels.
+template <int S, int P, class L, int NT_, int PW, int GEO, bool LAMW, int MINB_>
+struct k_qp {
+  using H = k_helm<S, P, L, NT_, PW, GEO, LAMW, MINB_>;
+  static constexpr int NT = NT_;
+  static constexpr int EB = L::EB;
+  static constexpr int MINB = MINB_;
+  static constexpr bool PERSIST = false;
+  static constexpr bool GEO_PF_AT_START = true;
+  __device__ static void prefetch_geo(const OpArgs<S, P>& A, long long t) { H::prefetch_geo(A, t); }
+  __device__ static void prefetch_in(const OpArgs<S, P>& A, long long t) {
+    const long long e0 = t * EB;
+    const long long n = A.Epad - e0 < EB ? A.Epad - e0 : EB;
+    prefetch_field<Dims<S, P>::NQ>(A.in, A.in_cstride, gridDim.y, e0, n, A.Epad, A.W);
+  }
+  __device__ static void run(const OpArgs<S, P>& A, long long tile, double* sm) {
+    using Dm = Dims<S, P>;
+    constexpr int Q0 = Dm::Q0, Q1 = Dm::Q1, Q2 = Dm::Q2, S2 = L::S2, NQ = Dm::NQ, PL = L::PLANE;
+    constexpr int UO = 0, V0O = PL;
+    const Ctx c = make_ctx<L::EB>(tile, A.E, A.Epad, A.W);
+    const double* src = A.in + blockIdx.y * A.in_cstride;
+    double* dst = A.out + blockIdx.y * A.out_cstride;
+    // u along i from the work buffer, v0 = D0 u
+    items<L, Q1 * Q2, NT>([&](int e, int ps) {
+      const int j = ps / Q2, k = ps - j * Q2;
+      const long long eg = c.e0 + e;
+      const bool live = eg < c.E;
+      const long long base = lane_base(live ? eg : 0, NQ, c.W);
+      double u[Q0], v[Q0];
+#pragma unroll
+      for (int i = 0; i < Q0; ++i) u[i] = live ? __ldcs(src + base + (long long)((i * Q1 + j) * Q2 + k) * c.W) : 0.0;
+      line_dd<S, P, 0>(A.D, u, v);
+#pragma unroll
+      for (int i = 0; i < Q0; ++i) {
+        sm[L::at(e, UO + (i * Q1 + j) * S2 + k)] = u[i];
+        sm[L::at(e, V0O + (i * Q1 + j) * S2 + k)] = v[i];
+      }
+    });
+    __syncthreads();
+    H::middle(A, c, sm, tile, -1);
+    // u' = U + D0^T w0 along i, to the work buffer
+    items<L, Q1 * Q2, NT>([&](int e, int ps) {
+      const int j = ps / Q2, k = ps - j * Q2;
+      const long long eg = c.e0 + e;
+      if (eg >= c.Epad) return;
+      const bool live = eg < c.E;
+      double w[Q0], r[Q0];
+#pragma unroll
+      for (int i = 0; i < Q0; ++i) {
+        w[i] = sm[L::at(e, V0O + (i * Q1 + j) * S2 + k)];
+        r[i] = sm[L::at(e, UO + (i * Q1 + j) * S2 + k)];
+      }
+      line_ddt_acc<S, P, 0>(A.D, w, r);
+      const long long base = lane_base(eg, NQ, c.W);
+#pragma unroll
+      for (int i = 0; i < Q0; ++i) __stcs(dst + base + (long long)((i * Q1 + j) * Q2 + k) * c.W, live ? r[i] : 0.0);
+    });
+  }
+};
+
 // W at point l (standard order) of element eg for the W-payload family
 template <int S, int P, int PW, int GEO>
 __device__ __forceinline__ double w_at(const OpArgs<S, P>& A, long long eg, bool live, int l) {
   if (!live) return 0.0;
+  if constexpr (GEO == GEO_UNIT) return 1.0;
   if constexpr (GEO == GEO_DEFORMED) {
     return __ldcs(A.pay + pay_base<PW>(eg, 1, Dims<S, P>::NQ) + (long long)l * PW);
   } else {

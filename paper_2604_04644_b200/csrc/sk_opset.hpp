@@ -9,7 +9,10 @@
 
 namespace sk {
 
-enum OpId : int { OP_HELM = 0, OP_MASS = 1, OP_BWD = 2, OP_IPROD = 3, OP_PDERIV = 4, OP_IPDERIV = 5, OP_HELM_NC = 6, OP_COUNT = 7 };
+enum OpId : int { OP_HELM = 0, OP_MASS = 1, OP_BWD = 2, OP_IPROD = 3, OP_PDERIV = 4, OP_IPDERIV = 5, OP_HELM_NC = 6,
+                  // staged collocated Helmholtz (bwd -> OP_QP -> OP_BT): the quadrature-point
+                  // kernel and the unweighted B^T
+                  OP_QP = 7, OP_BT = 8, OP_COUNT = 9 };
 
 struct LaunchReq {
   const void* fwd;    // FwdTab<S,P> (host copy, values)
@@ -49,6 +52,7 @@ struct OpSet {
   // instantiated for this order) and its host fill from the dense basis
   // matrix B (NQ x NM row-major) and the reference weights
   int dense_doubles;
+  int dense_mask;  // geometry classes with a dense kernel: bit 0 regular, bit 1 deformed
   void (*fill_dense)(const double* B, const double* refw, double* frags);
 };
 

@@ -169,14 +169,46 @@ constexpr bool kPrismWP[3][11] = {
     {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},
 };
 
+// Deformed Helmholtz geometry through a shared-memory ring fed by TMA bulk
+// copies (cp.async.bulk + mbarrier, sk_ops.cuh k_helm): the ring holds this
+// many k-slices of the tile's metric payload (0 = off: per-thread streaming
+// loads after a tile-start L2 prefetch).  The first slices are issued at
+// tile start and land during the F and M1 sweeps; the metric sweep refills
+// each slot as soon as every warp is done with it.
+constexpr int kGeoRing[4][11] = {
+    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},  // hex
+    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},  // prism
+    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},  // pyr
+    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},  // tet
+};
+#ifdef SK_GEO_RING
+SK_HD constexpr int geo_ring(int, int) { return SK_GEO_RING; }
+#else
+SK_HD constexpr int geo_ring(int S, int P) { return kGeoRing[S][P]; }
+#endif
+
 // Mass by the StdMat strategy on the FP64 tensor cores (sk_dense.cuh)
 // instead of sum factorisation, per geometry class (0 regular, 1 deformed)
 // x shape x order; instantiated up to kDenseMaxP.  Run-time override:
 // SK_MASS_DENSE=0 (never) / 1 (wherever instantiated).
-constexpr int kDenseMaxP = 4;
+constexpr int kDenseMaxP = 6;
+// Measured on B200 (profiles/r02/mass_dense_*.jsonl, roofline fraction
+// sum-fac -> dense): deformed P=1 every shape (hex 0.60 -> 0.70, prism 0.56
+// -> 0.74, pyr 0.46 -> 0.69, tet 0.41 -> 0.73), pyr / tet P=2 (0.46 -> 0.62,
+// 0.48 -> 0.53); regular (|J| M_ref, one GEMM): hex P<=2 (0.23/0.36 ->
+// 0.80/0.61), prism P<=4 (0.23-0.40 -> 0.50-0.73), pyr P<=4 (0.18-0.35 ->
+// 0.65-0.93); slower elsewhere.  Tet regular: see the P<=6 rows.
 constexpr bool kDenseMass[2][4][11] = {
-    {{0}, {0}, {0}, {0}},
-    {{0}, {0}, {0}, {0}},
+    // regular   P: 0  1  2  3  4  5  6
+    {{0, 1, 1, 0, 0, 0, 0},   // hex
+     {0, 1, 1, 1, 1, 0, 0},   // prism
+     {0, 1, 1, 1, 1, 0, 0},   // pyr
+     {0, 0, 0, 0, 0, 0, 0}},  // tet
+    // deformed
+    {{0, 1, 0, 0, 0, 0, 0},
+     {0, 1, 0, 0, 0, 0, 0},
+     {0, 1, 1, 0, 0, 0, 0},
+     {0, 1, 1, 0, 0, 0, 0}},
 };
 
 // Overrides for tuning builds (-DSK_EB_FIXED=... etc.) apply to every class.

@@ -34,6 +34,7 @@ __all__ = [
     "helmholtz_apply_noncoll",
     "helmholtz_apply_coll",
     "helmholtz_apply",
+    "helmholtz_apply_staged",
     "stiffness_apply",
     "apply_operator",
     "apply_to_field",
@@ -252,6 +253,43 @@ def _helmholtz(block: Block, lam: float, form: int, out: Block | None, name: str
             _p(xin), _p(pay), float(lam), _p(xout), _stream(),
         ),
         "sk_helmholtz_apply",
+    )
+    return out
+
+
+#: L2 budget of the staged variant's two quadrature-point work buffers (bytes)
+STAGED_WORK_BYTES = 48 << 20
+
+
+def helmholtz_apply_staged(block: Block, lam: float, out: Block | None = None, chunk_elements: int = 0) -> Block:
+    """Collocated Helmholtz (Alg. 6) as three kernels per element chunk --
+    BwdTrans, the quadrature-point kernel, the unweighted B^T -- with the
+    intermediates in L2-sized work buffers (sk_helmholtz_apply_staged).  Same
+    result as ``helmholtz_apply_coll``; kept for the fused-vs-staged
+    comparison.  Deformed geometry only."""
+    import torch
+
+    _require_state(block, FieldState.COEFF, "helmholtz_apply_staged")
+    if lam < 0.0:
+        raise ValueError(f"reaction coefficient must be nonnegative, got {lam}")
+    out = _out_block(block, out, FieldState.COEFF, block.n_components)
+    pay = block.payload(_lib.SK_PAYLOAD_HELMHOLTZ)
+    W = block.interleave_width
+    unit = 16
+    while unit % W:
+        unit += 16
+    nq = block.basis.n_points
+    chunk = chunk_elements or max(unit, STAGED_WORK_BYTES // (16 * nq) // unit * unit)
+    chunk = min(chunk, -(-block.padded_elements // unit) * unit)
+    work = torch.empty(2 * chunk * nq, dtype=torch.float64, device=torch.device("cuda", torch.cuda.current_device()))
+    xin = block.device(AccessQualifier.READ_ONLY)
+    xout = out.device(AccessQualifier.WRITE_ONLY)
+    _lib.check(
+        _lib.load().sk_helmholtz_apply_staged(
+            block.basis.handle, _geo(block), block.n_elements, W, block.n_components, _p(xin), _p(pay), float(lam),
+            _p(xout), _p(work), chunk, _stream(),
+        ),
+        "sk_helmholtz_apply_staged",
     )
     return out
 

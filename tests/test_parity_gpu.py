@@ -332,3 +332,24 @@ def test_dense_mass_streamed_and_forced_off(sk, monkeypatch):
         blk.set_elements(x)
         res[flag] = sk.mass_apply(blk).get_elements()
     assert _err(res["1"], res["0"]) <= TOL
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+@pytest.mark.parametrize("P", [2, 5, 8, 10])
+def test_staged_helmholtz_matches_fused(sk, shape, P):
+    """Staged collocated Helmholtz (bwd -> quadrature-point kernel ->
+    unweighted B^T over element chunks, sk_helmholtz_apply_staged) against
+    the oracle and the fused kernel: several chunks, a ragged last chunk,
+    two components, interleave width 8, lam 0 and > 0."""
+    n = 211
+    el = O.element(shape, P)
+    geo = O.synthetic_geometry(el, True, n, seed=13)
+    blk = _block_from(sk, shape, P, geo, 8, ncomp=2)
+    x = np.random.default_rng(P).uniform(-1, 1, (2, el.nm, n))
+    blk.set_elements(x)
+    for lam in (0.0, 0.9):
+        got = sk.helmholtz_apply_staged(blk, lam, chunk_elements=48).get_elements()
+        fused = sk.helmholtz_apply(blk, lam).get_elements()
+        for c in range(2):
+            assert _err(got[c], O.helmholtz_coll(el, geo, x[c], lam)) <= TOL, (lam, c)
+        assert _err(got, fused) <= TOL

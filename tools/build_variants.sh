@@ -37,6 +37,7 @@ for v in "$@"; do
       wp) extra="$extra -DSK_PRISM_WP=$n" ;;
       smt) extra="$extra -DSK_SMT=$n" ;;
       rrl) extra="$extra -DSK_RRL=$n" ;;
+      ring) extra="$extra -DSK_GEO_RING=$n" ;;
     esac
   done
   make -j"$(nproc)" BUILD=/tmp/sk200_build_$v LIB=$ROOT/paper_2604_04644_b200/libsk200_$v.so LINEINFO= EXTRA="$extra" > /tmp/sk200_build_$v.log 2>&1 \

@@ -36,6 +36,7 @@ def main():
     ap.add_argument("--gbytes", type=float, default=2.0)
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--fp64-tflops", type=float, default=None)
+    ap.add_argument("--chunk", type=int, default=0, help="staged variant: elements per chunk (0: default)")
     a = ap.parse_args()
     import torch
 
@@ -53,7 +54,8 @@ def main():
             fp64 = 34.2
     deformed = a.geo == "deformed"
     kinds = {"helm": (sk.OperatorKind.HELMHOLTZ_COLL, 1.0), "stiff": (sk.OperatorKind.HELMHOLTZ_COLL, 0.0),
-             "mass": (sk.OperatorKind.MASS, 1.0), "helmnc": (sk.OperatorKind.HELMHOLTZ_NONCOLL, 1.0)}
+             "mass": (sk.OperatorKind.MASS, 1.0), "helmnc": (sk.OperatorKind.HELMHOLTZ_NONCOLL, 1.0),
+             "helmstaged": (sk.OperatorKind.HELMHOLTZ_COLL, 1.0), "stiffstaged": (sk.OperatorKind.HELMHOLTZ_COLL, 0.0)}
     cases = []
     emax = 1
     for op in a.ops.split(","):
@@ -78,6 +80,8 @@ def main():
             fn = lambda: sk.mass_apply(blk, out=out)  # noqa: E731
         elif op == "helmnc":
             fn = lambda: sk.helmholtz_apply_noncoll(blk, lam, out=out)  # noqa: E731
+        elif op.endswith("staged"):
+            fn = lambda: sk.helmholtz_apply_staged(blk, lam, out=out, chunk_elements=a.chunk)  # noqa: E731
         else:
             fn = lambda: sk.helmholtz_apply(blk, lam, out=out)  # noqa: E731
         for _ in range(3):
@@ -92,7 +96,7 @@ def main():
         sec = t0.elapsed_time(t1) / 1e3 / a.reps
         gdof = b.n_modes * E / sec / 1e9
         flops = sk.operator_flops(kind, sk.Shape(s), P) * E
-        cfg = b.launch_config({"mass": 1, "helmnc": 6}.get(op, 0), deformed)
+        cfg = b.launch_config({"mass": 1, "helmnc": 6, "helmstaged": 7, "stiffstaged": 7}.get(op, 0), deformed)
         rec = {
             "op": op, "shape": s, "P": P, "geo": a.geo, "elements": E, "ms": sec * 1e3, "gdof_s": gdof,
             "hbm_gbs": bel * E / sec / 1e9, "hbm_frac": bel * E / sec / 1e9 / hbm,
