@@ -64,6 +64,11 @@ WORKLOADS = {
     "hex4": {"blocks": [("hex", 4, 1000)],
              "metric": "Helmholtz apply GDOF/s (hex, P=4, 10^3 deformed elements, cold L2, FP64)",
              "name": "helmholtz_coll hex P=4 deformed, 1000 elements per GPU (BASELINE configs[0])"},
+    # BASELINE configs[4] "max elements per GPU": one apply streams ~115 GB
+    # (payload + coefficients) of the 180 GB HBM
+    "tet4max": {"blocks": [("tet", 4, 12_800_000)],
+                "metric": "Helmholtz apply GDOF/s (tet, P=4, 12.8M deformed elements per GPU, FP64)",
+                "name": "helmholtz_coll tet P=4 deformed, 12.8M elements per GPU (~115 GB resident, BASELINE configs[4])"},
     # BASELINE configs[3]: mixed hex/prism/pyr/tet Helmholtz, P=6, sharded
     "mixed6": {"blocks": [("hex", 6, 1 << 17), ("prism", 6, 1 << 17), ("pyr", 6, 1 << 17), ("tet", 6, 1 << 17)],
                "metric": "Helmholtz apply GDOF/s (mixed hex/prism/pyr/tet, P=6, deformed, FP64)",

@@ -145,7 +145,7 @@ const double* device_dense(sk_basis* b, void* stream, int* status) {
   }
   for (int m = 0; m < nm; ++m)
     for (int q = 0; q < nq; ++q) B[(size_t)q * nm + m] = bt[(size_t)m * nq + q];
-  b->ops->fill_dense(B.data(), b->hb.refw.data(), frag.data());
+  b->ops->fill_dense(b->hb, B.data(), frag.data());
   e = cudaMalloc(&d_frag, sizeof(double) * frag.size());
   if (e == cudaSuccess) e = cudaMemcpy(d_frag, frag.data(), sizeof(double) * frag.size(), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) {
@@ -155,6 +155,17 @@ const double* device_dense(sk_basis* b, void* stream, int* status) {
   }
   b->dense_dev[dev] = d_frag;
   return d_frag;
+}
+
+// StdMat (DMMA) or sum factorisation for the regular collocated Helmholtz:
+// the tuned table, overridden by SK_HELM_DENSE=0/1
+bool use_dense_helm(const sk_basis* b, int geo) {
+  if (geo != SK_GEO_REGULAR || b->ops->dense_doubles <= 0 || !(b->ops->dense_mask & 4)) return false;
+  if (const char* v = std::getenv("SK_HELM_DENSE")) {
+    if (v[0] == '0') return false;
+    if (v[0] == '1') return true;
+  }
+  return sk::kDenseHelm[b->hb.shape][b->hb.P];
 }
 
 // StdMat (DMMA) or sum-factorised mass for this basis and geometry class:
@@ -388,8 +399,15 @@ int sk_helmholtz_apply(const sk_basis* b, int geo, int form, int64_t E, int W, i
   if (!(lam >= 0.0)) return fail(SK_ERR_ARG, "reaction coefficient must be nonnegative");
   if (form != SK_FORM_COLL && form != SK_FORM_NONCOLL) return fail(SK_ERR_ARG, "unknown Helmholtz form");
   if (int st = check_layout(E, W, ncomp)) return st;
-  return run(const_cast<sk_basis*>(b), form == SK_FORM_NONCOLL ? sk::OP_HELM_NC : sk::OP_HELM, geo, E, W, ncomp, uhat,
-             out, hpay, lam, b->hb.nm, b->hb.nm, stream);
+  sk_basis* bb = const_cast<sk_basis*>(b);
+  const double* dense = nullptr;
+  if (E > 0 && form == SK_FORM_COLL && use_dense_helm(bb, geo)) {
+    int st = SK_OK;
+    dense = device_dense(bb, stream, &st);
+    if (st) return st;
+  }
+  return run(bb, form == SK_FORM_NONCOLL ? sk::OP_HELM_NC : sk::OP_HELM, geo, E, W, ncomp, uhat, out, hpay, lam,
+             b->hb.nm, b->hb.nm, stream, dense);
 }
 
 int sk_helmholtz_apply_staged(const sk_basis* b, int geo, int64_t E, int W, int ncomp, const double* uhat,
@@ -538,7 +556,7 @@ int sk_apply_streamed(const sk_basis* b, int op, int geo, int64_t E, int W, int 
   r.ncomp = ncomp;
   r.geo = geo;
   r.lam = op == SK_STREAM_MASS ? 0.0 : lam;
-  if (kop == sk::OP_MASS && use_dense_mass(b, geo)) {
+  if ((kop == sk::OP_MASS && use_dense_mass(b, geo)) || (kop == sk::OP_HELM && use_dense_helm(b, geo))) {
     r.dense = device_dense(const_cast<sk_basis*>(b), stream, &st);
     if (st) {
       cleanup();

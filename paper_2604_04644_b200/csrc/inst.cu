@@ -321,6 +321,51 @@ int launch_dense_geo(const DenseArgs& a, int ncomp, void* stream) {
   }
 }
 
+template <int S, int P, bool LAMW>
+int launch_helm_dense_lam(const DenseArgs& a, double lam, int ncomp, void* stream) {
+  using X = DenseDims<S, P>;
+  if constexpr (!(X::MASK & 4)) {
+    return (int)cudaErrorInvalidValue;
+  } else {
+    constexpr int smem = (LAMW ? 7 : 6) * X::FR * 8;
+    auto kern = k_helm_dense<S, P, LAMW>;
+    static std::once_flag once;
+    static int per_sm = 1, sms = 148;
+    std::call_once(once, [&] {
+      ensure_smem(kern, smem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kDenseThreads, smem);
+      if (per_sm < 1) per_sm = 1;
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    });
+    const long long groups = (a.Epad + 7) / 8;
+    if (groups == 0) return 0;
+    const int gy = ncomp > 0 ? ncomp : 1;
+    const long long resident = (long long)per_sm * sms / gy;
+    const long long need = (groups + kDenseThreads / 32 - 1) / (kDenseThreads / 32);
+    const long long grid = need < resident ? need : (resident > 0 ? resident : 1);
+    kern<<<dim3((unsigned)grid, (unsigned)gy), kDenseThreads, smem, static_cast<cudaStream_t>(stream)>>>(a, lam);
+    return (int)cudaGetLastError();
+  }
+}
+
+template <int S, int P>
+int launch_helm_dense(const LaunchReq& r, void* stream) {
+  DenseArgs a;
+  a.frag = r.dense;
+  a.in = r.in;
+  a.out = r.out;
+  a.pay = r.pay;
+  a.E = r.E;
+  a.Epad = r.Epad;
+  a.in_cstride = r.in_cs;
+  a.out_cstride = r.out_cs;
+  a.W = r.W;
+  if (r.lam != 0.0) return launch_helm_dense_lam<S, P, true>(a, r.lam, r.ncomp, stream);
+  return launch_helm_dense_lam<S, P, false>(a, r.lam, r.ncomp, stream);
+}
+
 template <int S, int P, int PW>
 int launch_dense(const LaunchReq& r, void* stream) {
   DenseArgs a;
@@ -402,6 +447,10 @@ int launch(int op, const LaunchReq& r, void* stream) {
       if (def) {
         if (r.lam != 0.0) return go<S, P, OP_HELM, k_helm<S, P, typename C::L, C::NT, C::PW, GEO_DEFORMED, true, C::MINB, false, C::RING>>(a, r, r.ncomp, stream);
         return go<S, P, OP_HELM, k_helm<S, P, typename C::L, C::NT, C::PW, GEO_DEFORMED, false, C::MINB, false, C::RING>>(a, r, r.ncomp, stream);
+      }
+      if (r.dense) {  // regular geometry, StdMat on DMMA (sk_dense.cuh)
+        if constexpr (P <= kDenseMaxP) return launch_helm_dense<S, P>(r, stream);
+        return (int)cudaErrorInvalidValue;
       }
       using CR = Cfg<S, P, OP_HELM, true>;  // regular geometry: own tile width
       if (r.lam != 0.0) return go<S, P, OP_HELM, k_helm<S, P, typename CR::L, CR::NT, CR::PW, GEO_REGULAR, true, CR::MINB>, CR>(a, r, r.ncomp, stream);

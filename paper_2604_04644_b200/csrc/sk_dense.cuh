@@ -24,6 +24,7 @@
 
 #include <vector>
 
+#include "basis_host.hpp"
 #include "sk_common.cuh"
 
 namespace sk {
@@ -41,16 +42,21 @@ struct DenseDims {
   static constexpr int F1 = NT * KS1 * 32;       // GEMM1 B fragments: B^T[k = m][n = q]
   static constexpr int F2 = 2 * NT * MT * 32;    // GEMM2 B fragments: B[k = q][n = m]
   static constexpr int FR = KS1 * MT * 32;       // regular: M_ref[k][n]
-  static constexpr int DOUBLES = F1 + F2 + FR;
-  // a geometry class's kernel exists when its fragments fit in 100 KB of
-  // shared memory (two CTAs per SM); bit 0 regular, bit 1 deformed
-  static constexpr int MASK = (FR * 8 <= 100 * 1024 ? 1 : 0) | ((F1 + F2) * 8 <= 100 * 1024 ? 2 : 0);
+  static constexpr int FH = 7 * FR;              // regular Helmholtz: K_0..K_5, M_ref
+  static constexpr int DOUBLES = F1 + F2 + FR + FH;
+  // a kernel exists when its fragments fit in 100 KB of shared memory (two
+  // CTAs per SM): bit 0 regular mass, bit 1 deformed mass, bit 2 regular
+  // Helmholtz
+  static constexpr int MASK = (FR * 8 <= 100 * 1024 ? 1 : 0) | ((F1 + F2) * 8 <= 100 * 1024 ? 2 : 0) |
+                              (FH * 8 <= 100 * 1024 ? 4 : 0);
 };
 
-// host: fragment tables from the dense B (NQ x NM row-major) and refw
+// host: fragment tables from the dense B (NQ x NM row-major), the reference
+// weights, the collocation matrices and the Duffy factors G
 template <int S, int P>
-void fill_dense_frags(const double* B, const double* refw, double* f) {
+void fill_dense_frags(const HostBasis& hb, const double* B, double* f) {
   using X = DenseDims<S, P>;
+  const double* refw = hb.refw.data();
   auto b = [&](int q, int m) { return (q < X::NQ && m < X::NM) ? B[q * X::NM + m] : 0.0; };
   double* f1 = f;
   double* f2 = f + X::F1;
@@ -69,12 +75,57 @@ void fill_dense_frags(const double* B, const double* refw, double* f) {
       for (int q = 0; q < X::NQ; ++q) s += B[q * X::NM + i] * refw[q] * B[q * X::NM + j];
       M[(size_t)i * X::NM + j] = s;
     }
-  for (int ks = 0; ks < X::KS1; ++ks)
-    for (int mt = 0; mt < X::MT; ++mt)
-      for (int l = 0; l < 32; ++l) {
-        const int k = 4 * ks + (l & 3), n = 8 * mt + (l >> 2);
-        fr[(ks * X::MT + mt) * 32 + l] = (k < X::NM && n < X::NM) ? M[(size_t)k * X::NM + n] : 0.0;
+  auto put = [&](double* dst, const std::vector<double>& A) {
+    for (int ks = 0; ks < X::KS1; ++ks)
+      for (int mt = 0; mt < X::MT; ++mt)
+        for (int l = 0; l < 32; ++l) {
+          const int k = 4 * ks + (l & 3), n = 8 * mt + (l >> 2);
+          dst[(ks * X::MT + mt) * 32 + l] = (k < X::NM && n < X::NM) ? A[(size_t)k * X::NM + n] : 0.0;
+        }
+  };
+  put(fr, M);
+  // Regular Helmholtz: with T_a(m, l) = (G D B)_a, the Duffy-mapped reference
+  // gradient of mode m at point l (collocation D_d of column m of B along
+  // direction d, operators.py:449-464, then G, 471-490), the elemental
+  // operator of an affine element is sum_ab Lam_ab K_ab + lam |J| M_ref with
+  // K_ab[n][m] = sum_l refw_l T_b(n, l) T_a(m, l) (operators.py:502-523,
+  // 670-699).  Lam is symmetric: coefficient matrices for the payload order
+  // Lam00, Lam01, Lam02, Lam11, Lam12, Lam22 are K_aa and K_ab + K_ba.
+  const int Q0 = hb.Q[0], Q1 = hb.Q[1], Q2 = hb.Q[2];
+  std::vector<double> T((size_t)3 * X::NM * X::NQ);  // [a][m][l]
+  for (int m = 0; m < X::NM; ++m) {
+    for (int i = 0; i < Q0; ++i)
+      for (int j = 0; j < Q1; ++j)
+        for (int k = 0; k < Q2; ++k) {
+          const int l = (i * Q1 + j) * Q2 + k;
+          double v[3] = {0.0, 0.0, 0.0};
+          for (int a = 0; a < Q0; ++a) v[0] += hb.D[0][i * Q0 + a] * B[((a * Q1 + j) * Q2 + k) * X::NM + m];
+          for (int b = 0; b < Q1; ++b) v[1] += hb.D[1][j * Q1 + b] * B[((i * Q1 + b) * Q2 + k) * X::NM + m];
+          for (int c = 0; c < Q2; ++c) v[2] += hb.D[2][k * Q2 + c] * B[((i * Q1 + j) * Q2 + c) * X::NM + m];
+          for (int a = 0; a < 3; ++a) {
+            const double* g = &hb.G[9 * l + 3 * a];
+            T[((size_t)a * X::NM + m) * X::NQ + l] = g[0] * v[0] + g[1] * v[1] + g[2] * v[2];
+          }
+        }
+  }
+  const int ai[6] = {0, 0, 0, 1, 1, 2}, bi[6] = {0, 1, 2, 1, 2, 2};
+  std::vector<double> K((size_t)X::NM * X::NM);
+  for (int cidx = 0; cidx < 6; ++cidx) {
+    const int a = ai[cidx], b = bi[cidx];
+    for (int n = 0; n < X::NM; ++n)
+      for (int m = 0; m < X::NM; ++m) {
+        double s1 = 0.0, s2 = 0.0;
+        for (int l = 0; l < X::NQ; ++l) {
+          const double w = refw[l];
+          s1 += w * T[((size_t)b * X::NM + n) * X::NQ + l] * T[((size_t)a * X::NM + m) * X::NQ + l];
+          if (a != b) s2 += w * T[((size_t)a * X::NM + n) * X::NQ + l] * T[((size_t)b * X::NM + m) * X::NQ + l];
+        }
+        // B operand of outT = uhatT . H^T: element [k = m][n]
+        K[(size_t)m * X::NM + n] = s1 + s2;
       }
+    put(f + X::F1 + X::F2 + X::FR + cidx * X::FR, K);
+  }
+  put(f + X::F1 + X::F2 + X::FR + 6 * X::FR, M);
 }
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
@@ -166,6 +217,62 @@ __global__ void __launch_bounds__(kDenseThreads) k_mass_dense(const __grid_const
         const int m = 8 * mt + 2 * t;
         if (m < NM) __stcs(dst + ob + (long long)m * A.W, live ? c[mt][0] : 0.0);
         if (m + 1 < NM) __stcs(dst + ob + (long long)(m + 1) * A.W, live ? c[mt][1] : 0.0);
+      }
+    }
+  }
+}
+
+// Regular-geometry collocated Helmholtz / stiffness as StdMat on DMMA:
+// out_e = sum_c coef_e,c (H_c uhat_e), coef = (Lam00, Lam01, Lam02, Lam11,
+// Lam12, Lam22, lam |J|) from the regular Helmholtz payload (kRegPW lanes),
+// H_c = K_c / M_ref (fill_dense_frags).  One 8-element group per warp; per
+// output mode tile the seven products accumulate in two registers each and
+// are combined with the element's coefficients.
+template <int S, int P, bool LAMW>
+__global__ void __launch_bounds__(kDenseThreads) k_helm_dense(const __grid_constant__ DenseArgs A, double lam) {
+  using X = DenseDims<S, P>;
+  constexpr int NM = X::NM, KS1 = X::KS1, MT = X::MT, NC = LAMW ? 7 : 6;
+  extern __shared__ double sfr[];
+  for (int i = threadIdx.x; i < NC * X::FR / 2; i += kDenseThreads)
+    reinterpret_cast<double2*>(sfr)[i] = __ldg(reinterpret_cast<const double2*>(A.frag + X::F1 + X::F2 + X::FR) + i);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, t = lane & 3, r = lane >> 2;
+  const long long warps = (long long)gridDim.x * (kDenseThreads / 32);
+  const double* src = A.in + blockIdx.y * A.in_cstride;
+  double* dst = A.out + blockIdx.y * A.out_cstride;
+  const long long ngroups = (A.Epad + 7) / 8;
+  for (long long g = blockIdx.x * (kDenseThreads / 32) + (threadIdx.x >> 5); g < ngroups; g += warps) {
+    const long long e = g * 8 + r;
+    const bool live = e < A.E;
+    const long long base = lane_base(live ? e : 0, NM, A.W);
+    double a[KS1];
+#pragma unroll
+    for (int ks = 0; ks < KS1; ++ks) {
+      const int m = 4 * ks + t;
+      a[ks] = (live && m < NM) ? __ldcs(src + base + (long long)m * A.W) : 0.0;
+    }
+    double coef[NC];
+    const double* ge = A.pay + pay_base<kRegPW>(live ? e : 0, 8, 1);
+#pragma unroll
+    for (int cc = 0; cc < 6; ++cc) coef[cc] = live ? __ldg(ge + cc * kRegPW) : 0.0;
+    if constexpr (LAMW) coef[6] = live ? lam * __ldg(ge + 6 * kRegPW) : 0.0;
+    const bool store = e < A.Epad;
+    const long long ob = lane_base(store ? e : 0, NM, A.W);
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+      double o0 = 0.0, o1 = 0.0;
+#pragma unroll
+      for (int cc = 0; cc < NC; ++cc) {
+        double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < KS1; ++ks) dmma(c0, c1, a[ks], sfr[((cc * KS1 + ks) * MT + mt) * 32 + lane]);
+        o0 = fma(coef[cc], c0, o0);
+        o1 = fma(coef[cc], c1, o1);
+      }
+      const int m = 8 * mt + 2 * t;
+      if (store) {
+        if (m < NM) __stcs(dst + ob + (long long)m * A.W, o0);
+        if (m + 1 < NM) __stcs(dst + ob + (long long)(m + 1) * A.W, o1);
       }
     }
   }

@@ -52,8 +52,8 @@ struct OpSet {
   // instantiated for this order) and its host fill from the dense basis
   // matrix B (NQ x NM row-major) and the reference weights
   int dense_doubles;
-  int dense_mask;  // geometry classes with a dense kernel: bit 0 regular, bit 1 deformed
-  void (*fill_dense)(const double* B, const double* refw, double* frags);
+  int dense_mask;  // dense kernels: bit 0 regular mass, bit 1 deformed mass, bit 2 regular Helmholtz
+  void (*fill_dense)(const HostBasis& hb, const double* B, double* frags);
 };
 
 template <int S, int P>

@@ -192,23 +192,43 @@ SK_HD constexpr int geo_ring(int S, int P) { return kGeoRing[S][P]; }
 // x shape x order; instantiated up to kDenseMaxP.  Run-time override:
 // SK_MASS_DENSE=0 (never) / 1 (wherever instantiated).
 constexpr int kDenseMaxP = 6;
-// Measured on B200 (profiles/r02/mass_dense_*.jsonl, roofline fraction
-// sum-fac -> dense): deformed P=1 every shape (hex 0.60 -> 0.70, prism 0.56
-// -> 0.74, pyr 0.46 -> 0.69, tet 0.41 -> 0.73), pyr / tet P=2 (0.46 -> 0.62,
-// 0.48 -> 0.53); regular (|J| M_ref, one GEMM): hex P<=2 (0.23/0.36 ->
-// 0.80/0.61), prism P<=4 (0.23-0.40 -> 0.50-0.73), pyr P<=4 (0.18-0.35 ->
-// 0.65-0.93); slower elsewhere.  Tet regular: see the P<=6 rows.
+// Measured on B200 (roofline fraction sum-fac -> dense): deformed
+// (profiles/r02/mass_dense_def_*.jsonl) P=1 every shape (hex 0.60 -> 0.70,
+// prism 0.56 -> 0.74, pyr 0.46 -> 0.69, tet 0.41 -> 0.73), pyr / tet P=2
+// (0.46 -> 0.62, 0.48 -> 0.53); regular (|J| M_ref, one GEMM;
+// profiles/r02/dense_mass_regular_*.jsonl) hex P<=2 (0.23/0.35 ->
+// 0.76/0.58), prism P<=4 (0.22-0.38 -> 0.48-0.69), pyr P<=5 (0.17-0.37 ->
+// 0.59-0.89), tet P<=6 (0.19-0.33 -> 0.65-1.16); slower elsewhere.
 constexpr bool kDenseMass[2][4][11] = {
     // regular   P: 0  1  2  3  4  5  6
     {{0, 1, 1, 0, 0, 0, 0},   // hex
      {0, 1, 1, 1, 1, 0, 0},   // prism
-     {0, 1, 1, 1, 1, 0, 0},   // pyr
-     {0, 0, 0, 0, 0, 0, 0}},  // tet
+     {0, 1, 1, 1, 1, 1, 0},   // pyr
+     {0, 1, 1, 1, 1, 1, 1}},  // tet
     // deformed
     {{0, 1, 0, 0, 0, 0, 0},
      {0, 1, 0, 0, 0, 0, 0},
      {0, 1, 1, 0, 0, 0, 0},
      {0, 1, 1, 0, 0, 0, 0}},
+};
+
+// Regular-geometry collocated Helmholtz / stiffness by StdMat on DMMA
+// (sk_dense.cuh k_helm_dense: seven NM x NM element-independent matrices
+// combined with the element's Lam and |J|) instead of sum factorisation,
+// per shape x order (instantiated where the fragments fit, P <= kDenseMaxP).
+// Run-time override: SK_HELM_DENSE=0 / 1.
+// Measured (profiles/r02/dense_helm_regular_*.jsonl, roofline fraction of
+// the reference flop count, Helmholtz / stiffness): hex P<=2 (0.30/0.41 ->
+// 1.30/0.46), prism P<=3 (0.32-0.47 -> 0.55-0.99), pyr P<=3 (0.27-0.40 ->
+// 0.86-1.18), tet P<=4 (0.26-0.43 -> 1.00-1.35); the dense form does fewer
+// flops than the sum-factorised count there.  P>=4 (hex, prism, pyr) and P>=5
+// (tet): fragments beyond 100 KB of shared memory or slower.
+constexpr bool kDenseHelm[4][11] = {
+    // P: 0  1  2  3  4
+    {0, 1, 1, 0, 0},  // hex
+    {0, 1, 1, 1, 0},  // prism
+    {0, 1, 1, 1, 0},  // pyr
+    {0, 1, 1, 1, 1},  // tet
 };
 
 // Overrides for tuning builds (-DSK_EB_FIXED=... etc.) apply to every class.

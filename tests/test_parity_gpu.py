@@ -353,3 +353,24 @@ def test_staged_helmholtz_matches_fused(sk, shape, P):
         for c in range(2):
             assert _err(got[c], O.helmholtz_coll(el, geo, x[c], lam)) <= TOL, (lam, c)
         assert _err(got, fused) <= TOL
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+@pytest.mark.parametrize("P", [1, 2, 3, 4, 5, 6])
+def test_dense_dmma_regular_helmholtz(sk, monkeypatch, shape, P):
+    """Regular-geometry collocated Helmholtz and stiffness by StdMat on the
+    FP64 tensor cores (seven element-independent matrices, forced with
+    SK_HELM_DENSE=1 wherever the fragments fit) against the oracle on every
+    element; where no dense kernel exists the sum-factorised path runs."""
+    monkeypatch.setenv("SK_HELM_DENSE", "1")
+    n = 157
+    el = O.element(shape, P)
+    geo = O.synthetic_geometry(el, False, n, seed=12)
+    for width in (1, 8):
+        blk = _block(sk, shape, P, False, n, 12, width, ncomp=2)
+        x = np.random.default_rng(P).uniform(-1, 1, (2, el.nm, n))
+        blk.set_elements(x)
+        for lam in (0.0, 1.7):
+            got = sk.helmholtz_apply(blk, lam).get_elements()
+            for c in range(2):
+                assert _err(got[c], O.helmholtz_coll(el, geo, x[c], lam)) <= TOL, (width, lam, c)
