@@ -551,6 +551,31 @@ def run_sweep(args, ws, rank, dist, clk, quick=False):
     return tables, fp64
 
 
+def _sample_parity(blocks, outs, spec, rank, n_extra=2):
+    """Max-normalised error (speckern bench.py:192-194) of the timed outputs
+    on sampled elements of every block -- first, middle, last and random
+    ones -- against the CPU oracle on identical inputs (the same seeded
+    geometry, the device-resident coefficients)."""
+    import oracle as O
+    import paper_2604_04644_b200 as sk
+    from oracle.geom import deformed_coords
+
+    rng = np.random.default_rng(99)
+    worst = 0.0
+    for k, ((shape, P, E), blk, out) in enumerate(zip(spec, blocks, outs)):
+        idx = sorted({0, 1, E // 2, E - 2, E - 1, *[int(v) for v in rng.integers(0, E, n_extra)]})
+        idx = [i for i in idx if 0 <= i < E]
+        el = O.element(shape, P)
+        nm = blk.basis.n_modes
+        xs = blk.device(sk.AccessQualifier.READ_ONLY).view(E, nm)[idx].cpu().numpy().T
+        ys = out.device(sk.AccessQualifier.READ_ONLY).view(E, nm)[idx].cpu().numpy().T
+        prm = np.concatenate([O.deformation_params(1, SEED + k, first=rank * E + i) for i in idx])
+        geo = O.deformed_geometry_from_coords(el, deformed_coords(el, prm))
+        worst = max(worst, O.rel_diff(ys, O.helmholtz_coll(el, geo, xs, LAM)))
+    return {"max_rel_err": float(f"{worst:.2e}"), "elements_checked_per_block": len(idx),
+            "metric": "max-normalised vs CPU oracle (speckern bench.py:192-194)"}
+
+
 def run_device(args, ws, rank, local):
     import torch
 
@@ -634,6 +659,7 @@ def run_device(args, ws, rank, local):
     ndof = ndof_rank * ws
     value = ndof * args.steps / (ms_max / 1e3) / 1e9
     main_clocks = clk.summary(w0, w1)
+    parity = _sample_parity(blocks, outs, spec, rank) if rank == 0 else None
 
     warm_us = None
     if cold:
@@ -759,6 +785,7 @@ def run_device(args, ws, rank, local):
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
             "clocks": main_clocks,
+            "parity": parity,
             "comm": {"backend": "nccl" if dist else None, "world": ws, "collectives_in_timed_region": 0},
         }
         if nb > 1:
