@@ -583,15 +583,21 @@ def run_device(args, ws, rank, local):
     from paper_2604_04644_b200 import _lib
     import oracle as O
 
-    torch.cuda.set_device(local)
+    # SK_BENCH_SHARE_GPU=1: every rank on cuda:0 over gloo -- a functional
+    # check of the multi-rank code path on a one-GPU box (timings meaningless)
+    share = os.environ.get("SK_BENCH_SHARE_GPU") == "1"
+    torch.cuda.set_device(0 if share else local)
     dist = None
     if ws > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         chk = torch.ones(1, device="cuda")
         dist.all_reduce(chk)  # communicator up: comm_nranks == world size
-        assert int(chk.item()) == ws, "NCCL communicator does not span every rank"
+        assert int(chk.item()) == ws, "communicator does not span every rank"
     dev = torch.cuda.current_device()
     clk = Clocks(dev).start()  # sampling from before the warm-up on
     wl = WORKLOADS[args.workload]
@@ -786,7 +792,7 @@ def run_device(args, ws, rank, local):
             "gpu_launches": launches,
             "clocks": main_clocks,
             "parity": parity,
-            "comm": {"backend": "nccl" if dist else None, "world": ws, "collectives_in_timed_region": 0},
+            "comm": {"backend": dist.get_backend() if dist else None, "world": ws, "collectives_in_timed_region": 0},
         }
         if nb > 1:
             line["per_block_ms"] = {f"{b.shape.value}": m for b, m in zip(blocks, per_block_ms)}
@@ -893,7 +899,7 @@ def run_c0(args, ws, rank, dist, dev, wl, clk):
                     "d2h_bytes_per_step": 8 * mesh.n_dofs},
             "gpu_launches": launches,
             "clocks": clk.summary(w0, w1),
-            "comm": {"backend": "nccl" if dist else None, "world": ws,
+            "comm": {"backend": dist.get_backend() if dist else None, "world": ws,
                      "collectives_in_timed_region": "2 P2P send/recv per interface per step" if ws > 1 else 0},
         }
         print(json.dumps(line), flush=True)

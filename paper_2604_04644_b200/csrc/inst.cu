@@ -468,11 +468,11 @@ int launch(int op, const LaunchReq& r, void* stream) {
       return go<S, P, OP_MASS, k_mass<S, P, typename C::L, C::NT, C::PW, GEO_REGULAR, C::MINB>>(a, r, r.ncomp, stream);
     }
 #endif
-#if !defined(SK_ONLY_OP)
-    case OP_BWD: {
+    case OP_BWD: {  // always built: the dense kernels' basis matrix comes from it
       using C = Cfg<S, P, OP_BWD>;
       return go<S, P, OP_BWD, k_bwd<S, P, typename C::L, C::NT, C::MINB>>(a, r, r.ncomp, stream);
     }
+#if !defined(SK_ONLY_OP)
     case OP_IPROD: {
       using C = Cfg<S, P, OP_IPROD>;
       if (def) return go<S, P, OP_IPROD, k_iprod<S, P, typename C::L, C::NT, C::PW, GEO_DEFORMED, C::MINB>>(a, r, r.ncomp, stream);

@@ -144,9 +144,17 @@ struct DenseArgs {
 };
 
 constexpr int kDenseThreads = 256;
+// min CTAs per SM for the dense mass kernel's register budget (0: none) and
+// next-group prefetch of the coefficient fragments (tuning builds)
+#ifndef SK_DENSE_MINB
+#define SK_DENSE_MINB 0
+#endif
+#ifndef SK_DENSE_PF
+#define SK_DENSE_PF 0
+#endif
 
 template <int S, int P, int PW, int GEO>
-__global__ void __launch_bounds__(kDenseThreads) k_mass_dense(const __grid_constant__ DenseArgs A) {
+__global__ void __launch_bounds__(kDenseThreads, SK_DENSE_MINB) k_mass_dense(const __grid_constant__ DenseArgs A) {
   using X = DenseDims<S, P>;
   constexpr int NQ = X::NQ, NM = X::NM, KS1 = X::KS1, MT = X::MT;
   extern __shared__ double sfr[];
@@ -163,15 +171,29 @@ __global__ void __launch_bounds__(kDenseThreads) k_mass_dense(const __grid_const
   const double* src = A.in + blockIdx.y * A.in_cstride;
   double* dst = A.out + blockIdx.y * A.out_cstride;
   const long long ngroups = (A.Epad + 7) / 8;
-  for (long long g = blockIdx.x * (kDenseThreads / 32) + (threadIdx.x >> 5); g < ngroups; g += warps) {
-    const long long e = g * 8 + r;  // this lane's element (A-operand row = C row)
-    const bool live = e < A.E;
-    const long long base = lane_base(live ? e : 0, NM, A.W);
-    double a[KS1];
+  auto load_a = [&](long long gg, double (&dst)[KS1]) {
+    const long long ee = gg * 8 + r;
+    const bool lv = gg < ngroups && ee < A.E;
+    const long long bb = lane_base(lv ? ee : 0, NM, A.W);
 #pragma unroll
     for (int ks = 0; ks < KS1; ++ks) {
       const int m = 4 * ks + t;
-      a[ks] = (live && m < NM) ? __ldcs(src + base + (long long)m * A.W) : 0.0;
+      dst[ks] = (lv && m < NM) ? __ldcs(src + bb + (long long)m * A.W) : 0.0;
+    }
+  };
+  double a_next[KS1];
+  const long long g_first = blockIdx.x * (kDenseThreads / 32) + (threadIdx.x >> 5);
+  if constexpr (SK_DENSE_PF) load_a(g_first, a_next);
+  for (long long g = g_first; g < ngroups; g += warps) {
+    const long long e = g * 8 + r;  // this lane's element (A-operand row = C row)
+    const bool live = e < A.E;
+    double a[KS1];
+    if constexpr (SK_DENSE_PF) {
+#pragma unroll
+      for (int ks = 0; ks < KS1; ++ks) a[ks] = a_next[ks];
+      load_a(g + warps, a_next);  // next group's coefficients in flight during this one
+    } else {
+      load_a(g, a);
     }
     double c[MT][2];
 #pragma unroll

@@ -163,3 +163,19 @@ def test_bench_rank_count_must_match_gpus():
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "1"],
                          capture_output=True, text=True, env=env, timeout=120)
     assert out.returncode != 0 and "WORLD_SIZE=1" in out.stderr
+
+
+def test_bench_gpus_flag_relaunches_ranks():
+    """--gpus 2 outside a launcher re-executes bench.py under
+    torch.distributed.run with two ranks; rank 0 alone prints the line
+    (n_gpus 2), the other rank exits 0 (reference arm: no GPU needed)."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    env["SK_BENCH_CPU_PER_CORE"] = "64"
+    out = subprocess.run(
+        [sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2", "--steps", "1",
+         "--warmup", "1"],
+        capture_output=True, text=True, env=env, timeout=600,
+    )
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [json.loads(ln) for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1 and lines[0]["n_gpus"] == 2 and lines[0]["impl"] == "reference"

@@ -38,6 +38,8 @@ for v in "$@"; do
       smt) extra="$extra -DSK_SMT=$n" ;;
       rrl) extra="$extra -DSK_RRL=$n" ;;
       ring) extra="$extra -DSK_GEO_RING=$n" ;;
+      dminb) extra="$extra -DSK_DENSE_MINB=$n" ;;
+      dpf) extra="$extra -DSK_DENSE_PF=$n" ;;
     esac
   done
   make -j"$(nproc)" BUILD=/tmp/sk200_build_$v LIB=$ROOT/paper_2604_04644_b200/libsk200_$v.so LINEINFO= EXTRA="$extra" > /tmp/sk200_build_$v.log 2>&1 \

@@ -31,13 +31,21 @@ KEYS = [
 
 def summarise(path):
     rows = list(csv.reader(open(path)))
-    hdr, units, vals = rows[0], rows[1], rows[2]
+    hdr, units = rows[0], rows[1]
+    for vals in rows[2:]:
+        summarise_row(path, hdr, units, vals)
+
+
+def summarise_row(path, hdr, units, vals):
     d = dict(zip(hdr, vals))
     u = dict(zip(hdr, units))
     print(f"== {path}  {d.get('Kernel Name', '')[:140]}")
     for k, name in KEYS:
         if k in d:
             print(f"  {name:16s} {d[k]} {u[k]}")
+    for h, v in d.items():  # tensor-pipe (DMMA) activity, when the kernel uses it
+        if "pipe_tensor" in h and "pct_of_peak_sustained_active" in h and v not in ("", "0"):
+            print(f"  {h[:60]:60s} {v} {u[h]}")
     stalls = []
     for h, v in d.items():
         if h.startswith("smsp__pcsamp_warps_issue_stalled_") and not h.endswith("_not_issued"):
