@@ -412,8 +412,10 @@ SWEEP_BYTES = 1.2e9  # algorithmic bytes per apply per cell (>= 1 GB, >> L2)
 POOL = 1 << 16  # reference-seeded elements per pool, tiled to the cell size
 
 
-def _cells(quick: bool):
+def _cells(quick: bool, only=None):
     orders = (2, 4, 6, 8, 10) if quick else tuple(range(2, 11))
+    if only:
+        return [c for c in _cells(quick) if c[0] in only]
     out = []
     for s in SHAPES:
         for P in orders:
@@ -450,13 +452,14 @@ def run_sweep(args, ws, rank, dist, clk, quick=False):
     verts = {}
     rng = np.random.default_rng(1234 + rank)
     res = []
-    for tab, op, deformed, s, P in _cells(quick):
+    cell_bytes = args.sweep_gb * 1e9
+    for tab, op, deformed, s, P in _cells(quick, args.sweep_tables.split(",") if args.sweep_tables else None):
         kind, lam = kinds[op]
         shp = sk.Shape(s)
         b = sk.build_shape_basis(shp, P)
         bel = sk.operator_bytes(kind, shp, P, deformed, lam)
         if deformed:
-            E = max(POOL, int(SWEEP_BYTES / bel))
+            E = max(POOL, int(cell_bytes / bel))
             reps_e = -(-E // POOL)
             fac = sk.GeometricFactors(sk.GeometryClass.DEFORMED, shp, E, params=np.tile(params, (reps_e, 1))[:E], basis=b)
         else:
@@ -805,7 +808,7 @@ def run_device(args, ws, rank, local):
                             "bytes_el = 8(2N_P + 7N_Q) (6N_Q stiffness, N_Q mass; 7 / 6 / 1 regular), "
                             "flops_el = reference operator_flops",
                 "parity": "6 sampled elements per cell vs CPU oracle, max-normalised (speckern bench.py:192-194)",
-                "cells": f"deformed: max({POOL}, {SWEEP_BYTES / 1e9:.1f} GB / bytes_el) elements per apply; regular: "
+                "cells": f"deformed: max({POOL}, {args.sweep_gb:.1f} GB / bytes_el) elements per apply; regular: "
                          f"min(2^21, max({POOL}, 4e10 / flops_el)); tiled pool of {POOL} seeded elements; "
                          "time = CUDA events over >= 0.15 s of back-to-back applies",
                 "seconds": round(sweep_s, 1),
@@ -938,6 +941,9 @@ def main():
     ap.add_argument("--sweep", choices=["auto", "on", "off"], default="auto",
                     help="per (shape, P) table in the JSON line (auto: default workload only)")
     ap.add_argument("--sweep-quick", action="store_true", help="P in {2,4,6,8,10} only")
+    ap.add_argument("--sweep-gb", type=float, default=SWEEP_BYTES / 1e9,
+                    help="algorithmic GB per apply per deformed cell (e.g. 100: max elements per GPU, configs[4])")
+    ap.add_argument("--sweep-tables", default="", help="comma list of per_shape_P tables to run (default all)")
     ap.add_argument("--ref-sweep", action="store_true", help="with --impl reference: CPU GDOF/s per shape x order")
     args = ap.parse_args()
     if args.gpus < 1:

@@ -145,18 +145,23 @@ struct DenseArgs {
 
 constexpr int kDenseThreads = 256;
 // min CTAs per SM for the dense mass kernel's register budget (0: none) and
-// next-group prefetch of the coefficient fragments (tuning builds)
+// next-group prefetch of the coefficient fragments: on for regular geometry
+// (measured +4-38 % on regular pyr P=3-5 / tet P=3-6, profiles/r02/
+// dense_tune_reg.jsonl), off for deformed (slower at P=1, where the W stream
+// already keeps the loads in flight; dense_tune_def.jsonl).  SK_DENSE_PF=0/1
+// forces it in tuning builds.
 #ifndef SK_DENSE_MINB
 #define SK_DENSE_MINB 0
 #endif
 #ifndef SK_DENSE_PF
-#define SK_DENSE_PF 0
+#define SK_DENSE_PF -1
 #endif
 
 template <int S, int P, int PW, int GEO>
 __global__ void __launch_bounds__(kDenseThreads, SK_DENSE_MINB) k_mass_dense(const __grid_constant__ DenseArgs A) {
   using X = DenseDims<S, P>;
   constexpr int NQ = X::NQ, NM = X::NM, KS1 = X::KS1, MT = X::MT;
+  constexpr bool PF = SK_DENSE_PF >= 0 ? SK_DENSE_PF != 0 : GEO == GEO_REGULAR;
   extern __shared__ double sfr[];
   // fragments this geometry class reads: GEMM1 + GEMM2 (deformed) or M_ref
   constexpr int OFF = GEO == GEO_DEFORMED ? 0 : X::F1 + X::F2;
@@ -183,12 +188,12 @@ __global__ void __launch_bounds__(kDenseThreads, SK_DENSE_MINB) k_mass_dense(con
   };
   double a_next[KS1];
   const long long g_first = blockIdx.x * (kDenseThreads / 32) + (threadIdx.x >> 5);
-  if constexpr (SK_DENSE_PF) load_a(g_first, a_next);
+  if constexpr (PF) load_a(g_first, a_next);
   for (long long g = g_first; g < ngroups; g += warps) {
     const long long e = g * 8 + r;  // this lane's element (A-operand row = C row)
     const bool live = e < A.E;
     double a[KS1];
-    if constexpr (SK_DENSE_PF) {
+    if constexpr (PF) {
 #pragma unroll
       for (int ks = 0; ks < KS1; ++ks) a[ks] = a_next[ks];
       load_a(g + warps, a_next);  // next group's coefficients in flight during this one
