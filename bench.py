@@ -76,6 +76,11 @@ WORKLOADS = {
                        "(BASELINE configs[3])"},
     # BASELINE configs[4]: assembled C0 variant (hex, P=4), z-slab per GPU,
     # NCCL exchange of the shared DOF layers inside the timed region
+    # assembled C0 on an extruded triangulated prism mesh (signed maps)
+    "c0prism": {"blocks": [("prism", 4, 2 * 48 * 48 * 48)],
+                "metric": "Assembled C0 Helmholtz apply GDOF/s (global DOFs, prism P=4, deformed, FP64)",
+                "name": "assembled C0 helmholtz prism P=4, 48x48 triangulated squares x 48 layers per GPU "
+                        "(extrusion slabs), NCCL neighbour exchange of shared DOF layers (BASELINE configs[4])"},
     "c0hex": {"blocks": [("hex", 4, 64 * 64 * 64)],
               "metric": "Assembled C0 Helmholtz apply GDOF/s (global DOFs, hex P=4, deformed, FP64)",
               "name": "assembled C0 helmholtz hex P=4, 64x64x64 elements per GPU (z-slabs), "
@@ -605,7 +610,7 @@ def run_device(args, ws, rank, local):
     clk = Clocks(dev).start()  # sampling from before the warm-up on
     wl = WORKLOADS[args.workload]
     spec = [(s, P, args.elements or e) for s, P, e in wl["blocks"]]
-    if args.workload == "c0hex":
+    if args.workload in ("c0hex", "c0prism"):
         return run_c0(args, ws, rank, dist, dev, wl, clk)
 
     # every rank owns a contiguous slice of each block of the seeded mesh
@@ -826,11 +831,16 @@ def run_c0(args, ws, rank, dist, dev, wl, clk):
     import torch
 
     from paper_2604_04644_b200 import _lib
-    from paper_2604_04644_b200.assembly import C0HexMesh
+    from paper_2604_04644_b200.assembly import C0HexMesh, C0PrismMesh
 
-    n = 64 if not args.elements else max(1, round(args.elements ** (1.0 / 3.0)))
     P = 4
-    mesh = C0HexMesh(n, n, n * ws, P, rank=rank, world=ws)
+    prism = args.workload == "c0prism"
+    if prism:
+        n = 48 if not args.elements else max(1, round((args.elements / 2) ** (1.0 / 3.0)))
+        mesh = C0PrismMesh(n, n, n * ws, P, rank=rank, world=ws)
+    else:
+        n = 64 if not args.elements else max(1, round(args.elements ** (1.0 / 3.0)))
+        mesh = C0HexMesh(n, n, n * ws, P, rank=rank, world=ws)
     x = torch.empty(mesh.n_dofs, dtype=torch.float64, device="cuda").uniform_(-1.0, 1.0)
     mesh.block.payload(_lib.SK_PAYLOAD_HELMHOLTZ)
     for _ in range(args.warmup):
@@ -855,7 +865,7 @@ def run_c0(args, ws, rank, dist, dev, wl, clk):
     if dist:
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
     ms_max = float(tmax.item())
-    n_global = (n * P + 1) ** 2 * (n * ws * P + 1)
+    n_global = mesh.layer * (n * ws * P + 1)  # DOF layers along the slab axis
     value = n_global * args.steps / (ms_max / 1e3) / 1e9
     # e2e: host DOF vector in, host result out, every step
     xh = torch.empty(mesh.n_dofs, dtype=torch.float64).pin_memory().uniform_(-1.0, 1.0)
@@ -873,7 +883,7 @@ def run_c0(args, ws, rank, dist, dev, wl, clk):
     peaks, src = _peaks()
     import paper_2604_04644_b200 as sk
 
-    bel = sk.operator_bytes(sk.OperatorKind.HELMHOLTZ_COLL, sk.Shape.HEX, P, True, LAM)
+    bel = sk.operator_bytes(sk.OperatorKind.HELMHOLTZ_COLL, sk.Shape.PRISM if prism else sk.Shape.HEX, P, True, LAM)
     step_bytes = bel * mesh.E + 2 * 8 * mesh.n_dofs
     achieved = step_bytes / (ms / 1e3 / args.steps) / 1e9
     clk.stop()
@@ -890,7 +900,7 @@ def run_c0(args, ws, rank, dist, dev, wl, clk):
             "scaling": "weak",
             "vs_baseline": None,
             "dtype": "f64",
-            "data": "synthetic (conforming deformed hex mesh, device geometry builder)",
+            "data": f"synthetic (conforming deformed {'prism' if prism else 'hex'} mesh, device geometry builder)",
             "config": {"workload": wl["name"], "elements_per_gpu": mesh.E, "global_dofs": n_global, "order": P,
                        "lam": LAM, "l2": f"inputs > L2 ({step_bytes / 1e9:.2f} GB per step per GPU), no flush",
                        "parallelism": f"z-slabs over {ws} GPU(s), NCCL P2P exchange of 2 DOF layers per step"},

@@ -162,6 +162,16 @@ int sk_c0_scatter(int order, int nx, int ny, int64_t nz_local, const double* loc
 int sk_helmholtz_apply_c0(const sk_basis* b, int geo_class, int nx, int ny, int64_t nz_local, const double* x,
                           const double* hpay, double lam, double* out, void* stream);
 
+/* Generic signed assembly maps (any shape; the prism C0 variant): gather
+ * local(e, m) = sgn[e*n_modes+m] * x[l2g[e*n_modes+m]] into the lane-major
+ * field layout of width W; scatter y[g] = sum over k in [ptr[g], ptr[g+1])
+ * of csr_sgn[k] * local(loc[k] / n_modes, loc[k] % n_modes) -- a gather per
+ * global DOF (deterministic, no atomics).  All arrays device-resident. */
+int sk_c0_gather_map(int64_t E, int n_modes, const int64_t* l2g, const double* sgn, const double* x, int W,
+                     double* local, void* stream);
+int sk_c0_scatter_map(int64_t n_dofs, int n_modes, const int64_t* ptr, const int64_t* loc, const double* csr_sgn,
+                      const double* local, int W, double* y, void* stream);
+
 /* ---- device memory (for callers without CUDA runtime bindings) --------------
  * The MemoryRegion DEVICE space of a reference Block (field_block.py:67-149)
  * held by a binding that loads only this library (integration/speckern_sk200.py).

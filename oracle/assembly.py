@@ -21,7 +21,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from oracle.elements import element
+from oracle.elements import element, mode_set
 from oracle.geom import deformed_geometry_from_coords, quadrature_xi
 from oracle.ops import helmholtz_coll
 
@@ -81,3 +81,135 @@ def assembled_helmholtz(nx: int, ny: int, nz: int, P: int, x: np.ndarray, lam: f
 
 def n_global(nx: int, ny: int, nz: int, P: int) -> int:
     return (nx * P + 1) * (ny * P + 1) * (nz * P + 1)
+
+
+# ---------------------------------------------------------------------------
+# Assembled C0 on a conforming prism mesh: a triangulated nx x nw grid of
+# unit squares in the (x, z) plane (two triangles per square), extruded along
+# y in nz element layers.  The prism's collapsed pair (xi1, xi3) spans the
+# triangle, xi2 the extrusion (shapes.py:374-405: modes (p, q, r), r <= P-p,
+# psi_a(p)(eta1) psi_a(q)(eta2) psi_b(p, r)(eta3), (0, q, 1) the collapsed
+# vertex).  The triangle's modal set is a hierarchical C0 basis: vertex
+# modes (0,0) V0, (1,0) V1, (0,1) V2; edge modes of degree k = 2..P on
+# V0V1 (p=k, r=0), V1V2 (p=1, r=k-1) and V0V2 (p=0, r=k), each tracing
+# psi_a(k) along its edge parameter from the lower to the higher local vertex;
+# interior modes p >= 2, r >= 1.  A shared edge traversed against its global
+# direction (lower global vertex id -> higher) flips the sign of its odd
+# modes; triangular faces between layers and the extrusion direction need no
+# orientation (every prism of a column uses the same triangle).
+
+
+def _tri_topology(nx: int, nw: int):
+    """Triangles as global vertex ids (V0, V1, V2) and 2D corner points;
+    square (ix, iw) -> lower (c00, c10, c01), upper (c11, c01, c10)."""
+    vid = lambda ix, iw: iw * (nx + 1) + ix  # noqa: E731
+    tris, pts = [], []
+    for iw in range(nw):
+        for ix in range(nx):
+            c00, c10, c01, c11 = (ix, iw), (ix + 1, iw), (ix, iw + 1), (ix + 1, iw + 1)
+            for v in ((c00, c10, c01), (c11, c01, c10)):
+                tris.append(tuple(vid(*c) for c in v))
+                pts.append(np.array(v, dtype=float))
+    return tris, pts
+
+
+def _tri_dofs(nx: int, nw: int, P: int):
+    """Per triangle: {(p, r): (2D global dof, sign)} and the 2D dof count."""
+    tris, _ = _tri_topology(nx, nw)
+    nv = (nx + 1) * (nw + 1)
+    edges: dict = {}
+    for t in tris:
+        for a, b in ((t[0], t[1]), (t[1], t[2]), (t[0], t[2])):
+            key = (min(a, b), max(a, b))
+            edges.setdefault(key, len(edges))
+    ni = (P - 1) * (P - 2) // 2
+    base_e, base_i = nv, nv + len(edges) * (P - 1)
+    out = []
+    for ti, t in enumerate(tris):
+        d = {(0, 0): (t[0], 1.0), (1, 0): (t[1], 1.0), (0, 1): (t[2], 1.0)}
+
+        def edge(a, b, k):
+            eid = edges[(min(a, b), max(a, b))]
+            sign = 1.0 if a < b else (-1.0) ** k
+            return base_e + eid * (P - 1) + (k - 2), sign
+
+        for k in range(2, P + 1):
+            d[(k, 0)] = edge(t[0], t[1], k)  # V0V1
+            d[(1, k - 1)] = edge(t[1], t[2], k)  # V1V2
+            d[(0, k)] = edge(t[0], t[2], k)  # V0V2
+        j = 0
+        for p in range(2, P + 1):
+            for r in range(1, P + 1 - p):
+                d[(p, r)] = (base_i + ti * ni + j, 1.0)
+                j += 1
+        out.append(d)
+    return out, base_i + len(tris) * ni
+
+
+def prism_n_global(nx: int, nw: int, nz: int, P: int) -> int:
+    return _tri_dofs(nx, nw, P)[1] * (nz * P + 1)
+
+
+def prism_local_to_global(nx: int, nw: int, nz: int, P: int, first_layer: int = 0, n_layers: int | None = None):
+    """(l2g, sign), both (E, NM), for elements e = ez_local * NT + t of the
+    layers [first_layer, first_layer + n_layers); global dofs of the slab
+    vector (layer-major: extrusion node * N2D + 2D dof)."""
+    tri, n2d = _tri_dofs(nx, nw, P)
+    nl = nz - first_layer if n_layers is None else n_layers
+    modes = mode_set("prism", P)
+    E = nl * len(tri)
+    l2g = np.empty((E, len(modes)), dtype=np.int64)
+    sgn = np.empty((E, len(modes)))
+    for ez in range(nl):
+        for t, d in enumerate(tri):
+            e = ez * len(tri) + t
+            for m, (p, q, r) in enumerate(modes):
+                layer = dof_1d(ez, q, P)  # slab-relative extrusion node
+                g2, s = d[(p, r)]
+                l2g[e, m] = layer * n2d + g2
+                sgn[e, m] = s
+    return l2g, sgn
+
+
+def prism_mesh_coords(nx: int, nw: int, P: int, ez_first: int, n_layers: int, amp: float = 0.05):
+    """(E, NQ, 3) quadrature coordinates: triangle point from barycentrics
+    (1 - l1 - l2, l1 = (1 + xi1)/2, l2 = (1 + xi3)/2) in the (x, z) plane,
+    y = layer + (1 + xi2)/2, then the global map x = X + amp sin(pi X_perm / 2)."""
+    el = element("prism", P)
+    xi = quadrature_xi(el)
+    _, pts = _tri_topology(nx, nw)
+    l1, l2 = 0.5 * (1.0 + xi[:, 0]), 0.5 * (1.0 + xi[:, 2])
+    l0 = 1.0 - l1 - l2
+    out = np.empty((n_layers * len(pts), el.nq, 3))
+    for ez in range(n_layers):
+        for t, v in enumerate(pts):
+            X = np.empty((el.nq, 3))
+            xz = l0[:, None] * v[0] + l1[:, None] * v[1] + l2[:, None] * v[2]
+            X[:, 0], X[:, 2] = xz[:, 0], xz[:, 1]
+            X[:, 1] = ez_first + ez + 0.5 * (1.0 + xi[:, 1])
+            out[ez * len(pts) + t] = X + amp * np.sin(0.5 * np.pi * X[:, [1, 2, 0]])
+    return out
+
+
+def assembled_helmholtz_prism(nx: int, nw: int, nz: int, P: int, x: np.ndarray, lam: float, amp: float = 0.05):
+    """y = sum_e A_e^T H_e A_e x with signed local-to-global maps (numpy)."""
+    el = element("prism", P)
+    geo = deformed_geometry_from_coords(el, prism_mesh_coords(nx, nw, P, 0, nz, amp))
+    l2g, sgn = prism_local_to_global(nx, nw, nz, P)
+    xe = (x[l2g] * sgn).T
+    ye = helmholtz_coll(el, geo, xe, lam)
+    y = np.zeros_like(x)
+    np.add.at(y, l2g.T.ravel(), (ye * sgn.T).ravel())
+    return y
+
+
+def prism_eval(P: int, coeffs: np.ndarray, eta: np.ndarray) -> np.ndarray:
+    """Expansion sum_m coeffs[m] phi_m at collapsed points eta (n, 3)
+    (shapes.py:374-405 mode factors)."""
+    from oracle.elements import _factor_fns
+
+    out = np.zeros(eta.shape[0])
+    for c, m in zip(coeffs, mode_set("prism", P)):
+        f = _factor_fns("prism", m)
+        out += c * f[0][0](eta[:, 0]) * f[1][0](eta[:, 1]) * f[2][0](eta[:, 2])
+    return out

@@ -29,7 +29,7 @@ from paper_2604_04644_b200.operators import helmholtz_apply
 from paper_2604_04644_b200.sharding import partition
 from paper_2604_04644_b200.shapes import Shape, build_shape_basis
 
-__all__ = ["C0HexMesh", "exchange_interfaces"]
+__all__ = ["C0HexMesh", "C0PrismMesh", "exchange_interfaces"]
 
 
 def exchange_interfaces(y, layer: int, group=None) -> None:
@@ -143,6 +143,141 @@ class C0HexMesh:
                               ctypes.c_void_p(y.data_ptr()), s),
             "sk_c0_scatter",
         )
+        exchange_interfaces(y, self.layer, group)
+        return y
+
+    def slab_slice(self) -> slice:
+        """This slab's range in the global DOF vector."""
+        start = self.z0 * self.P * self.layer
+        return slice(start, start + self.n_dofs)
+
+
+def _prism_tri_maps(nx: int, nw: int, P: int):
+    """2D part of the prism C0 numbering on the triangulated nx x nw grid of
+    unit squares (two triangles per square, lower (c00, c10, c01), upper
+    (c11, c01, c10); prism local (xi1, xi3) span the triangle).  Returns the
+    triangles' global vertex ids (NT, 3), their corner points (NT, 3, 2), the
+    2D dof and sign of every triangle mode (p, r) as dicts of (NT,) arrays,
+    and the 2D dof count.  Edge modes of degree k (V0V1: (k, 0), V1V2:
+    (1, k-1), V0V2: (0, k)) trace psi_a(k) from the lower to the higher local
+    vertex; against the global edge direction (lower -> higher global vertex
+    id) odd degrees flip sign.  Edges are numbered by first appearance."""
+    ix, iw = np.meshgrid(np.arange(nx), np.arange(nw), indexing="xy")
+    ix, iw = ix.ravel(), iw.ravel()
+    vid = lambda a, b: b * (nx + 1) + a  # noqa: E731
+    low = np.stack([vid(ix, iw), vid(ix + 1, iw), vid(ix, iw + 1)], axis=1)
+    up = np.stack([vid(ix + 1, iw + 1), vid(ix, iw + 1), vid(ix + 1, iw)], axis=1)
+    tris = np.stack([low, up], axis=1).reshape(-1, 3)
+    c = lambda a, b: np.stack([a, b], axis=-1).astype(float)  # noqa: E731
+    pts = np.stack([np.stack([c(ix, iw), c(ix + 1, iw), c(ix, iw + 1)], axis=1),
+                    np.stack([c(ix + 1, iw + 1), c(ix, iw + 1), c(ix + 1, iw)], axis=1)], axis=1).reshape(-1, 3, 2)
+    nt, nv = tris.shape[0], (nx + 1) * (nw + 1)
+    pairs = ((0, 1), (1, 2), (0, 2))
+    a = np.stack([tris[:, i] for i, _ in pairs], axis=1)  # (NT, 3) local edge start vertex
+    b = np.stack([tris[:, j] for _, j in pairs], axis=1)
+    key = (np.minimum(a, b) * nv + np.maximum(a, b)).ravel()
+    _, first, inv = np.unique(key, return_index=True, return_inverse=True)
+    rank = np.empty_like(first)
+    rank[np.argsort(first, kind="stable")] = np.arange(first.size)
+    eid = rank[inv].reshape(nt, 3)
+    fwd = a < b
+    ni = (P - 1) * (P - 2) // 2
+    base_e, base_i = nv, nv + first.size * (P - 1)
+    dof, sgn = {}, {}
+    for k, (p, r) in enumerate(((0, 0), (1, 0), (0, 1))):
+        dof[(p, r)], sgn[(p, r)] = tris[:, k], np.ones(nt)
+    for k in range(2, P + 1):
+        for le, (p, r) in enumerate(((k, 0), (1, k - 1), (0, k))):
+            dof[(p, r)] = base_e + eid[:, le] * (P - 1) + (k - 2)
+            sgn[(p, r)] = np.where(fwd[:, le], 1.0, (-1.0) ** k)
+    j = 0
+    for p in range(2, P + 1):
+        for r in range(1, P + 1 - p):
+            dof[(p, r)], sgn[(p, r)] = base_i + np.arange(nt) * ni + j, np.ones(nt)
+            j += 1
+    return tris, pts, dof, sgn, base_i + nt * ni
+
+
+class C0PrismMesh:
+    """This rank's slab of a conforming prism mesh: the triangulated nx x nw
+    grid of unit squares in the (x, z) plane extruded along y in nz element
+    layers (the slab axis), deformed by the same smooth global map as
+    C0HexMesh.  y = A^T H_e A x with signed maps: sk_c0_gather_map -> the
+    elemental collocated Helmholtz (prism kernels) -> sk_c0_scatter_map
+    (a deterministic per-DOF gather over a CSR list), then the exchange of
+    the two shared DOF layers with the neighbouring ranks.  Parity:
+    oracle/assembly.py (prism section), whose map is checked for
+    conformity on CPU."""
+
+    def __init__(self, nx: int, nw: int, nz: int, order: int, amp: float = 0.05, rank: int = 0, world: int = 1):
+        import torch
+
+        if nz < world:
+            raise ValueError(f"need at least one element layer per rank: nz={nz} < world={world}")
+        P = order
+        self.nx, self.nw, self.nz, self.P, self.amp = nx, nw, nz, P, amp
+        self.z0, self.nzl = partition(nz, world, rank)
+        tris, pts, dof2, sgn2, n2d = _prism_tri_maps(nx, nw, P)
+        nt = tris.shape[0]
+        self.layer = n2d  # DOFs of one extrusion node (the exchanged interface)
+        self.n_dofs = n2d * (self.nzl * P + 1)
+        self.E = self.nzl * nt
+        self.basis = build_shape_basis(Shape.PRISM, P)
+        modes = self.basis.modes
+        nm = len(modes)
+        pm = np.array([0 if q == 0 else P if q == 1 else q - 1 for q in range(P + 1)])
+        ez = np.arange(self.nzl)
+        l2g = np.empty((self.nzl, nt, nm), dtype=np.int64)
+        sgn = np.empty((self.nzl, nt, nm))
+        for m, (p, q, r) in enumerate(modes):
+            l2g[:, :, m] = (ez[:, None] * P + pm[q]) * n2d + dof2[(p, r)][None, :]
+            sgn[:, :, m] = sgn2[(p, r)][None, :]
+        l2g, sgn = l2g.reshape(-1), sgn.reshape(-1)
+        order_ = np.argsort(l2g, kind="stable")
+        ptr = np.zeros(self.n_dofs + 1, dtype=np.int64)
+        np.cumsum(np.bincount(l2g, minlength=self.n_dofs), out=ptr[1:])
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self._l2g = torch.as_tensor(l2g, device=dev)
+        self._sgn = torch.as_tensor(sgn, device=dev)
+        self._ptr = torch.as_tensor(ptr, device=dev)
+        self._loc = torch.as_tensor(order_.astype(np.int64), device=dev)
+        self._csgn = torch.as_tensor(sgn[order_], device=dev)
+        # quadrature coordinates: barycentrics of the triangle in (x, z),
+        # y = layer + (1 + xi2) / 2, then the global deformation
+        xi = torch.as_tensor(quadrature_coords(self.basis), device=dev)
+        l1, l2 = 0.5 * (1.0 + xi[:, 0]), 0.5 * (1.0 + xi[:, 2])
+        lw = torch.stack([1.0 - l1 - l2, l1, l2], dim=1)  # (NQ, 3)
+        v = torch.as_tensor(pts, device=dev)  # (NT, 3, 2)
+        xz = torch.einsum("qk,tkc->tqc", lw, v)  # (NT, NQ, 2)
+        yl = (self.z0 + torch.arange(self.nzl, device=dev, dtype=torch.float64))[:, None, None] + 0.5 * (1.0 + xi[None, :, 1:2])
+        X = torch.empty((self.nzl, nt, xi.shape[0], 3), dtype=torch.float64, device=dev)
+        X[..., 0] = xz[None, ..., 0]
+        X[..., 2] = xz[None, ..., 1]
+        X[..., 1] = yl.expand(self.nzl, xi.shape[0], 1)[:, None, :, 0]
+        X = X.reshape(self.E, xi.shape[0], 3)
+        coords = X + amp * torch.sin(0.5 * np.pi * X[..., [1, 2, 0]])
+        self.factors = deformed_factors_from_coords(self.basis, coords)
+        del coords, X
+        self.block = Block(self.basis, self.factors, FieldState.COEFF, 1, 1)
+        self.out = self.block.like(FieldState.COEFF)
+
+    def helmholtz(self, x, lam: float, group=None):
+        """y = A^T H_e A x for this slab's DOF vector x (CUDA, length
+        n_dofs); the shared end layers are summed across ranks."""
+        import torch
+
+        lib = _lib.load()
+        s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+        vp = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+        nm = self.basis.n_modes
+        local = self.block.device(AccessQualifier.WRITE_ONLY)
+        _lib.check(lib.sk_c0_gather_map(self.E, nm, vp(self._l2g), vp(self._sgn), vp(x), 1, vp(local), s),
+                   "sk_c0_gather_map")
+        helmholtz_apply(self.block, lam, out=self.out)
+        y = torch.empty(self.n_dofs, dtype=torch.float64, device=x.device)
+        loc = self.out.device(AccessQualifier.READ_ONLY)
+        _lib.check(lib.sk_c0_scatter_map(self.n_dofs, nm, vp(self._ptr), vp(self._loc), vp(self._csgn), vp(loc), 1,
+                                         vp(y), s), "sk_c0_scatter_map")
         exchange_interfaces(y, self.layer, group)
         return y
 

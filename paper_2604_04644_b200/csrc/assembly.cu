@@ -90,6 +90,31 @@ __global__ void k_c0_scatter(int P, int nx, int ny, long long nzl, const double*
   }
 }
 
+// ---- generic signed maps (any shape): gather through l2g / sign, scatter as
+// a gather over each global dof's CSR list of (element, mode) contributions
+__global__ void k_c0_gather_map(long long E, int nm, const long long* __restrict__ l2g,
+                                const double* __restrict__ sgn, const double* __restrict__ x, int W,
+                                double* __restrict__ local) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < E * nm; t += (long long)gridDim.x * blockDim.x) {
+    const long long e = t / nm;
+    const int m = (int)(t - e * nm);
+    local[lane_idx(e, m, nm, W)] = sgn[t] * __ldg(x + l2g[t]);
+  }
+}
+
+__global__ void k_c0_scatter_map(long long n, int nm, const long long* __restrict__ ptr,
+                                 const long long* __restrict__ loc, const double* __restrict__ sgn,
+                                 const double* __restrict__ local, int W, double* __restrict__ y) {
+  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < n; g += (long long)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (long long k = ptr[g]; k < ptr[g + 1]; ++k) {
+      const long long t = loc[k], e = t / nm;
+      s = fma(sgn[k], local[lane_idx(e, (int)(t - e * nm), nm, W)], s);
+    }
+    y[g] = s;
+  }
+}
+
 unsigned grid_for(long long n) {
   long long g = (n + 255) / 256;
   if (g > 148LL * 32) g = 148LL * 32;
@@ -118,6 +143,29 @@ int sk_c0_scatter(int order, int nx, int ny, int64_t nz_local, const double* loc
   const long long N = ((long long)nx * order + 1) * ((long long)ny * order + 1) * (nz_local * order + 1);
   sk::count_launch();
   k_c0_scatter<<<grid_for(N), 256, 0, static_cast<cudaStream_t>(stream)>>>(order, nx, ny, nz_local, local, W, y);
+  return cudaGetLastError() == cudaSuccess ? SK_OK : SK_ERR_CUDA;
+}
+
+int sk_c0_gather_map(int64_t E, int n_modes, const int64_t* l2g, const double* sgn, const double* x, int W,
+                     double* local, void* stream) {
+  if (E < 0 || n_modes < 1 || W < 1) return SK_ERR_ARG;
+  if (E == 0) return SK_OK;
+  if (!l2g || !sgn || !x || !local) return SK_ERR_ARG;
+  sk::count_launch();
+  k_c0_gather_map<<<grid_for(E * n_modes), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      E, n_modes, reinterpret_cast<const long long*>(l2g), sgn, x, W, local);
+  return cudaGetLastError() == cudaSuccess ? SK_OK : SK_ERR_CUDA;
+}
+
+int sk_c0_scatter_map(int64_t n_dofs, int n_modes, const int64_t* ptr, const int64_t* loc, const double* sgn,
+                      const double* local, int W, double* y, void* stream) {
+  if (n_dofs < 0 || n_modes < 1 || W < 1) return SK_ERR_ARG;
+  if (n_dofs == 0) return SK_OK;
+  if (!ptr || !loc || !sgn || !local || !y) return SK_ERR_ARG;
+  sk::count_launch();
+  k_c0_scatter_map<<<grid_for(n_dofs), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      n_dofs, n_modes, reinterpret_cast<const long long*>(ptr), reinterpret_cast<const long long*>(loc), sgn, local, W,
+      y);
   return cudaGetLastError() == cudaSuccess ? SK_OK : SK_ERR_CUDA;
 }
 

@@ -133,3 +133,45 @@ def test_two_ranks_c0_slabs_with_exchange(cuda, tmp_path):
         got = np.load(tmp_path / f"slab{r}_dev.npy")
         lo = z0 * P * layer
         assert O.rel_diff(got, ref[lo:lo + got.size]) <= 1e-12, r
+
+
+C0P = (3, 2, 5, 3)  # nx, nw, nz, P
+
+
+def _c0_prism_worker(rank, world, port, out_dir):
+    import torch
+    import torch.distributed as dist
+
+    import oracle.assembly as A
+    from paper_2604_04644_b200.assembly import C0PrismMesh
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    nx, nw, nz, P = C0P
+    mesh = C0PrismMesh(nx, nw, nz, P, rank=rank, world=world)
+    x = np.random.default_rng(4).standard_normal(A.prism_n_global(nx, nw, nz, P))
+    y = mesh.helmholtz(torch.from_numpy(x[mesh.slab_slice()].copy()).cuda(), 1.0)
+    np.save(os.path.join(out_dir, f"pslab{rank}.npy"), y.cpu().numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_ranks_c0_prism_slabs_with_exchange(cuda, tmp_path):
+    import torch.multiprocessing as mp
+
+    import oracle.assembly as A
+    from paper_2604_04644_b200.sharding import partition
+
+    world = 2
+    mp.start_processes(_c0_prism_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, start_method="spawn")
+    nx, nw, nz, P = C0P
+    n2d = A.prism_n_global(nx, nw, nz, P) // (nz * P + 1)
+    x = np.random.default_rng(4).standard_normal(A.prism_n_global(nx, nw, nz, P))
+    ref = A.assembled_helmholtz_prism(nx, nw, nz, P, x, 1.0)
+    for r in range(world):
+        z0, _ = partition(nz, world, r)
+        got = np.load(tmp_path / f"pslab{r}.npy")
+        lo = z0 * P * n2d
+        assert O.rel_diff(got, ref[lo:lo + got.size]) <= 1e-12, r
