@@ -81,6 +81,11 @@ WORKLOADS = {
                 "metric": "Assembled C0 Helmholtz apply GDOF/s (global DOFs, prism P=4, deformed, FP64)",
                 "name": "assembled C0 helmholtz prism P=4, 48x48 triangulated squares x 48 layers per GPU "
                         "(extrusion slabs), NCCL neighbour exchange of shared DOF layers (BASELINE configs[4])"},
+    # assembled C0 on Kuhn-split cubes (tets in global vertex order)
+    "c0tet": {"blocks": [("tet", 4, 6 * 40 * 40 * 40)],
+              "metric": "Assembled C0 Helmholtz apply GDOF/s (global DOFs, tet P=4, deformed, FP64)",
+              "name": "assembled C0 helmholtz tet P=4, 40^3 Kuhn-split cubes per GPU (z slabs), "
+                      "NCCL neighbour exchange of shared DOF planes (BASELINE configs[4])"},
     "c0hex": {"blocks": [("hex", 4, 64 * 64 * 64)],
               "metric": "Assembled C0 Helmholtz apply GDOF/s (global DOFs, hex P=4, deformed, FP64)",
               "name": "assembled C0 helmholtz hex P=4, 64x64x64 elements per GPU (z-slabs), "
@@ -610,7 +615,7 @@ def run_device(args, ws, rank, local):
     clk = Clocks(dev).start()  # sampling from before the warm-up on
     wl = WORKLOADS[args.workload]
     spec = [(s, P, args.elements or e) for s, P, e in wl["blocks"]]
-    if args.workload in ("c0hex", "c0prism"):
+    if args.workload in ("c0hex", "c0prism", "c0tet"):
         return run_c0(args, ws, rank, dist, dev, wl, clk)
 
     # every rank owns a contiguous slice of each block of the seeded mesh
@@ -835,7 +840,13 @@ def run_c0(args, ws, rank, dist, dev, wl, clk):
 
     P = 4
     prism = args.workload == "c0prism"
-    if prism:
+    tet = args.workload == "c0tet"
+    if tet:
+        from paper_2604_04644_b200.assembly import C0TetMesh
+
+        n = 40 if not args.elements else max(1, round((args.elements / 6) ** (1.0 / 3.0)))
+        mesh = C0TetMesh(n, n, n * ws, P, rank=rank, world=ws)
+    elif prism:
         n = 48 if not args.elements else max(1, round((args.elements / 2) ** (1.0 / 3.0)))
         mesh = C0PrismMesh(n, n, n * ws, P, rank=rank, world=ws)
     else:
@@ -865,7 +876,10 @@ def run_c0(args, ws, rank, dist, dev, wl, clk):
     if dist:
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
     ms_max = float(tmax.item())
-    n_global = mesh.layer * (n * ws * P + 1)  # DOF layers along the slab axis
+    if tet:  # plane + between-level DOFs per cube layer, plus the last plane
+        n_global = (mesh.n_dofs - mesh.layer) // mesh.nzl * (n * ws) + mesh.layer
+    else:
+        n_global = mesh.layer * (n * ws * P + 1)  # DOF layers along the slab axis
     value = n_global * args.steps / (ms_max / 1e3) / 1e9
     # e2e: host DOF vector in, host result out, every step
     xh = torch.empty(mesh.n_dofs, dtype=torch.float64).pin_memory().uniform_(-1.0, 1.0)
@@ -883,7 +897,8 @@ def run_c0(args, ws, rank, dist, dev, wl, clk):
     peaks, src = _peaks()
     import paper_2604_04644_b200 as sk
 
-    bel = sk.operator_bytes(sk.OperatorKind.HELMHOLTZ_COLL, sk.Shape.PRISM if prism else sk.Shape.HEX, P, True, LAM)
+    shp = sk.Shape.TET if tet else sk.Shape.PRISM if prism else sk.Shape.HEX
+    bel = sk.operator_bytes(sk.OperatorKind.HELMHOLTZ_COLL, shp, P, True, LAM)
     step_bytes = bel * mesh.E + 2 * 8 * mesh.n_dofs
     achieved = step_bytes / (ms / 1e3 / args.steps) / 1e9
     clk.stop()
@@ -900,7 +915,7 @@ def run_c0(args, ws, rank, dist, dev, wl, clk):
             "scaling": "weak",
             "vs_baseline": None,
             "dtype": "f64",
-            "data": f"synthetic (conforming deformed {'prism' if prism else 'hex'} mesh, device geometry builder)",
+            "data": f"synthetic (conforming deformed {shp.value} mesh, device geometry builder)",
             "config": {"workload": wl["name"], "elements_per_gpu": mesh.E, "global_dofs": n_global, "order": P,
                        "lam": LAM, "l2": f"inputs > L2 ({step_bytes / 1e9:.2f} GB per step per GPU), no flush",
                        "parallelism": f"z-slabs over {ws} GPU(s), NCCL P2P exchange of 2 DOF layers per step"},

@@ -90,6 +90,12 @@ int sk_payload_from_params(const sk_basis* b, int kind, int64_t E, const double*
 /* Iso-parametric factors from coordinates coords (E,NQ,3) (geometry.py:161-212). */
 int sk_geometry_from_coords(const sk_basis* b, int64_t E, const double* coords,
                             double* dxi_dx, double* jac, int64_t* n_bad, void* stream);
+/* Same for elements of either orientation: jac = w|det J| (*n_bad counts
+ * det J == 0 only).  Used by the assembled C0 tet mesh, whose tets take
+ * their vertices in global-id order so that shared faces and edges are
+ * parameterised alike on both sides (half of them are reflected). */
+int sk_geometry_from_coords_oriented(const sk_basis* b, int64_t E, const double* coords,
+                                     double* dxi_dx, double* jac, int64_t* n_bad, void* stream);
 
 /* ---- operators (SUM_FAC_TOP: one CTA per element tile) -------------------- */
 /* bwd_trans (operators.py:551-561): coeff -> phys, per component */

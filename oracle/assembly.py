@@ -213,3 +213,180 @@ def prism_eval(P: int, coeffs: np.ndarray, eta: np.ndarray) -> np.ndarray:
         f = _factor_fns("prism", m)
         out += c * f[0][0](eta[:, 0]) * f[1][0](eta[:, 1]) * f[2][0](eta[:, 2])
     return out
+
+
+# ---------------------------------------------------------------------------
+# Assembled C0 on a conforming tet mesh: nx x ny x nz unit cubes, each split
+# into the six Kuhn tets along its main diagonal; every tet takes its
+# vertices in global-id order (= the diagonal path order), so on every shared
+# edge and face both tets use the same vertex correspondence and the modified
+# basis (shapes.py:374-405) conforms with no signs or permutations: edge
+# modes of degree k trace psi_a(k) from the lower to the higher vertex, face
+# modes trace psi_a(a)(s) psi_b(a, b)(t) collapsed towards the face's highest
+# vertex.  Half of the tets are reflected: their factors use w|det J|
+# (deformed_geometry_from_coords(..., either_orientation=True)).
+# Global dofs are ordered by geometric level -- plane z=0, the entities
+# between z=0 and z=1, plane z=1, ... -- so a slab of cube layers owns one
+# contiguous range whose first / last plane is shared with its neighbours;
+# within a level, vertices, edges and faces in ascending sorted global
+# vertex ids, then the tets' interior modes.
+
+_KUHN = ((0, 1, 2), (0, 2, 1), (1, 0, 2), (1, 2, 0), (2, 0, 1), (2, 1, 0))
+
+
+def _tet_topology(nx: int, ny: int, nz: int):
+    """Tets (e = ((iz*ny + iy)*nx + ix)*6 + kuhn) as ascending global vertex
+    id 4-tuples, their vertex coordinates (4, 3) and the z of every vertex."""
+    vid = lambda x, y, z: (z * (ny + 1) + y) * (nx + 1) + x  # noqa: E731
+    tets, pts = [], []
+    for iz in range(nz):
+        for iy in range(ny):
+            for ix in range(nx):
+                for perm in _KUHN:
+                    c = [ix, iy, iz]
+                    vs = [tuple(c)]
+                    for ax in perm:
+                        c = list(c)
+                        c[ax] += 1
+                        vs.append(tuple(c))
+                    tets.append(tuple(vid(*v) for v in vs))
+                    pts.append(np.array(vs, dtype=float))
+    return tets, pts
+
+
+def _tet_mode_entity(P: int):
+    """Per local tet mode (p, q, r): ('v', i) | ('e', (i, j), k) | ('f', (i, j, l), idx) | ('i', idx)
+    with local vertex indices and the canonical face-mode index."""
+    face_ab = [(a, b) for a in range(2, P + 1) for b in range(1, P + 1 - a)]
+    fidx = {ab: i for i, ab in enumerate(face_ab)}
+    out, ni = [], 0
+    for p, q, r in mode_set("tet", P):
+        if (p, q, r) in ((0, 0, 0), (1, 0, 0), (0, 1, 0), (0, 0, 1)):
+            out.append(("v", [(0, 0, 0), (1, 0, 0), (0, 1, 0), (0, 0, 1)].index((p, q, r))))
+        elif q == 0 and r == 0:
+            out.append(("e", (0, 1), p))
+        elif p == 0 and r == 0:
+            out.append(("e", (0, 2), q))
+        elif p == 1 and r == 0:
+            out.append(("e", (1, 2), q + 1))
+        elif p == 0 and q == 0:
+            out.append(("e", (0, 3), r))
+        elif p == 1 and q == 0:
+            out.append(("e", (1, 3), r + 1))
+        elif p == 0 and q == 1:
+            out.append(("e", (2, 3), r + 1))
+        elif r == 0:
+            out.append(("f", (0, 1, 2), fidx[(p, q)]))
+        elif q == 0:
+            out.append(("f", (0, 1, 3), fidx[(p, r)]))
+        elif p == 0:
+            out.append(("f", (0, 2, 3), fidx[(q, r)]))
+        elif p == 1:
+            out.append(("f", (1, 2, 3), fidx[(q + 1, r)]))
+        else:
+            out.append(("i", ni))
+            ni += 1
+    return out, len(face_ab), ni
+
+
+def _tet_numbering(nx: int, ny: int, nz: int, P: int):
+    """Global dof of every (tet, local mode), the per-level dof offsets and
+    the plane size (dofs of one z = const plane)."""
+    tets, _ = _tet_topology(nx, ny, nz)
+    ent, nf, ni = _tet_mode_entity(P)
+    zof = lambda v: v // ((nx + 1) * (ny + 1))  # noqa: E731
+    size = {"v": 1, "e": P - 1, "f": nf}
+    levels: dict = {}  # level -> {(kind, verts): None}
+    for t in tets:
+        for kind, k in (("v", 1), ("e", 2), ("f", 3)):
+            for sub in _subsets(t, k):
+                zs = [zof(v) for v in sub]
+                lev = 2 * min(zs) + (0 if min(zs) == max(zs) else 1)
+                levels.setdefault(lev, {})[(kind, sub)] = None
+    order = {"v": 0, "e": 1, "f": 2}
+    start, offs = 0, {}
+    level_start = {}
+    for lev in range(2 * nz + 1):
+        level_start[lev] = start
+        ents = sorted(levels.get(lev, {}), key=lambda x: (order[x[0]], x[1]))
+        for kind, sub in ents:
+            offs[(kind, sub)] = start
+            start += size[kind]
+        if lev % 2 == 1:  # interiors of the tets of cube layer lev // 2
+            iz = lev // 2
+            for e in range(iz * nx * ny * 6, (iz + 1) * nx * ny * 6):
+                offs[("i", e)] = start
+                start += ni
+    level_start[2 * nz + 1] = start
+    l2g = np.empty((len(tets), len(ent)), dtype=np.int64)
+    for e, t in enumerate(tets):
+        for m, en in enumerate(ent):
+            if en[0] == "v":
+                l2g[e, m] = offs[("v", (t[en[1]],))]
+            elif en[0] == "e":
+                l2g[e, m] = offs[("e", tuple(t[i] for i in en[1]))] + en[2] - 2
+            elif en[0] == "f":
+                l2g[e, m] = offs[("f", tuple(t[i] for i in en[1]))] + en[2]
+            else:
+                l2g[e, m] = offs[("i", e)] + en[1]
+    plane = level_start[1] - level_start[0]
+    return l2g, level_start, plane
+
+
+def _subsets(t, k):
+    import itertools
+
+    return [tuple(c) for c in itertools.combinations(t, k)]
+
+
+def tet_n_global(nx: int, ny: int, nz: int, P: int) -> int:
+    return _tet_numbering(nx, ny, nz, P)[1][2 * nz + 1]
+
+
+def tet_mesh_coords(nx: int, ny: int, nz: int, P: int, amp: float = 0.05):
+    """(E, NQ, 3): affine image of the reference tet on each Kuhn tet
+    (x = v0 + sum_i (1 + xi_i)/2 (v_i - v0)), then the global deformation."""
+    el = element("tet", P)
+    xi = quadrature_xi(el)
+    _, pts = _tet_topology(nx, ny, nz)
+    lam = 0.5 * (1.0 + xi)  # (NQ, 3)
+    out = np.empty((len(pts), el.nq, 3))
+    for e, v in enumerate(pts):
+        X = v[0][None, :] + lam @ (v[1:] - v[0][None, :])
+        out[e] = X + amp * np.sin(0.5 * np.pi * X[:, [1, 2, 0]])
+    return out
+
+
+def assembled_helmholtz_tet(nx: int, ny: int, nz: int, P: int, x: np.ndarray, lam: float, amp: float = 0.05):
+    """y = sum_e A_e^T H_e A_e x (numpy), factors with w|det J|."""
+    el = element("tet", P)
+    geo = deformed_geometry_from_coords(el, tet_mesh_coords(nx, ny, nz, P, amp), either_orientation=True)
+    l2g, _, _ = _tet_numbering(nx, ny, nz, P)
+    ye = helmholtz_coll(el, geo, x[l2g].T, lam)
+    y = np.zeros_like(x)
+    np.add.at(y, l2g.T.ravel(), ye.ravel())
+    return y
+
+
+def tet_eval(P: int, coeffs: np.ndarray, eta: np.ndarray) -> np.ndarray:
+    """Tet expansion at collapsed points eta (n, 3)."""
+    from oracle.elements import _factor_fns
+
+    out = np.zeros(eta.shape[0])
+    for c, m in zip(coeffs, mode_set("tet", P)):
+        f = _factor_fns("tet", m)
+        out += c * f[0][0](eta[:, 0]) * f[1][0](eta[:, 1]) * f[2][0](eta[:, 2])
+    return out
+
+
+TET_REF = np.array([[-1.0, -1.0, -1.0], [1.0, -1.0, -1.0], [-1.0, 1.0, -1.0], [-1.0, -1.0, 1.0]])
+
+
+def tet_collapse(xi: np.ndarray) -> np.ndarray:
+    """Duffy map xi -> eta of the tet (shapes.py:218-239), away from the
+    collapsed points."""
+    eta = np.empty_like(xi)
+    eta[:, 0] = 2.0 * (1.0 + xi[:, 0]) / (-xi[:, 1] - xi[:, 2]) - 1.0
+    eta[:, 1] = 2.0 * (1.0 + xi[:, 1]) / (1.0 - xi[:, 2]) - 1.0
+    eta[:, 2] = xi[:, 2]
+    return eta

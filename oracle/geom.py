@@ -56,9 +56,11 @@ def affine_geometry(shape: str, verts: np.ndarray) -> Geometry:
     return Geometry(False, np.linalg.inv(jm), det)
 
 
-def deformed_geometry_from_coords(el: RefElement, coords: np.ndarray) -> Geometry:
+def deformed_geometry_from_coords(el: RefElement, coords: np.ndarray, either_orientation: bool = False) -> Geometry:
     """Iso-parametric factors (geometry.py:161-212): collocation derivatives
-    on the collapsed grid, Duffy chain rule, pointwise det/inverse."""
+    on the collapsed grid, Duffy chain rule, pointwise det/inverse.
+    ``either_orientation`` (assembled tet mesh only): w|det J| for reflected
+    elements instead of the reference's rejection."""
     coords = np.asarray(coords, dtype=float)
     ne = coords.shape[0]
     full = coords.reshape(ne, *el.q, 3)
@@ -81,6 +83,8 @@ def deformed_geometry_from_coords(el: RefElement, coords: np.ndarray) -> Geometr
                 else:
                     jm[..., j] += dxdeta[..., m] * g[None, :, None]
     det = np.linalg.det(jm)
+    if either_orientation:
+        det = np.abs(det)
     if np.any(det <= 0.0):
         raise ValueError("nonpositive Jacobian")
     return Geometry(True, np.linalg.inv(jm), el.refw[None, :] * det)

@@ -38,6 +38,7 @@ SIGNATURES = {
     "sk_geometry_deformed": (_I, [_P, _L, _P, _P, _P, _PL, _P]),
     "sk_payload_from_params": (_I, [_P, _I, _L, _P, _P, _PL, _P]),
     "sk_geometry_from_coords": (_I, [_P, _L, _P, _P, _P, _PL, _P]),
+    "sk_geometry_from_coords_oriented": (_I, [_P, _L, _P, _P, _P, _PL, _P]),
     "sk_bwd_trans": (_I, [_P, _L, _I, _I, _P, _P, _P]),
     "sk_iproduct_wrt_base": (_I, [_P, _I, _L, _I, _I, _P, _P, _P, _P]),
     "sk_phys_deriv": (_I, [_P, _I, _L, _I, _P, _P, _P, _P]),

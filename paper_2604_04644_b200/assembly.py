@@ -29,7 +29,7 @@ from paper_2604_04644_b200.operators import helmholtz_apply
 from paper_2604_04644_b200.sharding import partition
 from paper_2604_04644_b200.shapes import Shape, build_shape_basis
 
-__all__ = ["C0HexMesh", "C0PrismMesh", "exchange_interfaces"]
+__all__ = ["C0HexMesh", "C0PrismMesh", "C0TetMesh", "exchange_interfaces"]
 
 
 def exchange_interfaces(y, layer: int, group=None) -> None:
@@ -284,4 +284,168 @@ class C0PrismMesh:
     def slab_slice(self) -> slice:
         """This slab's range in the global DOF vector."""
         start = self.z0 * self.P * self.layer
+        return slice(start, start + self.n_dofs)
+
+
+_KUHN = ((0, 1, 2), (0, 2, 1), (1, 0, 2), (1, 2, 0), (2, 0, 1), (2, 1, 0))
+_TET_EDGES = ((0, 1), (0, 2), (1, 2), (0, 3), (1, 3), (2, 3))
+_TET_FACES = ((0, 1, 2), (0, 1, 3), (0, 2, 3), (1, 2, 3))
+
+
+def _tet_mode_table(P: int):
+    """Entity of every local tet mode (p, q, r) (shapes.py:374-405 modes):
+    (kind, local index, sub-index) with kind 0 vertex (index into the 4
+    vertices), 1 edge (into _TET_EDGES; sub-index degree - 2), 2 face (into
+    _TET_FACES; sub-index of the face's canonical (a, b) mode, a >= 2,
+    b >= 1), 3 interior.  Edge / face modes trace psi_a along the edge from
+    the lower vertex, psi_a(a) psi_b(a, b) on the face collapsed towards its
+    highest vertex, so elements whose vertices are in global-id order agree
+    on every shared entity."""
+    face_ab = {ab: i for i, ab in enumerate((a, b) for a in range(2, P + 1) for b in range(1, P + 1 - a))}
+    out, ni = [], 0
+    for p in range(P + 1):
+        for q in range(P + 1 - p):
+            for r in range(P + 1 - p - q):
+                verts = {(0, 0, 0): 0, (1, 0, 0): 1, (0, 1, 0): 2, (0, 0, 1): 3}
+                if (p, q, r) in verts:
+                    out.append((0, verts[(p, q, r)], 0))
+                elif q == 0 and r == 0:
+                    out.append((1, 0, p - 2))
+                elif p == 0 and r == 0:
+                    out.append((1, 1, q - 2))
+                elif p == 1 and r == 0:
+                    out.append((1, 2, q - 1))
+                elif p == 0 and q == 0:
+                    out.append((1, 3, r - 2))
+                elif p == 1 and q == 0:
+                    out.append((1, 4, r - 1))
+                elif p == 0 and q == 1:
+                    out.append((1, 5, r - 1))
+                elif r == 0:
+                    out.append((2, 0, face_ab[(p, q)]))
+                elif q == 0:
+                    out.append((2, 1, face_ab[(p, r)]))
+                elif p == 0:
+                    out.append((2, 2, face_ab[(q, r)]))
+                elif p == 1:
+                    out.append((2, 3, face_ab[(q + 1, r)]))
+                else:
+                    out.append((3, 0, ni))
+                    ni += 1
+    return out, len(face_ab), ni
+
+
+def _tet_maps(nx: int, ny: int, nz: int, z0: int, nzl: int, P: int):
+    """Numbering of the C0 tet mesh slab of cube layers [z0, z0 + nzl) (see
+    C0TetMesh): vertex coordinates (E, 4, 3) of its Kuhn tets, the
+    slab-relative global dof of every (tet, local mode), the slab's dof
+    count and the dofs of one z plane."""
+    nxy = (nx + 1) * (ny + 1)
+    nv = nxy * (nz + 1)
+    # Kuhn tets of the slab (cubes x fastest, then y, then z), vertices
+    # ascending = the path along the cube's main diagonal
+    ix, iy, iz = np.meshgrid(np.arange(nx), np.arange(ny), z0 + np.arange(nzl), indexing="ij")
+    base = np.stack([ix.T.ravel(), iy.T.ravel(), iz.T.ravel()], axis=1)  # (cubes, 3)
+    steps = np.eye(3, dtype=np.int64)
+    corners = []
+    for perm in _KUHN:
+        path = [np.zeros(3, dtype=np.int64)]
+        for ax in perm:
+            path.append(path[-1] + steps[ax])
+        corners.append(np.stack(path))
+    pts = (base[:, None, None, :] + np.stack(corners)[None]).reshape(-1, 4, 3)
+    verts = (pts[..., 2] * (ny + 1) + pts[..., 1]) * (nx + 1) + pts[..., 0]
+    E = verts.shape[0]
+    # every entity occurrence as (level, kind, key): level 2z for entities in
+    # the plane z, 2z+1 between z and z+1; key = sorted vertex ids
+    recs = []
+    for kind, subs in ((0, ((0,), (1,), (2,), (3,))), (1, _TET_EDGES), (2, _TET_FACES)):
+        arr = np.stack([verts[:, list(sub)] for sub in subs], axis=1)  # (E, n, k)
+        z = arr // nxy
+        lev = 2 * z.min(axis=-1) + (z.min(axis=-1) != z.max(axis=-1))
+        key = np.zeros(arr.shape[:2], dtype=np.int64)
+        for c in range(arr.shape[-1]):
+            key = key * nv + arr[..., c]
+        recs.append((lev, np.full(arr.shape[:2], kind), key))
+    cz = verts[:, 0] // nxy  # cube layer of each tet: its interior modes
+    recs.append(((2 * cz + 1)[:, None], np.full((E, 1), 3), np.arange(E, dtype=np.int64)[:, None]))
+    lev = np.concatenate([r[0].ravel() for r in recs])
+    kind = np.concatenate([r[1].ravel() for r in recs])
+    key = np.concatenate([r[2].ravel() for r in recs])
+    order_ = np.lexsort((key, kind, lev))
+    srt = np.stack([lev[order_], kind[order_], key[order_]], axis=1)
+    new = np.ones(len(srt), dtype=bool)
+    new[1:] = np.any(srt[1:] != srt[:-1], axis=1)
+    uid = np.empty(len(srt), dtype=np.int64)
+    uid[order_] = np.cumsum(new) - 1
+    modes, nf, ni = _tet_mode_table(P)
+    usize = np.array([1, P - 1, nf, ni])[srt[new, 1]]
+    uoff = np.concatenate([[0], np.cumsum(usize)[:-1]])
+    n_dofs = int(usize.sum())
+    layer = nxy + (nx * (ny + 1) + (nx + 1) * ny + nx * ny) * (P - 1) + 2 * nx * ny * nf  # one z plane
+    cut = np.cumsum([0, E * 4, E * 6, E * 4, E])
+    ent = [uid[cut[k]:cut[k + 1]].reshape(E, -1) for k in range(4)]
+    l2g = np.empty((E, len(modes)), dtype=np.int64)
+    for m, (k, li, sub) in enumerate(modes):
+        l2g[:, m] = uoff[ent[k][:, li]] + sub
+    return pts, l2g, n_dofs, layer
+
+
+class C0TetMesh:
+    """This rank's slab of a conforming tet mesh: nx x ny x nz unit cubes,
+    each split into the six Kuhn tets along its main diagonal, every tet
+    taking its vertices in global-id order (so shared edges and faces are
+    parameterised alike on both sides; the reflected half gets w|det J|,
+    sk_geometry_from_coords_oriented), deformed by the global map of
+    C0HexMesh.  Global DOFs are ordered by geometric level (plane z, the
+    entities between z and z+1, ...; within a level vertices, edges, faces
+    by sorted global vertex ids, then the tets' interior modes), so a slab of
+    cube layers is one contiguous range whose end planes are shared with the
+    neighbouring ranks.  y = A^T H_e A x by sk_c0_gather_map -> the tet
+    kernels -> sk_c0_scatter_map, then the plane exchange.  Parity:
+    oracle/assembly.py (tet section, conformity-checked on CPU)."""
+
+    def __init__(self, nx: int, ny: int, nz: int, order: int, amp: float = 0.05, rank: int = 0, world: int = 1):
+        import torch
+
+        if nz < world:
+            raise ValueError(f"need at least one element layer per rank: nz={nz} < world={world}")
+        P = order
+        self.nx, self.ny, self.nz, self.P, self.amp = nx, ny, nz, P, amp
+        self.z0, self.nzl = partition(nz, world, rank)
+        pts, l2g, self.n_dofs, self.layer = _tet_maps(nx, ny, nz, self.z0, self.nzl, P)
+        E = pts.shape[0]
+        self.E = E
+        self.basis = build_shape_basis(Shape.TET, P)
+        assert l2g.shape[1] == self.basis.n_modes
+        l2g = l2g.reshape(-1)
+        order_ = np.argsort(l2g, kind="stable")
+        ptr = np.zeros(self.n_dofs + 1, dtype=np.int64)
+        np.cumsum(np.bincount(l2g, minlength=self.n_dofs), out=ptr[1:])
+        dev = torch.device("cuda", torch.cuda.current_device())
+        ones = torch.ones(l2g.size, dtype=torch.float64, device=dev)
+        self._l2g = torch.as_tensor(l2g, device=dev)
+        self._sgn = ones
+        self._ptr = torch.as_tensor(ptr, device=dev)
+        self._loc = torch.as_tensor(order_.astype(np.int64), device=dev)
+        self._csgn = ones
+        # quadrature coordinates: affine image of the reference tet, then the
+        # global deformation
+        xi = torch.as_tensor(quadrature_coords(self.basis), device=dev)
+        lam = 0.5 * (1.0 + xi)  # (NQ, 3)
+        v = torch.as_tensor(pts, dtype=torch.float64, device=dev)  # (E, 4, 3)
+        X = v[:, None, 0, :] + torch.einsum("qk,ekc->eqc", lam, v[:, 1:, :] - v[:, :1, :])
+        coords = X + amp * torch.sin(0.5 * np.pi * X[..., [1, 2, 0]])
+        self.factors = deformed_factors_from_coords(self.basis, coords, either_orientation=True)
+        del coords, X
+        self.block = Block(self.basis, self.factors, FieldState.COEFF, 1, 1)
+        self.out = self.block.like(FieldState.COEFF)
+
+    helmholtz = C0PrismMesh.helmholtz
+
+    def slab_slice(self) -> slice:
+        """This slab's range in the global DOF vector (cube layers [z0, z0 +
+        nzl): every level between plane z0 and plane z0 + nzl)."""
+        per_layer = self.n_dofs - self.layer  # plane + between-level dofs of one cube layer
+        start = self.z0 * (per_layer // self.nzl)
         return slice(start, start + self.n_dofs)

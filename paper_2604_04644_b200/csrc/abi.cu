@@ -337,6 +337,11 @@ int sk_geometry_from_coords(const sk_basis* b, int64_t E, const double* coords, 
   return geometry_common(b, 0, E, coords, dxi, jac, -1, nullptr, n_bad, stream);
 }
 
+int sk_geometry_from_coords_oriented(const sk_basis* b, int64_t E, const double* coords, double* dxi, double* jac,
+                                     int64_t* n_bad, void* stream) {
+  return geometry_common(b, 2, E, coords, dxi, jac, -1, nullptr, n_bad, stream);
+}
+
 int sk_payload_from_params(const sk_basis* b, int kind, int64_t E, const double* params, double* pay,
                            int64_t* n_bad, void* stream) {
   if (kind < 0 || kind > 3) return fail(SK_ERR_ARG, "bad payload kind");

@@ -678,7 +678,7 @@ __global__ void __launch_bounds__(128) k_geom(long long E, const double* __restr
   for (long long e = blockIdx.x; e < E; e += gridDim.x) {
     __syncthreads();
     for (int l = threadIdx.x; l < NQ; l += blockDim.x) {
-      if (MODE == 0) {
+      if (MODE != 1) {  // coordinates (MODE 2: either orientation)
 #pragma unroll
         for (int c = 0; c < 3; ++c) x[c][l] = src[(e * NQ + l) * 3 + c];
       } else {
@@ -738,7 +738,9 @@ __global__ void __launch_bounds__(128) k_geom(long long E, const double* __restr
       const double c01 = J[1][2] * J[2][0] - J[1][0] * J[2][2];
       const double c02 = J[1][0] * J[2][1] - J[1][1] * J[2][0];
       const double det = J[0][0] * c00 + J[0][1] * c01 + J[0][2] * c02;
-      if (!(det > 0.0)) atomicAdd(bad, 1ULL);
+      // MODE 2 accepts reflected elements (the assembled tet mesh orders each
+      // tet's vertices by global id): the weight uses |det J|
+      if (!(MODE == 2 ? fabs(det) > 0.0 : det > 0.0)) atomicAdd(bad, 1ULL);
       const double id = 1.0 / det;
       double inv[3][3];
       inv[0][0] = c00 * id;
@@ -750,7 +752,7 @@ __global__ void __launch_bounds__(128) k_geom(long long E, const double* __restr
       inv[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) * id;
       inv[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) * id;
       inv[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) * id;
-      const double wjac = gtab[GLayout<S, P>::REFW + l] * det;
+      const double wjac = gtab[GLayout<S, P>::REFW + l] * (MODE == 2 ? fabs(det) : det);
       if (dxi_out) {
 #pragma unroll
         for (int a = 0; a < 3; ++a)
@@ -771,6 +773,8 @@ int geometry(int mode, long long E, const double* src, double* dxi, double* jac,
   long long g = E < 148LL * 32 ? E : 148LL * 32;
   if (mode == 0)
     k_geom<S, P, 0><<<(unsigned)g, 128, 0, s>>>(E, src, dxi, jac, kind, pay, bad, gtab);
+  else if (mode == 2)
+    k_geom<S, P, 2><<<(unsigned)g, 128, 0, s>>>(E, src, dxi, jac, kind, pay, bad, gtab);
   else
     k_geom<S, P, 1><<<(unsigned)g, 128, 0, s>>>(E, src, dxi, jac, kind, pay, bad, gtab);
   return (int)cudaGetLastError();

@@ -43,7 +43,8 @@ struct OpSet {
   long long (*payload_elements)(int kind, long long E);  // elements incl. lane padding
   int (*pack)(int kind, int geo, long long E, const double* dxi, const double* jac, double* pay,
               const double* gtab, void* stream);
-  // geometry builder: mode 0 from coords (E,NQ,3), mode 1 from params (E,12).
+  // geometry builder: mode 0 from coords (E,NQ,3), mode 1 from params (E,12),
+  // mode 2 from coords accepting either orientation (w|det J|).
   // Writes dxi/jac (either may be null) and/or the payload of `kind`
   // (kind < 0: none).  Counts nonpositive-Jacobian points into *bad (device).
   int (*geometry)(int mode, long long E, const double* src, double* dxi, double* jac, int kind,

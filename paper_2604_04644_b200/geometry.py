@@ -217,9 +217,11 @@ def quadrature_coords(basis: ShapeBasis) -> np.ndarray:
     return xi
 
 
-def deformed_factors_from_coords(basis: ShapeBasis, coords) -> GeometricFactors:
+def deformed_factors_from_coords(basis: ShapeBasis, coords, either_orientation: bool = False) -> GeometricFactors:
     """Per-point factors from coordinates (E, NQ, 3) on the device
-    (geometry.py:161-212)."""
+    (geometry.py:161-212).  ``either_orientation``: accept reflected
+    elements with w|det J| (the assembled tet mesh; the reference rejects
+    det J <= 0)."""
     torch = _torch()
     c = torch.as_tensor(np.asarray(coords, dtype=float) if not hasattr(coords, "data_ptr") else coords)
     if c.dim() == 2:
@@ -232,10 +234,8 @@ def deformed_factors_from_coords(basis: ShapeBasis, coords) -> GeometricFactors:
     dxi = torch.empty((E, basis.n_points, 3, 3), dtype=torch.float64, device=dev)
     jac = torch.empty((E, basis.n_points), dtype=torch.float64, device=dev)
     bad = ctypes.c_int64()
-    _lib.check(
-        _lib.load().sk_geometry_from_coords(basis.handle, E, _ptr(c), _ptr(dxi), _ptr(jac), ctypes.byref(bad), _stream()),
-        "sk_geometry_from_coords",
-    )
+    fn = _lib.load().sk_geometry_from_coords_oriented if either_orientation else _lib.load().sk_geometry_from_coords
+    _lib.check(fn(basis.handle, E, _ptr(c), _ptr(dxi), _ptr(jac), ctypes.byref(bad), _stream()), "sk_geometry_from_coords")
     if bad.value:
         raise DegenerateElementError(f"{bad.value} quadrature points with nonpositive Jacobian")
     return GeometricFactors(GeometryClass.DEFORMED, basis.shape, E, dxi, jac)

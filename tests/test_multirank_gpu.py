@@ -175,3 +175,43 @@ def test_two_ranks_c0_prism_slabs_with_exchange(cuda, tmp_path):
         got = np.load(tmp_path / f"pslab{r}.npy")
         lo = z0 * P * n2d
         assert O.rel_diff(got, ref[lo:lo + got.size]) <= 1e-12, r
+
+
+C0T = (2, 2, 4, 3)  # nx, ny, nz, P
+
+
+def _c0_tet_worker(rank, world, port, out_dir):
+    import torch
+    import torch.distributed as dist
+
+    import oracle.assembly as A
+    from paper_2604_04644_b200.assembly import C0TetMesh
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    nx, ny, nz, P = C0T
+    mesh = C0TetMesh(nx, ny, nz, P, rank=rank, world=world)
+    x = np.random.default_rng(5).standard_normal(A.tet_n_global(nx, ny, nz, P))
+    y = mesh.helmholtz(torch.from_numpy(x[mesh.slab_slice()].copy()).cuda(), 1.0)
+    np.save(os.path.join(out_dir, f"tslab{rank}.npy"), y.cpu().numpy())
+    np.save(os.path.join(out_dir, f"tslice{rank}.npy"), np.array([mesh.slab_slice().start, mesh.slab_slice().stop]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_ranks_c0_tet_slabs_with_exchange(cuda, tmp_path):
+    import torch.multiprocessing as mp
+
+    import oracle.assembly as A
+
+    world = 2
+    mp.start_processes(_c0_tet_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, start_method="spawn")
+    nx, ny, nz, P = C0T
+    x = np.random.default_rng(5).standard_normal(A.tet_n_global(nx, ny, nz, P))
+    ref = A.assembled_helmholtz_tet(nx, ny, nz, P, x, 1.0)
+    for r in range(world):
+        got = np.load(tmp_path / f"tslab{r}.npy")
+        lo, hi = np.load(tmp_path / f"tslice{r}.npy")
+        assert O.rel_diff(got, ref[lo:hi]) <= 1e-12, r
