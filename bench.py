@@ -86,6 +86,11 @@ WORKLOADS = {
               "metric": "Assembled C0 Helmholtz apply GDOF/s (global DOFs, tet P=4, deformed, FP64)",
               "name": "assembled C0 helmholtz tet P=4, 40^3 Kuhn-split cubes per GPU (z slabs), "
                       "NCCL neighbour exchange of shared DOF planes (BASELINE configs[4])"},
+    # assembled C0 on six pyramids per cube (apex at the centre)
+    "c0pyr": {"blocks": [("pyr", 4, 6 * 40 * 40 * 40)],
+              "metric": "Assembled C0 Helmholtz apply GDOF/s (global DOFs, pyr P=4, deformed, FP64)",
+              "name": "assembled C0 helmholtz pyr P=4, 40^3 cubes x 6 pyramids per GPU (z slabs), "
+                      "NCCL neighbour exchange of shared DOF planes (BASELINE configs[4])"},
     "c0hex": {"blocks": [("hex", 4, 64 * 64 * 64)],
               "metric": "Assembled C0 Helmholtz apply GDOF/s (global DOFs, hex P=4, deformed, FP64)",
               "name": "assembled C0 helmholtz hex P=4, 64x64x64 elements per GPU (z-slabs), "
@@ -615,7 +620,7 @@ def run_device(args, ws, rank, local):
     clk = Clocks(dev).start()  # sampling from before the warm-up on
     wl = WORKLOADS[args.workload]
     spec = [(s, P, args.elements or e) for s, P, e in wl["blocks"]]
-    if args.workload in ("c0hex", "c0prism", "c0tet"):
+    if args.workload in ("c0hex", "c0prism", "c0tet", "c0pyr"):
         return run_c0(args, ws, rank, dist, dev, wl, clk)
 
     # every rank owns a contiguous slice of each block of the seeded mesh
@@ -840,12 +845,13 @@ def run_c0(args, ws, rank, dist, dev, wl, clk):
 
     P = 4
     prism = args.workload == "c0prism"
-    tet = args.workload == "c0tet"
+    tet = args.workload in ("c0tet", "c0pyr")  # cube meshes with level-ordered DOFs
     if tet:
-        from paper_2604_04644_b200.assembly import C0TetMesh
+        from paper_2604_04644_b200.assembly import C0PyrMesh, C0TetMesh
 
         n = 40 if not args.elements else max(1, round((args.elements / 6) ** (1.0 / 3.0)))
-        mesh = C0TetMesh(n, n, n * ws, P, rank=rank, world=ws)
+        cls = C0TetMesh if args.workload == "c0tet" else C0PyrMesh
+        mesh = cls(n, n, n * ws, P, rank=rank, world=ws)
     elif prism:
         n = 48 if not args.elements else max(1, round((args.elements / 2) ** (1.0 / 3.0)))
         mesh = C0PrismMesh(n, n, n * ws, P, rank=rank, world=ws)
@@ -897,7 +903,7 @@ def run_c0(args, ws, rank, dist, dev, wl, clk):
     peaks, src = _peaks()
     import paper_2604_04644_b200 as sk
 
-    shp = sk.Shape.TET if tet else sk.Shape.PRISM if prism else sk.Shape.HEX
+    shp = mesh.basis.shape
     bel = sk.operator_bytes(sk.OperatorKind.HELMHOLTZ_COLL, shp, P, True, LAM)
     step_bytes = bel * mesh.E + 2 * 8 * mesh.n_dofs
     achieved = step_bytes / (ms / 1e3 / args.steps) / 1e9

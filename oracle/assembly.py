@@ -390,3 +390,174 @@ def tet_collapse(xi: np.ndarray) -> np.ndarray:
     eta[:, 1] = 2.0 * (1.0 + xi[:, 1]) / (1.0 - xi[:, 2]) - 1.0
     eta[:, 2] = xi[:, 2]
     return eta
+
+
+# ---------------------------------------------------------------------------
+# Assembled C0 on a conforming pyramid mesh: nx x ny x nz unit cubes, each
+# split into six pyramids with the cube centre as apex and a cube face as
+# base.  Every pyramid's base axes (eta1, eta2) run along the face's two
+# global axes (lower axis first) in increasing direction from the face's
+# minimum corner (V0), so shared base quads, shared triangular faces (base
+# edge + apex) and every edge are parameterised alike on both sides
+# (shapes.py:374-405 pyramid modes: psi_a(p) psi_a(q) psi_b(max(p,q), r),
+# (0,0,1) the apex); reflected pyramids use w|det J|.  Dofs are ordered by
+# level like the tet mesh (corner z = iz, cube centres between).
+
+_PYR_FACES = ((0, 0), (0, 1), (1, 0), (1, 1), (2, 0), (2, 1))  # (normal axis, side)
+
+
+def _pyr_topology(nx: int, ny: int, nz: int):
+    """Pyramids (e = cube * 6 + face) as vertex id 5-tuples (V0..V3 base,
+    V4 apex; corners (z*(ny+1)+y)*(nx+1)+x, centres n_corners + cube),
+    their doubled-z levels and vertex coordinates (5, 3)."""
+    nc = (nx + 1) * (ny + 1) * (nz + 1)
+    vid = lambda c: (c[2] * (ny + 1) + c[1]) * (nx + 1) + c[0]  # noqa: E731
+    pyrs, pts, z2 = [], [], []
+    cube = 0
+    for iz in range(nz):
+        for iy in range(ny):
+            for ix in range(nx):
+                o = np.array([ix, iy, iz])
+                for n, side in _PYR_FACES:
+                    a, b = [ax for ax in range(3) if ax != n]
+                    v0 = o.copy()
+                    v0[n] += side
+                    ea, eb = np.eye(3, dtype=int)[a], np.eye(3, dtype=int)[b]
+                    base = [v0, v0 + ea, v0 + ea + eb, v0 + eb]
+                    pyrs.append(tuple(vid(c) for c in base) + (nc + cube,))
+                    pts.append(np.array([*base, o + 0.5], dtype=float))
+                    z2.append(tuple(2 * c[2] for c in base) + (2 * iz + 1,))
+                cube += 1
+    return pyrs, pts, z2
+
+
+def _pyr_mode_entity(P: int):
+    """Per local pyramid mode: ('v', i) | ('e', (i, j), degree) |
+    ('q', canonical quad index) | ('t', (i, j, k), canonical triangle index) | ('i', idx)."""
+    tri = {ab: i for i, ab in enumerate((a, b) for a in range(2, P + 1) for b in range(1, P + 1 - a))}
+    quad = {pq: i for i, pq in enumerate((p, q) for p in range(2, P + 1) for q in range(2, P + 1))}
+    vert = {(0, 0, 0): 0, (1, 0, 0): 1, (1, 1, 0): 2, (0, 1, 0): 3, (0, 0, 1): 4}
+    out, ni = [], 0
+    for p, q, r in mode_set("pyr", P):
+        if (p, q, r) in vert:
+            out.append(("v", vert[(p, q, r)]))
+        elif r == 0 and q in (0, 1) and p >= 2:
+            out.append(("e", (0, 1) if q == 0 else (3, 2), p))
+        elif r == 0 and p in (0, 1) and q >= 2:
+            out.append(("e", (0, 3) if p == 0 else (1, 2), q))
+        elif r == 0:
+            out.append(("q", quad[(p, q)]))
+        elif p in (0, 1) and q in (0, 1):
+            base = {(0, 0): 0, (1, 0): 1, (1, 1): 2, (0, 1): 3}[(p, q)]
+            out.append(("e", (base, 4), r + (1 if (p, q) != (0, 0) else 0)))
+        elif q in (0, 1):  # p >= 2: faces V0 V1 V4 (eta2 = -1) / V3 V2 V4 (eta2 = 1)
+            out.append(("t", (0, 1, 4) if q == 0 else (3, 2, 4), tri[(p, r)]))
+        elif p in (0, 1):  # q >= 2: faces V0 V3 V4 (eta1 = -1) / V1 V2 V4 (eta1 = 1)
+            out.append(("t", (0, 3, 4) if p == 0 else (1, 2, 4), tri[(q, r)]))
+        else:
+            out.append(("i", ni))
+            ni += 1
+    return out, len(quad), len(tri), ni
+
+
+def _pyr_numbering(nx: int, ny: int, nz: int, P: int):
+    pyrs, _, z2 = _pyr_topology(nx, ny, nz)
+    ent, nq, nt, ni = _pyr_mode_entity(P)
+    size = {"v": 1, "e": P - 1, "q": nq, "t": nt}
+    levels: dict = {}
+    zmap = {}
+    for t, zz in zip(pyrs, z2):
+        for v, z in zip(t, zz):
+            zmap[v] = z
+
+    def level(sub):
+        zs = [zmap[v] for v in sub]
+        if min(zs) == max(zs) and min(zs) % 2 == 0:
+            return min(zs)
+        return 2 * (min(zs) // 2) + 1
+
+    for t in pyrs:
+        subs = [("v", (v,)) for v in t]
+        subs += [("e", tuple(sorted((t[i], t[j])))) for i, j in ((0, 1), (3, 2), (0, 3), (1, 2), (0, 4), (1, 4), (2, 4), (3, 4))]
+        subs += [("q", tuple(sorted(t[:4])))]
+        subs += [("t", tuple(sorted(t[i] for i in f))) for f in ((0, 1, 4), (3, 2, 4), (0, 3, 4), (1, 2, 4))]
+        for kind, sub in subs:
+            levels.setdefault(level(sub), {})[(kind, sub)] = None
+    order = {"v": 0, "e": 1, "q": 2, "t": 3}
+    start, offs, level_start = 0, {}, {}
+    per_layer = nx * ny * 6
+    for lev in range(2 * nz + 1):
+        level_start[lev] = start
+        for kind, sub in sorted(levels.get(lev, {}), key=lambda x: (order[x[0]], x[1])):
+            offs[(kind, sub)] = start
+            start += size[kind]
+        if lev % 2 == 1:
+            for e in range((lev // 2) * per_layer, (lev // 2 + 1) * per_layer):
+                offs[("i", e)] = start
+                start += ni
+    level_start[2 * nz + 1] = start
+    l2g = np.empty((len(pyrs), len(ent)), dtype=np.int64)
+    for e, t in enumerate(pyrs):
+        for m, en in enumerate(ent):
+            k = en[0]
+            if k == "v":
+                l2g[e, m] = offs[("v", (t[en[1]],))]
+            elif k == "e":
+                l2g[e, m] = offs[("e", tuple(sorted(t[i] for i in en[1])))] + en[2] - 2
+            elif k == "q":
+                l2g[e, m] = offs[("q", tuple(sorted(t[:4])))] + en[1]
+            elif k == "t":
+                l2g[e, m] = offs[("t", tuple(sorted(t[i] for i in en[1])))] + en[2]
+            else:
+                l2g[e, m] = offs[("i", e)] + en[1]
+    return l2g, level_start, level_start[1] - level_start[0]
+
+
+def pyr_n_global(nx: int, ny: int, nz: int, P: int) -> int:
+    return _pyr_numbering(nx, ny, nz, P)[1][2 * nz + 1]
+
+
+def pyr_mesh_coords(nx: int, ny: int, nz: int, P: int, amp: float = 0.05):
+    """(E, NQ, 3): x = V0 + l1 (V1 - V0) + l2 (V3 - V0) + l3 (V4 - V0),
+    l_i = (1 + xi_i)/2 (the reference pyramid's apex is xi = (-1,-1,1)), then
+    the global deformation."""
+    el = element("pyr", P)
+    xi = quadrature_xi(el)
+    _, pts, _ = _pyr_topology(nx, ny, nz)
+    lam = 0.5 * (1.0 + xi)
+    out = np.empty((len(pts), el.nq, 3))
+    for e, v in enumerate(pts):
+        X = v[0][None, :] + lam @ np.stack([v[1] - v[0], v[3] - v[0], v[4] - v[0]])
+        out[e] = X + amp * np.sin(0.5 * np.pi * X[:, [1, 2, 0]])
+    return out
+
+
+def assembled_helmholtz_pyr(nx: int, ny: int, nz: int, P: int, x: np.ndarray, lam: float, amp: float = 0.05):
+    el = element("pyr", P)
+    geo = deformed_geometry_from_coords(el, pyr_mesh_coords(nx, ny, nz, P, amp), either_orientation=True)
+    l2g, _, _ = _pyr_numbering(nx, ny, nz, P)
+    ye = helmholtz_coll(el, geo, x[l2g].T, lam)
+    y = np.zeros_like(x)
+    np.add.at(y, l2g.T.ravel(), ye.ravel())
+    return y
+
+
+PYR_REF = np.array([[-1.0, -1.0, -1.0], [1.0, -1.0, -1.0], [1.0, 1.0, -1.0], [-1.0, 1.0, -1.0], [-1.0, -1.0, 1.0]])
+
+
+def pyr_collapse(xi: np.ndarray) -> np.ndarray:
+    eta = np.empty_like(xi)
+    eta[:, 0] = 2.0 * (1.0 + xi[:, 0]) / (1.0 - xi[:, 2]) - 1.0
+    eta[:, 1] = 2.0 * (1.0 + xi[:, 1]) / (1.0 - xi[:, 2]) - 1.0
+    eta[:, 2] = xi[:, 2]
+    return eta
+
+
+def pyr_eval(P: int, coeffs: np.ndarray, eta: np.ndarray) -> np.ndarray:
+    from oracle.elements import _factor_fns
+
+    out = np.zeros(eta.shape[0])
+    for c, m in zip(coeffs, mode_set("pyr", P)):
+        f = _factor_fns("pyr", m)
+        out += c * f[0][0](eta[:, 0]) * f[1][0](eta[:, 1]) * f[2][0](eta[:, 2])
+    return out

@@ -29,7 +29,7 @@ from paper_2604_04644_b200.operators import helmholtz_apply
 from paper_2604_04644_b200.sharding import partition
 from paper_2604_04644_b200.shapes import Shape, build_shape_basis
 
-__all__ = ["C0HexMesh", "C0PrismMesh", "C0TetMesh", "exchange_interfaces"]
+__all__ = ["C0HexMesh", "C0PrismMesh", "C0TetMesh", "C0PyrMesh", "exchange_interfaces"]
 
 
 def exchange_interfaces(y, layer: int, group=None) -> None:
@@ -449,3 +449,157 @@ class C0TetMesh:
         per_layer = self.n_dofs - self.layer  # plane + between-level dofs of one cube layer
         start = self.z0 * (per_layer // self.nzl)
         return slice(start, start + self.n_dofs)
+
+
+_PYR_FACES = ((0, 0), (0, 1), (1, 0), (1, 1), (2, 0), (2, 1))  # (normal axis, side) of the base
+_PYR_EDGES = ((0, 1), (3, 2), (0, 3), (1, 2), (0, 4), (1, 4), (2, 4), (3, 4))
+_PYR_TRIS = ((0, 1, 4), (3, 2, 4), (0, 3, 4), (1, 2, 4))
+
+
+def _pyr_mode_table(P: int):
+    """Entity of every local pyramid mode (p, q, r) (shapes.py:374-405):
+    (kind, local index, sub-index); kinds 0 vertex, 1 edge (_PYR_EDGES,
+    sub-index degree - 2), 2 base quad (canonical (p, q)), 3 triangular face
+    (_PYR_TRIS, canonical (a, b): psi_a(a) along the base edge, psi_b(a, b)
+    towards the apex), 4 interior."""
+    tri = {ab: i for i, ab in enumerate((a, b) for a in range(2, P + 1) for b in range(1, P + 1 - a))}
+    quad = {pq: i for i, pq in enumerate((p, q) for p in range(2, P + 1) for q in range(2, P + 1))}
+    vert = {(0, 0, 0): 0, (1, 0, 0): 1, (1, 1, 0): 2, (0, 1, 0): 3, (0, 0, 1): 4}
+    corner = {(0, 0): 0, (1, 0): 1, (1, 1): 2, (0, 1): 3}
+    out, ni = [], 0
+    for p in range(P + 1):
+        for q in range(P + 1):
+            for r in range(P + 1 - max(p, q)):
+                if (p, q, r) in vert:
+                    out.append((0, vert[(p, q, r)], 0))
+                elif r == 0 and q <= 1 and p >= 2:
+                    out.append((1, q, p - 2))  # edges V0V1 / V3V2
+                elif r == 0 and p <= 1 and q >= 2:
+                    out.append((1, 2 + p, q - 2))  # edges V0V3 / V1V2
+                elif r == 0:
+                    out.append((2, 0, quad[(p, q)]))
+                elif p <= 1 and q <= 1:
+                    c = corner[(p, q)]
+                    out.append((1, 4 + c, r - 2 if c == 0 else r - 1))  # apex edges
+                elif q <= 1:
+                    out.append((3, q, tri[(p, r)]))
+                elif p <= 1:
+                    out.append((3, 2 + p, tri[(q, r)]))
+                else:
+                    out.append((4, 0, ni))
+                    ni += 1
+    return out, len(quad), len(tri), ni
+
+
+def _pyr_maps(nx: int, ny: int, nz: int, z0: int, nzl: int, P: int):
+    """Numbering of the C0 pyramid mesh slab of cube layers [z0, z0 + nzl)
+    (see C0PyrMesh): vertex coordinates (E, 5, 3), the slab-relative global
+    dof of every (pyramid, local mode), the slab's dof count and the dofs of
+    one z plane."""
+    nc = (nx + 1) * (ny + 1) * (nz + 1)
+    ix, iy, iz = np.meshgrid(np.arange(nx), np.arange(ny), z0 + np.arange(nzl), indexing="ij")
+    base = np.stack([ix.T.ravel(), iy.T.ravel(), iz.T.ravel()], axis=1)  # (cubes, 3), x fastest
+    cube = (base[:, 2] * ny + base[:, 1]) * nx + base[:, 0]
+    eye = np.eye(3, dtype=np.int64)
+    quads = []
+    for n, side in _PYR_FACES:
+        a, b = [ax for ax in range(3) if ax != n]
+        v0 = side * eye[n]
+        quads.append(np.stack([v0, v0 + eye[a], v0 + eye[a] + eye[b], v0 + eye[b]]))
+    quads = np.stack(quads)  # (6, 4, 3)
+    corners = base[:, None, None, :] + quads[None]  # (cubes, 6, 4, 3)
+    ncube = base.shape[0]
+    pts = np.empty((ncube, 6, 5, 3))
+    pts[:, :, :4] = corners
+    pts[:, :, 4] = base[:, None, :] + 0.5
+    pts = pts.reshape(-1, 5, 3)
+    cid = (corners[..., 2] * (ny + 1) + corners[..., 1]) * (nx + 1) + corners[..., 0]
+    verts = np.concatenate([cid, np.broadcast_to((nc + cube)[:, None, None], (ncube, 6, 1))], axis=2).reshape(-1, 5)
+    z2 = np.concatenate([2 * corners[..., 2], np.broadcast_to((2 * base[:, 2] + 1)[:, None, None], (ncube, 6, 1))],
+                        axis=2).reshape(-1, 5)
+    E = verts.shape[0]
+    nkey = nc + nx * ny * nz
+    recs = []
+    for kind, subs in ((0, tuple((i,) for i in range(5))), (1, _PYR_EDGES), (2, ((0, 1, 2, 3),)), (3, _PYR_TRIS)):
+        arr = np.stack([verts[:, list(s)] for s in subs], axis=1)  # (E, n, k)
+        zz = np.stack([z2[:, list(s)] for s in subs], axis=1)
+        zmin, zmax = zz.min(axis=-1), zz.max(axis=-1)
+        lev = np.where((zmin == zmax) & (zmin % 2 == 0), zmin, 2 * (zmin // 2) + 1)
+        arr = np.sort(arr, axis=-1)
+        key = np.zeros(arr.shape[:2], dtype=np.int64)
+        for c in range(arr.shape[-1]):
+            key = key * nkey + arr[..., c]
+        recs.append((lev, np.full(arr.shape[:2], kind), key))
+    recs.append(((2 * np.repeat(base[:, 2], 6) + 1)[:, None], np.full((E, 1), 4), np.arange(E, dtype=np.int64)[:, None]))
+    lev = np.concatenate([r[0].ravel() for r in recs])
+    kind = np.concatenate([r[1].ravel() for r in recs])
+    key = np.concatenate([r[2].ravel() for r in recs])
+    order_ = np.lexsort((key, kind, lev))
+    srt = np.stack([lev[order_], kind[order_], key[order_]], axis=1)
+    new = np.ones(len(srt), dtype=bool)
+    new[1:] = np.any(srt[1:] != srt[:-1], axis=1)
+    uid = np.empty(len(srt), dtype=np.int64)
+    uid[order_] = np.cumsum(new) - 1
+    modes, nq, nt, ni = _pyr_mode_table(P)
+    usize = np.array([1, P - 1, nq, nt, ni])[srt[new, 1]]
+    uoff = np.concatenate([[0], np.cumsum(usize)[:-1]])
+    n_dofs = int(usize.sum())
+    layer = (nx + 1) * (ny + 1) + (nx * (ny + 1) + (nx + 1) * ny) * (P - 1) + nx * ny * nq  # one z plane
+    cut = np.cumsum([0, E * 5, E * 8, E, E * 4, E])
+    ent = [uid[cut[k]:cut[k + 1]].reshape(E, -1) for k in range(5)]
+    l2g = np.empty((E, len(modes)), dtype=np.int64)
+    for m, (k, li, sub) in enumerate(modes):
+        l2g[:, m] = uoff[ent[k][:, li]] + sub
+    return pts, l2g, n_dofs, layer
+
+
+class C0PyrMesh:
+    """This rank's slab of a conforming pyramid mesh: nx x ny x nz unit
+    cubes, each split into six pyramids (apex = the cube centre, base = a
+    cube face), each base's (eta1, eta2) along the face's two global axes in
+    increasing direction from its minimum corner -- so shared base quads,
+    triangular faces and edges are parameterised alike on both sides with no
+    signs (the reflected half gets w|det J|) -- deformed by the global map
+    of C0HexMesh, level-ordered DOFs as C0TetMesh.  y = A^T H_e A x by
+    sk_c0_gather_map -> the pyramid kernels -> sk_c0_scatter_map, then the
+    plane exchange.  Parity: oracle/assembly.py (pyramid section,
+    conformity-checked on CPU)."""
+
+    def __init__(self, nx: int, ny: int, nz: int, order: int, amp: float = 0.05, rank: int = 0, world: int = 1):
+        import torch
+
+        if nz < world:
+            raise ValueError(f"need at least one element layer per rank: nz={nz} < world={world}")
+        P = order
+        self.nx, self.ny, self.nz, self.P, self.amp = nx, ny, nz, P, amp
+        self.z0, self.nzl = partition(nz, world, rank)
+        pts, l2g, self.n_dofs, self.layer = _pyr_maps(nx, ny, nz, self.z0, self.nzl, P)
+        self.E = pts.shape[0]
+        self.basis = build_shape_basis(Shape.PYR, P)
+        assert l2g.shape[1] == self.basis.n_modes
+        l2g = l2g.reshape(-1)
+        order_ = np.argsort(l2g, kind="stable")
+        ptr = np.zeros(self.n_dofs + 1, dtype=np.int64)
+        np.cumsum(np.bincount(l2g, minlength=self.n_dofs), out=ptr[1:])
+        dev = torch.device("cuda", torch.cuda.current_device())
+        ones = torch.ones(l2g.size, dtype=torch.float64, device=dev)
+        self._l2g = torch.as_tensor(l2g, device=dev)
+        self._sgn = ones
+        self._ptr = torch.as_tensor(ptr, device=dev)
+        self._loc = torch.as_tensor(order_.astype(np.int64), device=dev)
+        self._csgn = ones
+        # affine image of the reference pyramid (apex at xi = (-1,-1,1)):
+        # x = V0 + l1 (V1 - V0) + l2 (V3 - V0) + l3 (V4 - V0), l = (1 + xi) / 2
+        xi = torch.as_tensor(quadrature_coords(self.basis), device=dev)
+        lam = 0.5 * (1.0 + xi)
+        v = torch.as_tensor(pts, dtype=torch.float64, device=dev)  # (E, 5, 3)
+        axes = torch.stack([v[:, 1] - v[:, 0], v[:, 3] - v[:, 0], v[:, 4] - v[:, 0]], dim=1)  # (E, 3, 3)
+        X = v[:, None, 0, :] + torch.einsum("qk,ekc->eqc", lam, axes)
+        coords = X + amp * torch.sin(0.5 * np.pi * X[..., [1, 2, 0]])
+        self.factors = deformed_factors_from_coords(self.basis, coords, either_orientation=True)
+        del coords, X
+        self.block = Block(self.basis, self.factors, FieldState.COEFF, 1, 1)
+        self.out = self.block.like(FieldState.COEFF)
+
+    helmholtz = C0PrismMesh.helmholtz
+    slab_slice = C0TetMesh.slab_slice

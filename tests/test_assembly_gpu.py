@@ -135,3 +135,19 @@ def test_assembled_tet_stiffness_annihilates_constants(torch):
     x[l2g[:, vert].ravel()] = 1.0
     y = mesh.helmholtz(torch.from_numpy(x).cuda(), 0.0).cpu().numpy()
     assert np.max(np.abs(y)) <= 1e-11
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 4, 6])
+def test_assembled_pyr_matches_oracle(torch, P):
+    """Assembled C0 pyramid Helmholtz (six pyramids per cube, bases along the
+    global axes) against the oracle on the same mesh."""
+    from paper_2604_04644_b200.assembly import C0PyrMesh
+
+    nx, ny, nz = 2, 2, 3
+    mesh = C0PyrMesh(nx, ny, nz, P)
+    N = A.pyr_n_global(nx, ny, nz, P)
+    assert mesh.n_dofs == N
+    x = np.random.default_rng(P).standard_normal(N)
+    for lam in (0.0, 1.0):
+        y = mesh.helmholtz(torch.from_numpy(x).cuda(), lam).cpu().numpy()
+        assert O.rel_diff(y, A.assembled_helmholtz_pyr(nx, ny, nz, P, x, lam)) <= 1e-12, lam

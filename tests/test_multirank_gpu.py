@@ -215,3 +215,44 @@ def test_two_ranks_c0_tet_slabs_with_exchange(cuda, tmp_path):
         got = np.load(tmp_path / f"tslab{r}.npy")
         lo, hi = np.load(tmp_path / f"tslice{r}.npy")
         assert O.rel_diff(got, ref[lo:hi]) <= 1e-12, r
+
+
+C0Y = (2, 2, 3, 2)  # nx, ny, nz, P
+
+
+def _c0_pyr_worker(rank, world, port, out_dir):
+    import torch
+    import torch.distributed as dist
+
+    import oracle.assembly as A
+    from paper_2604_04644_b200.assembly import C0PyrMesh
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    nx, ny, nz, P = C0Y
+    mesh = C0PyrMesh(nx, ny, nz, P, rank=rank, world=world)
+    x = np.random.default_rng(6).standard_normal(A.pyr_n_global(nx, ny, nz, P))
+    sl = mesh.slab_slice()
+    y = mesh.helmholtz(torch.from_numpy(x[sl].copy()).cuda(), 1.0)
+    np.save(os.path.join(out_dir, f"yslab{rank}.npy"), y.cpu().numpy())
+    np.save(os.path.join(out_dir, f"yslice{rank}.npy"), np.array([sl.start, sl.stop]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_ranks_c0_pyr_slabs_with_exchange(cuda, tmp_path):
+    import torch.multiprocessing as mp
+
+    import oracle.assembly as A
+
+    world = 2
+    mp.start_processes(_c0_pyr_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, start_method="spawn")
+    nx, ny, nz, P = C0Y
+    x = np.random.default_rng(6).standard_normal(A.pyr_n_global(nx, ny, nz, P))
+    ref = A.assembled_helmholtz_pyr(nx, ny, nz, P, x, 1.0)
+    for r in range(world):
+        got = np.load(tmp_path / f"yslab{r}.npy")
+        lo, hi = np.load(tmp_path / f"yslice{r}.npy")
+        assert O.rel_diff(got, ref[lo:hi]) <= 1e-12, r
