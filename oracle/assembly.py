@@ -1,4 +1,5 @@
-"""CPU oracle of the assembled C0 operator on a conforming hex mesh.
+"""CPU oracle of the assembled C0 operators on conforming hex, prism, tet and
+pyramid meshes (the hex section first; the others below).
 
 The reference stops at elemental operators (global assembly is out of its
 scope), so this restatement is the checker for the

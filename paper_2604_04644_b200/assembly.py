@@ -198,7 +198,60 @@ def _prism_tri_maps(nx: int, nw: int, P: int):
     return tris, pts, dof, sgn, base_i + nt * ni
 
 
-class C0PrismMesh:
+class _MappedC0Mesh:
+    """Assembled C0 slab applied through explicit maps: signed gather
+    (sk_c0_gather_map) -> the elemental collocated Helmholtz of the shape ->
+    deterministic CSR scatter (sk_c0_scatter_map) -> exchange of the two
+    shared end layers / planes (``layer`` DOFs each) with the neighbouring
+    ranks.  Subclasses build the maps and the quadrature coordinates."""
+
+    def _setup(self, shape: Shape, l2g: np.ndarray, sgn, coords, either_orientation: bool) -> None:
+        """l2g (E, NM) slab-relative global DOFs, sgn (E, NM) or None (all +1),
+        coords (E, NQ, 3) CUDA tensor of quadrature-point coordinates."""
+        import torch
+
+        self.basis = build_shape_basis(shape, self.P)
+        assert l2g.shape == (self.E, self.basis.n_modes)
+        flat = l2g.reshape(-1)
+        order_ = np.argsort(flat, kind="stable")
+        ptr = np.zeros(self.n_dofs + 1, dtype=np.int64)
+        np.cumsum(np.bincount(flat, minlength=self.n_dofs), out=ptr[1:])
+        dev = coords.device
+        self._l2g = torch.as_tensor(flat, device=dev)
+        self._ptr = torch.as_tensor(ptr, device=dev)
+        self._loc = torch.as_tensor(order_.astype(np.int64), device=dev)
+        if sgn is None:
+            self._sgn = self._csgn = torch.ones(flat.size, dtype=torch.float64, device=dev)
+        else:
+            sg = sgn.reshape(-1)
+            self._sgn = torch.as_tensor(sg, device=dev)
+            self._csgn = torch.as_tensor(sg[order_], device=dev)
+        self.factors = deformed_factors_from_coords(self.basis, coords, either_orientation=either_orientation)
+        self.block = Block(self.basis, self.factors, FieldState.COEFF, 1, 1)
+        self.out = self.block.like(FieldState.COEFF)
+
+    def helmholtz(self, x, lam: float, group=None):
+        """y = A^T H_e A x for this slab's DOF vector x (CUDA, length
+        n_dofs); the shared end layers are summed across ranks."""
+        import torch
+
+        lib = _lib.load()
+        s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+        vp = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+        nm = self.basis.n_modes
+        local = self.block.device(AccessQualifier.WRITE_ONLY)
+        _lib.check(lib.sk_c0_gather_map(self.E, nm, vp(self._l2g), vp(self._sgn), vp(x), 1, vp(local), s),
+                   "sk_c0_gather_map")
+        helmholtz_apply(self.block, lam, out=self.out)
+        y = torch.empty(self.n_dofs, dtype=torch.float64, device=x.device)
+        loc = self.out.device(AccessQualifier.READ_ONLY)
+        _lib.check(lib.sk_c0_scatter_map(self.n_dofs, nm, vp(self._ptr), vp(self._loc), vp(self._csgn), vp(loc), 1,
+                                         vp(y), s), "sk_c0_scatter_map")
+        exchange_interfaces(y, self.layer, group)
+        return y
+
+
+class C0PrismMesh(_MappedC0Mesh):
     """This rank's slab of a conforming prism mesh: the triangulated nx x nw
     grid of unit squares in the (x, z) plane extruded along y in nz element
     layers (the slab axis), deformed by the same smooth global map as
@@ -222,8 +275,7 @@ class C0PrismMesh:
         self.layer = n2d  # DOFs of one extrusion node (the exchanged interface)
         self.n_dofs = n2d * (self.nzl * P + 1)
         self.E = self.nzl * nt
-        self.basis = build_shape_basis(Shape.PRISM, P)
-        modes = self.basis.modes
+        modes = build_shape_basis(Shape.PRISM, P).modes
         nm = len(modes)
         pm = np.array([0 if q == 0 else P if q == 1 else q - 1 for q in range(P + 1)])
         ez = np.arange(self.nzl)
@@ -232,54 +284,21 @@ class C0PrismMesh:
         for m, (p, q, r) in enumerate(modes):
             l2g[:, :, m] = (ez[:, None] * P + pm[q]) * n2d + dof2[(p, r)][None, :]
             sgn[:, :, m] = sgn2[(p, r)][None, :]
-        l2g, sgn = l2g.reshape(-1), sgn.reshape(-1)
-        order_ = np.argsort(l2g, kind="stable")
-        ptr = np.zeros(self.n_dofs + 1, dtype=np.int64)
-        np.cumsum(np.bincount(l2g, minlength=self.n_dofs), out=ptr[1:])
-        dev = torch.device("cuda", torch.cuda.current_device())
-        self._l2g = torch.as_tensor(l2g, device=dev)
-        self._sgn = torch.as_tensor(sgn, device=dev)
-        self._ptr = torch.as_tensor(ptr, device=dev)
-        self._loc = torch.as_tensor(order_.astype(np.int64), device=dev)
-        self._csgn = torch.as_tensor(sgn[order_], device=dev)
         # quadrature coordinates: barycentrics of the triangle in (x, z),
         # y = layer + (1 + xi2) / 2, then the global deformation
-        xi = torch.as_tensor(quadrature_coords(self.basis), device=dev)
+        dev = torch.device("cuda", torch.cuda.current_device())
+        xi = torch.as_tensor(quadrature_coords(build_shape_basis(Shape.PRISM, P)), device=dev)
         l1, l2 = 0.5 * (1.0 + xi[:, 0]), 0.5 * (1.0 + xi[:, 2])
         lw = torch.stack([1.0 - l1 - l2, l1, l2], dim=1)  # (NQ, 3)
-        v = torch.as_tensor(pts, device=dev)  # (NT, 3, 2)
-        xz = torch.einsum("qk,tkc->tqc", lw, v)  # (NT, NQ, 2)
-        yl = (self.z0 + torch.arange(self.nzl, device=dev, dtype=torch.float64))[:, None, None] + 0.5 * (1.0 + xi[None, :, 1:2])
+        xz = torch.einsum("qk,tkc->tqc", lw, torch.as_tensor(pts, device=dev))  # (NT, NQ, 2)
         X = torch.empty((self.nzl, nt, xi.shape[0], 3), dtype=torch.float64, device=dev)
         X[..., 0] = xz[None, ..., 0]
         X[..., 2] = xz[None, ..., 1]
-        X[..., 1] = yl.expand(self.nzl, xi.shape[0], 1)[:, None, :, 0]
+        X[..., 1] = (self.z0 + torch.arange(self.nzl, device=dev, dtype=torch.float64))[:, None, None] \
+            + 0.5 * (1.0 + xi[None, None, :, 1])
         X = X.reshape(self.E, xi.shape[0], 3)
-        coords = X + amp * torch.sin(0.5 * np.pi * X[..., [1, 2, 0]])
-        self.factors = deformed_factors_from_coords(self.basis, coords)
-        del coords, X
-        self.block = Block(self.basis, self.factors, FieldState.COEFF, 1, 1)
-        self.out = self.block.like(FieldState.COEFF)
-
-    def helmholtz(self, x, lam: float, group=None):
-        """y = A^T H_e A x for this slab's DOF vector x (CUDA, length
-        n_dofs); the shared end layers are summed across ranks."""
-        import torch
-
-        lib = _lib.load()
-        s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
-        vp = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
-        nm = self.basis.n_modes
-        local = self.block.device(AccessQualifier.WRITE_ONLY)
-        _lib.check(lib.sk_c0_gather_map(self.E, nm, vp(self._l2g), vp(self._sgn), vp(x), 1, vp(local), s),
-                   "sk_c0_gather_map")
-        helmholtz_apply(self.block, lam, out=self.out)
-        y = torch.empty(self.n_dofs, dtype=torch.float64, device=x.device)
-        loc = self.out.device(AccessQualifier.READ_ONLY)
-        _lib.check(lib.sk_c0_scatter_map(self.n_dofs, nm, vp(self._ptr), vp(self._loc), vp(self._csgn), vp(loc), 1,
-                                         vp(y), s), "sk_c0_scatter_map")
-        exchange_interfaces(y, self.layer, group)
-        return y
+        self._setup(Shape.PRISM, l2g.reshape(self.E, nm), sgn.reshape(self.E, nm),
+                    X + amp * torch.sin(0.5 * np.pi * X[..., [1, 2, 0]]), either_orientation=False)
 
     def slab_slice(self) -> slice:
         """This slab's range in the global DOF vector."""
@@ -391,7 +410,7 @@ def _tet_maps(nx: int, ny: int, nz: int, z0: int, nzl: int, P: int):
     return pts, l2g, n_dofs, layer
 
 
-class C0TetMesh:
+class C0TetMesh(_MappedC0Mesh):
     """This rank's slab of a conforming tet mesh: nx x ny x nz unit cubes,
     each split into the six Kuhn tets along its main diagonal, every tet
     taking its vertices in global-id order (so shared edges and faces are
@@ -414,34 +433,16 @@ class C0TetMesh:
         self.nx, self.ny, self.nz, self.P, self.amp = nx, ny, nz, P, amp
         self.z0, self.nzl = partition(nz, world, rank)
         pts, l2g, self.n_dofs, self.layer = _tet_maps(nx, ny, nz, self.z0, self.nzl, P)
-        E = pts.shape[0]
-        self.E = E
-        self.basis = build_shape_basis(Shape.TET, P)
-        assert l2g.shape[1] == self.basis.n_modes
-        l2g = l2g.reshape(-1)
-        order_ = np.argsort(l2g, kind="stable")
-        ptr = np.zeros(self.n_dofs + 1, dtype=np.int64)
-        np.cumsum(np.bincount(l2g, minlength=self.n_dofs), out=ptr[1:])
-        dev = torch.device("cuda", torch.cuda.current_device())
-        ones = torch.ones(l2g.size, dtype=torch.float64, device=dev)
-        self._l2g = torch.as_tensor(l2g, device=dev)
-        self._sgn = ones
-        self._ptr = torch.as_tensor(ptr, device=dev)
-        self._loc = torch.as_tensor(order_.astype(np.int64), device=dev)
-        self._csgn = ones
+        self.E = pts.shape[0]
         # quadrature coordinates: affine image of the reference tet, then the
         # global deformation
-        xi = torch.as_tensor(quadrature_coords(self.basis), device=dev)
+        dev = torch.device("cuda", torch.cuda.current_device())
+        xi = torch.as_tensor(quadrature_coords(build_shape_basis(Shape.TET, P)), device=dev)
         lam = 0.5 * (1.0 + xi)  # (NQ, 3)
         v = torch.as_tensor(pts, dtype=torch.float64, device=dev)  # (E, 4, 3)
         X = v[:, None, 0, :] + torch.einsum("qk,ekc->eqc", lam, v[:, 1:, :] - v[:, :1, :])
-        coords = X + amp * torch.sin(0.5 * np.pi * X[..., [1, 2, 0]])
-        self.factors = deformed_factors_from_coords(self.basis, coords, either_orientation=True)
-        del coords, X
-        self.block = Block(self.basis, self.factors, FieldState.COEFF, 1, 1)
-        self.out = self.block.like(FieldState.COEFF)
-
-    helmholtz = C0PrismMesh.helmholtz
+        self._setup(Shape.TET, l2g, None, X + amp * torch.sin(0.5 * np.pi * X[..., [1, 2, 0]]),
+                    either_orientation=True)
 
     def slab_slice(self) -> slice:
         """This slab's range in the global DOF vector (cube layers [z0, z0 +
@@ -553,7 +554,7 @@ def _pyr_maps(nx: int, ny: int, nz: int, z0: int, nzl: int, P: int):
     return pts, l2g, n_dofs, layer
 
 
-class C0PyrMesh:
+class C0PyrMesh(_MappedC0Mesh):
     """This rank's slab of a conforming pyramid mesh: nx x ny x nz unit
     cubes, each split into six pyramids (apex = the cube centre, base = a
     cube face), each base's (eta1, eta2) along the face's two global axes in
@@ -575,31 +576,15 @@ class C0PyrMesh:
         self.z0, self.nzl = partition(nz, world, rank)
         pts, l2g, self.n_dofs, self.layer = _pyr_maps(nx, ny, nz, self.z0, self.nzl, P)
         self.E = pts.shape[0]
-        self.basis = build_shape_basis(Shape.PYR, P)
-        assert l2g.shape[1] == self.basis.n_modes
-        l2g = l2g.reshape(-1)
-        order_ = np.argsort(l2g, kind="stable")
-        ptr = np.zeros(self.n_dofs + 1, dtype=np.int64)
-        np.cumsum(np.bincount(l2g, minlength=self.n_dofs), out=ptr[1:])
-        dev = torch.device("cuda", torch.cuda.current_device())
-        ones = torch.ones(l2g.size, dtype=torch.float64, device=dev)
-        self._l2g = torch.as_tensor(l2g, device=dev)
-        self._sgn = ones
-        self._ptr = torch.as_tensor(ptr, device=dev)
-        self._loc = torch.as_tensor(order_.astype(np.int64), device=dev)
-        self._csgn = ones
         # affine image of the reference pyramid (apex at xi = (-1,-1,1)):
         # x = V0 + l1 (V1 - V0) + l2 (V3 - V0) + l3 (V4 - V0), l = (1 + xi) / 2
-        xi = torch.as_tensor(quadrature_coords(self.basis), device=dev)
+        dev = torch.device("cuda", torch.cuda.current_device())
+        xi = torch.as_tensor(quadrature_coords(build_shape_basis(Shape.PYR, P)), device=dev)
         lam = 0.5 * (1.0 + xi)
         v = torch.as_tensor(pts, dtype=torch.float64, device=dev)  # (E, 5, 3)
         axes = torch.stack([v[:, 1] - v[:, 0], v[:, 3] - v[:, 0], v[:, 4] - v[:, 0]], dim=1)  # (E, 3, 3)
         X = v[:, None, 0, :] + torch.einsum("qk,ekc->eqc", lam, axes)
-        coords = X + amp * torch.sin(0.5 * np.pi * X[..., [1, 2, 0]])
-        self.factors = deformed_factors_from_coords(self.basis, coords, either_orientation=True)
-        del coords, X
-        self.block = Block(self.basis, self.factors, FieldState.COEFF, 1, 1)
-        self.out = self.block.like(FieldState.COEFF)
+        self._setup(Shape.PYR, l2g, None, X + amp * torch.sin(0.5 * np.pi * X[..., [1, 2, 0]]),
+                    either_orientation=True)
 
-    helmholtz = C0PrismMesh.helmholtz
     slab_slice = C0TetMesh.slab_slice
