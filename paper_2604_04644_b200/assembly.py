@@ -230,6 +230,15 @@ class _MappedC0Mesh:
         self.block = Block(self.basis, self.factors, FieldState.COEFF, 1, 1)
         self.out = self.block.like(FieldState.COEFF)
 
+    def slab_slice(self) -> slice:
+        """This slab's range in the global DOF vector.  Level-ordered meshes
+        (tet, pyramid): cube layers [z0, z0 + nzl) own every level from plane
+        z0 to plane z0 + nzl, and every cube layer holds the same number of
+        plane + between-level DOFs."""
+        per_layer = (self.n_dofs - self.layer) // self.nzl
+        start = self.z0 * per_layer
+        return slice(start, start + self.n_dofs)
+
     def helmholtz(self, x, lam: float, group=None):
         """y = A^T H_e A x for this slab's DOF vector x (CUDA, length
         n_dofs); the shared end layers are summed across ranks."""
@@ -444,12 +453,6 @@ class C0TetMesh(_MappedC0Mesh):
         self._setup(Shape.TET, l2g, None, X + amp * torch.sin(0.5 * np.pi * X[..., [1, 2, 0]]),
                     either_orientation=True)
 
-    def slab_slice(self) -> slice:
-        """This slab's range in the global DOF vector (cube layers [z0, z0 +
-        nzl): every level between plane z0 and plane z0 + nzl)."""
-        per_layer = self.n_dofs - self.layer  # plane + between-level dofs of one cube layer
-        start = self.z0 * (per_layer // self.nzl)
-        return slice(start, start + self.n_dofs)
 
 
 _PYR_FACES = ((0, 0), (0, 1), (1, 0), (1, 1), (2, 0), (2, 1))  # (normal axis, side) of the base
@@ -586,5 +589,3 @@ class C0PyrMesh(_MappedC0Mesh):
         X = v[:, None, 0, :] + torch.einsum("qk,ekc->eqc", lam, axes)
         self._setup(Shape.PYR, l2g, None, X + amp * torch.sin(0.5 * np.pi * X[..., [1, 2, 0]]),
                     either_orientation=True)
-
-    slab_slice = C0TetMesh.slab_slice
