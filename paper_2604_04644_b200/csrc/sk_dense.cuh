@@ -151,14 +151,22 @@ constexpr int kDenseThreads = 256;
 // already keeps the loads in flight; dense_tune_def.jsonl).  SK_DENSE_PF=0/1
 // forces it in tuning builds.
 #ifndef SK_DENSE_MINB
-#define SK_DENSE_MINB 0
+#define SK_DENSE_MINB -1
 #endif
+// deformed: 5 CTAs per SM (<= 51 registers, no spills) measured +0-29 %
+// over the unbounded 60-register build (pyr P=2 0.48 -> 0.62, tet P=1-3
+// +1-10 %, dense_tune_def.jsonl); regular: unbounded (the prefetch needs the
+// registers)
+template <int GEO>
+constexpr int dense_minb() {
+  return SK_DENSE_MINB >= 0 ? SK_DENSE_MINB : GEO == GEO_DEFORMED ? 5 : 0;
+}
 #ifndef SK_DENSE_PF
 #define SK_DENSE_PF -1
 #endif
 
 template <int S, int P, int PW, int GEO>
-__global__ void __launch_bounds__(kDenseThreads, SK_DENSE_MINB) k_mass_dense(const __grid_constant__ DenseArgs A) {
+__global__ void __launch_bounds__(kDenseThreads, dense_minb<GEO>()) k_mass_dense(const __grid_constant__ DenseArgs A) {
   using X = DenseDims<S, P>;
   constexpr int NQ = X::NQ, NM = X::NM, KS1 = X::KS1, MT = X::MT;
   constexpr bool PF = SK_DENSE_PF >= 0 ? SK_DENSE_PF != 0 : GEO == GEO_REGULAR;
