@@ -243,6 +243,42 @@ def test_large_block_properties(sk):
     del torch
 
 
+@pytest.mark.parametrize("shape,P,n", [("tet", 4, 1 << 20), ("hex", 8, 1 << 16), ("pyr", 6, 1 << 18), ("prism", 10, 1 << 14)])
+def test_every_element_at_scale_by_independent_routes(sk, shape, P, n):
+    """Full-size blocks, EVERY element checked: the collocated kernel (Alg. 6)
+    against the non-collocated one (Alg. 5: derivative-table sum
+    factorisation, a different set of sweeps) -- the reference's own
+    coll == noncoll identity (test_acceptance.py:129-142) -- and the
+    sum-factorised mass against the StdMat/DMMA mass where one exists.  A
+    skipped, duplicated or misplaced element anywhere in the block would
+    break the per-element comparison (sampled oracle checks and the
+    symmetry identity cannot see that)."""
+    import os
+
+    b = sk.build_shape_basis(sk.Shape(shape), P)
+    fac = sk.make_synthetic_factors(b, sk.GeometryClass.DEFORMED, n, seed=3)
+    blk = sk.Block(b, fac, sk.FieldState.COEFF, 1, 1)
+    xd = blk.device(sk.AccessQualifier.WRITE_ONLY)
+    xd.uniform_(-1.0, 1.0)
+    coll = sk.helmholtz_apply(blk, 1.0).device().view(n, -1)
+    nonc = sk.helmholtz_apply_noncoll(blk, 1.0).device().view(n, -1)
+    per_el = ((coll - nonc).abs().amax(dim=1) / coll.abs().amax(dim=1)).max().item()
+    assert per_el <= 1e-12, per_el
+    assert (coll.abs().amax(dim=1) > 0).all()  # no element left unwritten
+    old = os.environ.get("SK_MASS_DENSE")
+    try:
+        os.environ["SK_MASS_DENSE"] = "0"
+        ms = sk.mass_apply(blk).device().view(n, -1).clone()
+        os.environ["SK_MASS_DENSE"] = "1"
+        md = sk.mass_apply(blk).device().view(n, -1)
+    finally:
+        if old is None:
+            os.environ.pop("SK_MASS_DENSE", None)
+        else:
+            os.environ["SK_MASS_DENSE"] = old
+    assert ((ms - md).abs().amax(dim=1) / ms.abs().amax(dim=1)).max().item() <= 1e-12
+
+
 @pytest.mark.parametrize("shape,P,width,ncomp", [("tet", 4, 1, 1), ("hex", 3, 8, 2), ("prism", 5, 3, 1)])
 def test_streamed_host_apply(sk, shape, P, width, ncomp):
     """Host-resident input >= STREAM_MIN_BYTES: the chunk-pipelined
