@@ -59,6 +59,12 @@ typedef struct sk_basis sk_basis;
  * Duffy chain-rule factors (shapes.py:265-323), built natively in FP64.
  * Host-only; device copies are made lazily per device on first use. */
 int sk_basis_create(int shape, int order, sk_basis** out);
+/* Same with a per-direction quadrature override (shapes.py:521-541: each
+ * count >= the default P+2 Gauss-Lobatto / P+1 Gauss-Radau-Jacobi, <= 64):
+ * the default counts give the specialised kernels; any other override runs
+ * every operator on the run-time-size dense path (generic.cu), whose
+ * geometry payload is the factors themselves (dxi and w|J|). */
+int sk_basis_create_q(int shape, int order, const int qpoints[3], sk_basis** out);
 int sk_basis_destroy(sk_basis* b);
 /* counts: out[0..5] = Q0, Q1, Q2, n_points, n_modes, order */
 int sk_basis_counts(const sk_basis* b, int64_t out[6]);

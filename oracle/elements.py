@@ -158,9 +158,11 @@ def _warped(P: int, z: np.ndarray):
 
 
 @lru_cache(maxsize=None)
-def element(shape: str, P: int) -> RefElement:
-    """Assemble the per-(shape, P) bundle (shapes.py:466-518, 555-583)."""
-    q = qcounts(shape, P)
+def element(shape: str, P: int, q: tuple | None = None) -> RefElement:
+    """Assemble the per-(shape, P) bundle (shapes.py:466-518, 555-583);
+    ``q`` overrides the per-direction point counts (build_shape_basis
+    qpoints, shapes.py:521-541)."""
+    q = qcounts(shape, P) if q is None else tuple(int(v) for v in q)
     rules = [quad_rule(k, n) for k, n in zip(_KINDS[shape], q)]
     z = tuple(r[0] for r in rules)
     w = tuple(r[1] for r in rules)

@@ -30,6 +30,7 @@ _PL = ctypes.POINTER(ctypes.c_int64)
 _PD = ctypes.POINTER(ctypes.c_double)
 SIGNATURES = {
     "sk_basis_create": (_I, [_I, _I, ctypes.POINTER(_P)]),
+    "sk_basis_create_q": (_I, [_I, _I, ctypes.POINTER(_I), ctypes.POINTER(_P)]),
     "sk_basis_destroy": (_I, [_P]),
     "sk_basis_counts": (_I, [_P, _PL]),
     "sk_basis_table": (_I, [_P, ctypes.c_char_p, _PD, _L, _PL]),

@@ -13,6 +13,7 @@
 
 #include "../../include/sk200.h"
 #include "sk_tune.h"
+#include "generic.hpp"
 #include "sk_opset.hpp"
 
 namespace sk {
@@ -61,6 +62,11 @@ struct sk_basis {
   // first use from the dense B the bwd_trans kernel produces
   std::mutex dmu;
   std::vector<double*> dense_dev;
+  // quadrature override (qpoints): no specialised kernels, the run-time-size
+  // path of generic.cu on device copies of the dense tables
+  bool generic = false;
+  std::mutex gmu;
+  std::vector<double*> gen_dev;
 };
 
 namespace {
@@ -160,7 +166,7 @@ const double* device_dense(sk_basis* b, void* stream, int* status) {
 // StdMat (DMMA) or sum factorisation for the regular collocated Helmholtz:
 // the tuned table, overridden by SK_HELM_DENSE=0/1
 bool use_dense_helm(const sk_basis* b, int geo) {
-  if (geo != SK_GEO_REGULAR || b->ops->dense_doubles <= 0 || !(b->ops->dense_mask & 4)) return false;
+  if (b->generic || geo != SK_GEO_REGULAR || b->ops->dense_doubles <= 0 || !(b->ops->dense_mask & 4)) return false;
   if (const char* v = std::getenv("SK_HELM_DENSE")) {
     if (v[0] == '0') return false;
     if (v[0] == '1') return true;
@@ -171,12 +177,76 @@ bool use_dense_helm(const sk_basis* b, int geo) {
 // StdMat (DMMA) or sum-factorised mass for this basis and geometry class:
 // the tuned table, overridden by SK_MASS_DENSE=0/1
 bool use_dense_mass(const sk_basis* b, int geo) {
-  if (b->ops->dense_doubles <= 0 || !(b->ops->dense_mask & (geo == SK_GEO_DEFORMED ? 2 : 1))) return false;
+  if (b->generic || b->ops->dense_doubles <= 0 || !(b->ops->dense_mask & (geo == SK_GEO_DEFORMED ? 2 : 1)))
+    return false;
   if (const char* v = std::getenv("SK_MASS_DENSE")) {
     if (v[0] == '0') return false;
     if (v[0] == '1') return true;
   }
   return sk::kDenseMass[geo == SK_GEO_DEFORMED ? 1 : 0][b->hb.shape][b->hb.P];
+}
+
+// device tables of a quadrature-override basis: one buffer per device
+// [B | DB0 | DB1 | DB2 | D0 | D1 | D2 | G | refw | z0 | z1 | z2]
+int generic_tables(sk_basis* b, sk::GenTables* t) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_status(e, "cudaGetDevice");
+  const sk::HostBasis& hb = b->hb;
+  const size_t nqm = (size_t)hb.nq * hb.nm;
+  const size_t sizes[12] = {nqm, nqm, nqm, nqm, hb.D[0].size(), hb.D[1].size(), hb.D[2].size(),
+                            hb.G.size(), hb.refw.size(), hb.z[0].size(), hb.z[1].size(), hb.z[2].size()};
+  const double* src[12] = {hb.Bd.data(), hb.DBd[0].data(), hb.DBd[1].data(), hb.DBd[2].data(), hb.D[0].data(),
+                           hb.D[1].data(), hb.D[2].data(), hb.G.data(), hb.refw.data(), hb.z[0].data(),
+                           hb.z[1].data(), hb.z[2].data()};
+  size_t off[13] = {0};
+  for (int i = 0; i < 12; ++i) off[i + 1] = off[i] + sizes[i];
+  {
+    std::lock_guard<std::mutex> lk(b->gmu);
+    if ((int)b->gen_dev.size() <= dev) b->gen_dev.resize(dev + 1, nullptr);
+    if (!b->gen_dev[dev]) {
+      double* p = nullptr;
+      e = cudaMalloc(&p, sizeof(double) * off[12]);
+      for (int i = 0; i < 12 && e == cudaSuccess; ++i)
+        e = cudaMemcpy(p + off[i], src[i], sizeof(double) * sizes[i], cudaMemcpyHostToDevice);
+      if (e != cudaSuccess) {
+        cudaFree(p);
+        return cuda_status(e, "generic table upload");
+      }
+      b->gen_dev[dev] = p;
+    }
+  }
+  const double* p = b->gen_dev[dev];
+  t->B = p + off[0];
+  t->DB0 = p + off[1];
+  t->DB1 = p + off[2];
+  t->DB2 = p + off[3];
+  t->D0 = p + off[4];
+  t->D1 = p + off[5];
+  t->D2 = p + off[6];
+  t->G = p + off[7];
+  t->refw = p + off[8];
+  t->z0 = p + off[9];
+  t->z1 = p + off[10];
+  t->z2 = p + off[11];
+  for (int d = 0; d < 3; ++d) t->Q[d] = hb.Q[d];
+  t->nq = hb.nq;
+  t->nm = hb.nm;
+  t->shape = hb.shape;
+  return SK_OK;
+}
+
+int generic_op(int op) {
+  switch (op) {
+    case sk::OP_BWD: return sk::GEN_BWD;
+    case sk::OP_IPROD: return sk::GEN_IPROD;
+    case sk::OP_MASS: return sk::GEN_MASS;
+    case sk::OP_HELM:
+    case sk::OP_HELM_NC: return sk::GEN_HELM;
+    case sk::OP_PDERIV: return sk::GEN_PDERIV;
+    case sk::OP_IPDERIV: return sk::GEN_IPDERIV;
+  }
+  return -1;
 }
 
 int check_layout(long long E, int W, int ncomp) {
@@ -191,6 +261,27 @@ long long padded(long long E, int W) { return ((E + W - 1) / W) * (long long)W; 
 int run(sk_basis* b, int op, int geo, long long E, int W, int ncomp, const double* in, double* out,
         const double* pay, double lam, long long in_n, long long out_n, void* stream, const double* dense) {
   int st = SK_OK;
+  if (b->generic) {
+    sk::GenTables t;
+    if ((st = generic_tables(b, &t))) return st;
+    sk::GenReq r;
+    r.op = generic_op(op);
+    if (r.op < 0) return fail(SK_ERR_UNSUPPORTED, "operator not on the quadrature-override path");
+    r.geo = geo;
+    r.E = E;
+    r.Epad = padded(E, W);
+    r.in_cs = r.Epad * in_n;
+    r.out_cs = r.Epad * out_n;
+    r.W = W;
+    r.ncomp = ncomp;
+    r.in = in;
+    r.out = out;
+    r.pay = pay;
+    r.lam = lam;
+    if (r.Epad == 0) return SK_OK;
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return cuda_status(sk::generic_launch(t, r, stream), "generic kernel launch");
+  }
   const double* g = device_gtab(b, &st);
   if (st) return st;
   sk::LaunchReq r;
@@ -246,11 +337,42 @@ int sk_basis_create(int shape, int order, sk_basis** out) {
   return SK_OK;
 }
 
+int sk_basis_create_q(int shape, int order, const int qpoints[3], sk_basis** out) {
+  if (!out) return fail(SK_ERR_ARG, "null output handle");
+  *out = nullptr;
+  if (!qpoints) return sk_basis_create(shape, order, out);
+  if (shape < SK_SHAPE_QUAD || shape > SK_SHAPE_TET) return fail(SK_ERR_STATE, "unknown shape id");
+  if (shape < SK_SHAPE_HEX) return fail(SK_ERR_UNSUPPORTED, "2D shapes are not on the device path");
+  if (order < 1 || order > 10) return fail(SK_ERR_UNSUPPORTED, "order outside the compiled range 1..10");
+  const int s = shape - SK_SHAPE_HEX;
+  sk::HostBasis probe;
+  if (!sk::build_host_basis(s, order, probe)) return fail(SK_ERR_UNSUPPORTED, "unsupported (shape, order)");
+  bool dflt = true;
+  for (int d = 0; d < 3; ++d) {
+    if (qpoints[d] < probe.Q[d]) return fail(SK_ERR_ARG, "quadrature override below the default point count");
+    if (qpoints[d] > 64) return fail(SK_ERR_UNSUPPORTED, "quadrature override above 64 points per direction");
+    dflt = dflt && qpoints[d] == probe.Q[d];
+  }
+  if (dflt) return sk_basis_create(shape, order, out);
+  std::unique_ptr<sk_basis> b(new sk_basis());
+  b->shape_ref = shape;
+  try {
+    if (!sk::build_host_basis(s, order, b->hb, qpoints)) return fail(SK_ERR_ARG, "bad quadrature override");
+  } catch (const std::exception& ex) {
+    return fail(SK_ERR_ARG, ex.what());
+  }
+  b->generic = true;
+  *out = b.release();
+  return SK_OK;
+}
+
 int sk_basis_destroy(sk_basis* b) {
   if (!b) return SK_OK;
   for (double* p : b->gtab_dev)
     if (p) cudaFree(p);
   for (double* p : b->dense_dev)
+    if (p) cudaFree(p);
+  for (double* p : b->gen_dev)
     if (p) cudaFree(p);
   delete b;
   return SK_OK;
@@ -284,6 +406,10 @@ int sk_payload_size(const sk_basis* b, int geo_class, int kind, int64_t E, int64
   if (geo_class != SK_GEO_REGULAR && geo_class != SK_GEO_DEFORMED) return fail(SK_ERR_ARG, "bad geometry class");
   if (kind < 0 || kind > 3) return fail(SK_ERR_ARG, "bad payload kind");
   if (E < 0) return fail(SK_ERR_ARG, "element count must be nonnegative");
+  if (b->generic) {  // the factors themselves: dxi (9 per point / element) and w|J|
+    *n = 10 * E * (geo_class == SK_GEO_DEFORMED ? (int64_t)b->hb.nq : 1);
+    return SK_OK;
+  }
   *n = b->ops->payload_doubles(kind, geo_class) * b->ops->payload_elements(kind, E);
   return SK_OK;
 }
@@ -293,6 +419,13 @@ int sk_payload_pack(const sk_basis* b, int geo_class, int kind, int64_t E, const
   if (!b || (E > 0 && (!dxi || !jac || !pay))) return fail(SK_ERR_ARG, "null argument");
   if (geo_class != SK_GEO_REGULAR && geo_class != SK_GEO_DEFORMED) return fail(SK_ERR_ARG, "bad geometry class");
   if (kind < 0 || kind > 3 || E < 0) return fail(SK_ERR_ARG, "bad payload kind or element count");
+  if (b->generic) {
+    const size_t nd = (size_t)E * (geo_class == SK_GEO_DEFORMED ? b->hb.nq : 1);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaError_t e = cudaMemcpyAsync(pay, dxi, sizeof(double) * 9 * nd, cudaMemcpyDeviceToDevice, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(pay + 9 * nd, jac, sizeof(double) * nd, cudaMemcpyDeviceToDevice, s);
+    return cuda_status(e, "payload copy");
+  }
   int st = SK_OK;
   const double* g = device_gtab(const_cast<sk_basis*>(b), &st);
   if (st) return st;
@@ -305,7 +438,17 @@ static int geometry_common(const sk_basis* b, int mode, int64_t E, const double*
   if (!b || (E > 0 && !src)) return fail(SK_ERR_ARG, "null argument");
   if (E < 0) return fail(SK_ERR_ARG, "element count must be nonnegative");
   int st = SK_OK;
-  const double* g = device_gtab(const_cast<sk_basis*>(b), &st);
+  sk::GenTables gt;
+  const double* g = nullptr;
+  if (b->generic) {
+    if ((st = generic_tables(const_cast<sk_basis*>(b), &gt))) return st;
+    if (kind >= 0) {  // a payload is the factors: dxi then w|J|
+      dxi = pay;
+      jac = pay + (size_t)9 * E * b->hb.nq;
+    }
+  } else {
+    g = device_gtab(const_cast<sk_basis*>(b), &st);
+  }
   if (st) return st;
   unsigned long long* d_bad = nullptr;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -313,7 +456,8 @@ static int geometry_common(const sk_basis* b, int mode, int64_t E, const double*
   if (e == cudaSuccess) e = cudaMemsetAsync(d_bad, 0, sizeof(unsigned long long), s);
   if (e != cudaSuccess) return cuda_status(e, "geometry scratch");
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  int r = b->ops->geometry(mode, E, src, dxi, jac, kind, pay, d_bad, g, stream);
+  int r = b->generic ? sk::generic_geometry(gt, mode, E, src, dxi, jac, d_bad, stream)
+                     : b->ops->geometry(mode, E, src, dxi, jac, kind, pay, d_bad, g, stream);
   if (r) {
     cudaFreeAsync(d_bad, s);
     return cuda_status(r, "geometry kernel");
@@ -420,6 +564,7 @@ int sk_helmholtz_apply_staged(const sk_basis* b, int geo, int64_t E, int W, int 
                               void* stream) {
   if (!b || (E > 0 && (!uhat || !hpay || !out || !work))) return fail(SK_ERR_ARG, "null argument");
   if (geo != SK_GEO_DEFORMED) return fail(SK_ERR_UNSUPPORTED, "the staged variant is built for deformed geometry");
+  if (b->generic) return fail(SK_ERR_UNSUPPORTED, "the staged variant needs the default quadrature");
   if (!(lam >= 0.0)) return fail(SK_ERR_ARG, "reaction coefficient must be nonnegative");
   if (int st = check_layout(E, W, ncomp)) return st;
   // chunks start on a multiple of the interleave width and of 16 (tile and
@@ -512,6 +657,7 @@ int sk_apply_streamed(const sk_basis* b, int op, int geo, int64_t E, int W, int 
   if (geo != SK_GEO_REGULAR && geo != SK_GEO_DEFORMED) return fail(SK_ERR_ARG, "bad geometry class");
   if (op != SK_STREAM_HELMHOLTZ && op != SK_STREAM_HELMHOLTZ_NC && op != SK_STREAM_MASS)
     return fail(SK_ERR_ARG, "unknown streamed operator");
+  if (b->generic) return fail(SK_ERR_UNSUPPORTED, "streamed applies need the default quadrature");
   if (op != SK_STREAM_MASS && !(lam >= 0.0)) return fail(SK_ERR_ARG, "reaction coefficient must be nonnegative");
   if (int st = check_layout(E, W, ncomp)) return st;
   const int kop = op == SK_STREAM_MASS ? sk::OP_MASS : op == SK_STREAM_HELMHOLTZ_NC ? sk::OP_HELM_NC : sk::OP_HELM;
@@ -597,6 +743,7 @@ int sk_apply_streamed(const sk_basis* b, int op, int geo, int64_t E, int W, int 
 
 int sk_helmholtz_apply_c0(const sk_basis* b, int geo, int nx, int ny, int64_t nz_local, const double* x,
                           const double* hpay, double lam, double* out, void* stream) {
+  if (b && b->generic) return fail(SK_ERR_UNSUPPORTED, "the C0 variant needs the default quadrature");
   if (!b || nx < 1 || ny < 1 || nz_local < 0) return fail(SK_ERR_ARG, "bad C0 slab");
   if (b->ops->S != sk::HEX) return fail(SK_ERR_UNSUPPORTED, "assembled C0 variant is hex only");
   if (geo != SK_GEO_DEFORMED || !(lam > 0.0)) return fail(SK_ERR_UNSUPPORTED, "fused C0 gather: deformed, lam > 0");
@@ -675,6 +822,12 @@ int sk_launch_config(const sk_basis* b, int op, int64_t out[3]) {
 
 int sk_launch_config_geo(const sk_basis* b, int op, int geo_class, int64_t out[3]) {
   if (!b || !out || op < 0 || op >= sk::OP_COUNT) return fail(SK_ERR_ARG, "bad argument");
+  if (b->generic) {  // generic.cu: one element per 128-thread CTA
+    out[0] = 1;
+    out[1] = 128;
+    out[2] = 8 * (b->hb.nm + 4 * (int64_t)b->hb.nq);
+    return SK_OK;
+  }
   if (geo_class != SK_GEO_REGULAR && geo_class != SK_GEO_DEFORMED) return fail(SK_ERR_ARG, "bad geometry class");
   b->ops->config(op, geo_class, out);  // SK_GEO_* == sk::GEO_* (0 regular, 1 deformed)
   return SK_OK;

@@ -10,6 +10,7 @@
 //   sum-fac tables               speckern/shapes.py:555-583
 #include "basis_host.hpp"
 
+#include <algorithm>
 #include <cmath>
 #include <stdexcept>
 
@@ -204,6 +205,66 @@ void warped_family(int P, const std::vector<double>& z, std::vector<std::vector<
 
 }  // namespace
 
+// Dense basis matrix B[l][m] (shapes.py:491-492 bmat; mode factors with the
+// collapsed-vertex exceptions of shapes.py:374-405) and its collocation
+// derivatives DB_d = D_d B along each tensor direction (operators.py:449-464)
+void build_dense(HostBasis& B) {
+  const int Q0 = B.Q[0], Q1 = B.Q[1], Q2 = B.Q[2], P1 = B.P + 1, nm = B.nm, nq = B.nq;
+  B.Bd.assign((size_t)nq * nm, 0.0);
+  for (int m = 0; m < nm; ++m) {
+    const int p = B.modes[3 * m], q = B.modes[3 * m + 1], r = B.modes[3 * m + 2];
+    for (int i = 0; i < Q0; ++i)
+      for (int j = 0; j < Q1; ++j)
+        for (int k = 0; k < Q2; ++k) {
+          double f0 = B.a[0][i * P1 + p], f1 = 0.0, f2 = 0.0;
+          switch (B.shape) {
+            case HEX:
+              f1 = B.a[1][j * P1 + q];
+              f2 = B.a[2][k * P1 + r];
+              break;
+            case PRISM:
+              f1 = B.a[1][j * P1 + q];
+              f2 = B.c2[p][k * (P1 - p) + r];
+              if (p == 0 && r == 1) f0 = 1.0;  // (0, q, 1): psi_b(0,1)(eta3) psi_a(q)(eta2)
+              break;
+            case PYR: {
+              const int mx = std::max(p, q);
+              f1 = B.a[1][j * P1 + q];
+              f2 = B.c2[mx][k * (P1 - mx) + r];
+              if (p == 0 && q == 0 && r == 1) f0 = f1 = 1.0;  // apex
+              break;
+            }
+            case TET:
+              f1 = B.b1[p][j * (P1 - p) + q];
+              f2 = B.c2[p + q][k * (P1 - p - q) + r];
+              if (p == 0 && q == 0 && r == 1) f0 = f1 = 1.0;  // apex
+              if (p == 0 && q == 1) {                        // (0, 1, r): psi_b(0,1)(eta2) psi_b(1,r)(eta3)
+                f0 = 1.0;
+                f1 = B.b1[0][j * P1 + 1];
+                f2 = B.c2[1][k * (P1 - 1) + r];
+              }
+              break;
+          }
+          B.Bd[(size_t)((i * Q1 + j) * Q2 + k) * nm + m] = f0 * f1 * f2;
+        }
+  }
+  for (int d = 0; d < 3; ++d) {
+    B.DBd[d].assign((size_t)nq * nm, 0.0);
+    const int Qd = B.Q[d];
+    for (int i = 0; i < Q0; ++i)
+      for (int j = 0; j < Q1; ++j)
+        for (int k = 0; k < Q2; ++k) {
+          const int l = (i * Q1 + j) * Q2 + k, a = d == 0 ? i : d == 1 ? j : k;
+          for (int b = 0; b < Qd; ++b) {
+            const int lb = d == 0 ? (b * Q1 + j) * Q2 + k : d == 1 ? (i * Q1 + b) * Q2 + k : (i * Q1 + j) * Q2 + b;
+            const double dab = B.D[d][a * Qd + b];
+            if (dab == 0.0) continue;
+            for (int m = 0; m < nm; ++m) B.DBd[d][(size_t)l * nm + m] += dab * B.Bd[(size_t)lb * nm + m];
+          }
+        }
+  }
+}
+
 int mode_count(int shape, int P) {
   switch (shape) {
     case HEX: return (P + 1) * (P + 1) * (P + 1);
@@ -214,7 +275,7 @@ int mode_count(int shape, int P) {
   return 0;
 }
 
-bool build_host_basis(int shape, int P, HostBasis& B) {
+bool build_host_basis(int shape, int P, HostBasis& B, const int* qpoints) {
   if (shape < HEX || shape > TET || P < 1 || P > 10) return false;
   static const Kind kinds[4][3] = {
       {GLL, GLL, GLL}, {GLL, GLL, GRJ1}, {GLL, GLL, GRJ2}, {GLL, GRJ1, GRJ2}};
@@ -224,7 +285,10 @@ bool build_host_basis(int shape, int P, HostBasis& B) {
   B.shape = shape;
   B.P = P;
   for (int d = 0; d < 3; ++d) {
-    B.Q[d] = kinds[shape][d] == GLL ? P + 2 : P + 1;
+    const int qdef = kinds[shape][d] == GLL ? P + 2 : P + 1;
+    // shapes.py:532-541: an override may only raise the per-direction count
+    if (qpoints && qpoints[d] < qdef) return false;
+    B.Q[d] = qpoints ? qpoints[d] : qdef;
     rule(kinds[shape][d], B.Q[d], B.z[d], B.w[d]);
     B.D[d] = diff_matrix(B.z[d]);
   }
@@ -310,6 +374,10 @@ bool build_host_basis(int shape, int P, HostBasis& B) {
   }
   N["refw"] = B.refw;
   N["G"] = B.G;
+  if (qpoints) {  // the generic device path of a quadrature override works on dense matrices
+    build_dense(B);
+    N["B"] = B.Bd;
+  }
   N["modes"] = std::vector<double>(B.modes.begin(), B.modes.end());
   return true;
 }

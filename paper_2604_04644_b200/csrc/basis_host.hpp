@@ -26,11 +26,17 @@ struct HostBasis {
   std::vector<std::vector<double>> b1, db1;  // direction 1 (tet)
   std::vector<std::vector<double>> c2, dc2;  // direction 2 (prism, pyr, tet)
   std::vector<int> modes;            // nm x 3 (p, q, r)
+  // dense basis matrix (nq x nm, row-major) and its collocation derivatives
+  // per tensor direction: the generic (quadrature-override) device path
+  std::vector<double> Bd, DBd[3];
   std::map<std::string, std::vector<double>> named;  // flat view for sk_basis_table
 };
 
-// Build all tables; returns false for unsupported (shape, order).
-bool build_host_basis(int shape, int P, HostBasis& out);
+// Build all tables; returns false for unsupported (shape, order) or a
+// quadrature override below the default counts.  qpoints: per-direction point
+// counts (null: P+2 Gauss-Lobatto / P+1 Gauss-Radau-Jacobi, shapes.py:132-139).
+bool build_host_basis(int shape, int P, HostBasis& out, const int* qpoints = nullptr);
+void build_dense(HostBasis& B);
 
 int mode_count(int shape, int P);
 

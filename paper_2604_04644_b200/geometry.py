@@ -81,8 +81,8 @@ class GeometricFactors:
     deformed; ``jac``: |J| (E,) regular, w|J| (E, NQ) deformed.  Deformed
     factors may be held lazily as deformation parameters (``params``, E x 12)
     and materialised on demand.  Device payloads are cached per (basis
-    shape, order, kind, device) and are independent of the block's
-    interleave width.
+    shape, order, point counts, kind, device) and are independent of the
+    block's interleave width.
     """
 
     def __init__(
@@ -150,7 +150,7 @@ class GeometricFactors:
         dev = torch.cuda.current_device()
         # the payload layout (lane width, point count) depends on the basis:
         # one regular GeometricFactors may serve bases of several orders
-        key = (basis.shape, basis.order, kind, dev)
+        key = (basis.shape, basis.order, basis.qcounts, kind, dev)
         if key in self._payloads:
             return self._payloads[key]
         lib = _lib.load()

@@ -123,7 +123,7 @@ def _streamed(block: Block, out: Block, op: int, pay, lam: float) -> bool:
     leaving input and output live in both spaces (one transfer each, as the
     plain path would count them).  Returns False when not applicable."""
     reg = block.region
-    if not reg.host_resident() or out is block or reg.length * 8 < STREAM_MIN_BYTES:
+    if not reg.host_resident() or out is block or reg.length * 8 < STREAM_MIN_BYTES or block.basis.generic:
         return False
     import torch
 

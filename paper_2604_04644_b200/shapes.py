@@ -107,14 +107,18 @@ class ShapeBasis:
     reference dataclass, shapes.py:412-441).  ``handle`` is the
     ``sk_basis*`` every device operator takes."""
 
-    def __init__(self, shape: Shape, order: int):
+    def __init__(self, shape: Shape, order: int, qpoints: tuple[int, int, int] | None = None):
         if shape not in DEVICE_SHAPES:
             from paper_2604_04644_b200.operators import UnsupportedStrategyError
 
             raise UnsupportedStrategyError(f"{shape.value}: only 3D shapes are on the device path")
         lib = _lib.load()
         h = ctypes.c_void_p()
-        _lib.check(lib.sk_basis_create(shape.abi_id, order, ctypes.byref(h)), "sk_basis_create")
+        if qpoints is None:
+            _lib.check(lib.sk_basis_create(shape.abi_id, order, ctypes.byref(h)), "sk_basis_create")
+        else:
+            q = (ctypes.c_int * 3)(*qpoints)
+            _lib.check(lib.sk_basis_create_q(shape.abi_id, order, q, ctypes.byref(h)), "sk_basis_create_q")
         self.handle = h
         self.shape = shape
         self.order = order
@@ -123,6 +127,9 @@ class ShapeBasis:
         self.qcounts = (int(cnt[0]), int(cnt[1]), int(cnt[2]))
         self.n_points = int(cnt[3])
         self.n_modes = int(cnt[4])
+        # a quadrature override runs on the run-time-size device path
+        # (generic.cu); the default counts on the specialised kernels
+        self.generic = self.qcounts != quad_point_counts(shape, order)
         self._tables: dict[str, np.ndarray] = {}
 
     def __del__(self):
@@ -189,17 +196,24 @@ class ShapeBasis:
 
 
 @lru_cache(maxsize=None)
-def _cached(shape: Shape, order: int) -> ShapeBasis:
-    return ShapeBasis(shape, order)
+def _cached(shape: Shape, order: int, qpoints: tuple[int, int, int] | None = None) -> ShapeBasis:
+    return ShapeBasis(shape, order, qpoints)
 
 
 def build_shape_basis(shape: Shape, order: int, qpoints: tuple[int, ...] | None = None) -> ShapeBasis:
-    """shapes.py:521-541.  The device kernels are specialised for the default
-    quadrature, so a ``qpoints`` override other than the default raises."""
+    """shapes.py:521-541.  ``qpoints`` overrides the per-direction point
+    counts (each at least the default, as the reference checks); the
+    default counts run on the specialised kernels, any other override on the
+    run-time-size dense device path (same operators, no CPU fallback)."""
     if order < 1:
         raise ValueError(f"polynomial order must be at least 1, got {order}")
-    if qpoints is not None and tuple(int(q) for q in qpoints) != quad_point_counts(shape, order):
-        from paper_2604_04644_b200.operators import UnsupportedStrategyError
-
-        raise UnsupportedStrategyError("device kernels are specialised for the default quadrature")
-    return _cached(shape, order)
+    if qpoints is not None:
+        qpoints = tuple(int(q) for q in qpoints)
+        if len(qpoints) != 3:
+            raise ValueError(f"{shape.value} needs 3 point counts, got {len(qpoints)}")
+        for q, qmin in zip(qpoints, quad_point_counts(shape, order)):
+            if q < qmin:
+                raise ValueError(f"direction needs at least {qmin} points for order {order}, got {q}")
+        if qpoints == quad_point_counts(shape, order):
+            qpoints = None
+    return _cached(shape, order, qpoints)

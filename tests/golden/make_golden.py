@@ -141,15 +141,59 @@ def bench_workload(out):
     out["bench_tet_P4_x"] = np.ascontiguousarray(vals[idx].T)
 
 
+#: quadrature overrides (shapes.py:521-541): every shape, one or more
+#: directions above the default P+2 / P+1 counts
+QPOINT_CASES = [
+    (Shape.HEX, 2, (5, 4, 6)),
+    (Shape.PRISM, 3, (6, 5, 6)),
+    (Shape.PYR, 2, (5, 6, 4)),
+    (Shape.TET, 3, (6, 5, 6)),
+    (Shape.TET, 1, (3, 4, 2)),
+]
+
+
+def qpoint_operators(out):
+    """Every operator on blocks whose basis carries a quadrature override."""
+    for shp, P, q in QPOINT_CASES:
+        sidx = list(Shape).index(shp)
+        sb = build_shape_basis(shp, P, q)
+        for gcls in (GeometryClass.REGULAR, GeometryClass.DEFORMED):
+            k = f"{shp.value}_P{P}_q{''.join(map(str, q))}_{gcls.value}"
+            fac = make_synthetic_factors(sb, gcls, N_EL, seed=5)
+            out[f"{k}_dxi"] = fac.dxi_dx
+            out[f"{k}_jac"] = fac.jac
+            cb = Block(sb, fac, FieldState.COEFF, 1, WIDTH)
+            out[f"{k}_x"] = _fill(cb, [5, sidx, P, 1])
+            out[f"{k}_bwd"] = bwd_trans(cb, Strategy.SUM_FAC).get_elements()[0]
+            out[f"{k}_mass"] = mass_apply(cb, Strategy.SUM_FAC).get_elements()[0]
+            for lam in (0.0, 1.0):
+                out[f"{k}_helm_{lam}"] = helmholtz_apply_coll(cb, lam, Strategy.SUM_FAC).get_elements()[0]
+            out[f"{k}_helmnc_1.0"] = helmholtz_apply_noncoll(cb, 1.0, Strategy.SUM_FAC).get_elements()[0]
+            pb = Block(sb, fac, FieldState.PHYS, 1, WIDTH)
+            out[f"{k}_y"] = _fill(pb, [5, sidx, P, 2])
+            out[f"{k}_iprod"] = iproduct_wrt_base(pb, Strategy.SUM_FAC).get_elements()[0]
+            out[f"{k}_dphys"] = phys_deriv(pb).get_elements()
+            vb = Block(sb, fac, FieldState.PHYS, 3, WIDTH)
+            v = np.random.default_rng([5, sidx, P, 3]).uniform(-1.0, 1.0, size=(3, sb.n_points, N_EL))
+            vb.set_elements(v)
+            out[f"{k}_v"] = v
+            out[f"{k}_ipderiv"] = iproduct_wrt_deriv_base(vb, Strategy.SUM_FAC).get_elements()[0]
+
+
 def main():
-    t = {}
-    tables(t)
-    np.savez_compressed(os.path.join(HERE, "tables.npz"), **t)
-    o = {}
-    operators(o)
-    bench_workload(o)
-    np.savez_compressed(os.path.join(HERE, "operators.npz"), **o)
-    for name in ("tables.npz", "operators.npz"):
+    only_q = len(sys.argv) > 1 and sys.argv[1] == "qpoints"
+    if not only_q:
+        t = {}
+        tables(t)
+        np.savez_compressed(os.path.join(HERE, "tables.npz"), **t)
+        o = {}
+        operators(o)
+        bench_workload(o)
+        np.savez_compressed(os.path.join(HERE, "operators.npz"), **o)
+    qo = {}
+    qpoint_operators(qo)
+    np.savez_compressed(os.path.join(HERE, "operators_qpoints.npz"), **qo)
+    for name in ("tables.npz", "operators.npz", "operators_qpoints.npz"):
         print(name, os.path.getsize(os.path.join(HERE, name)) // 1024, "KiB")
 
 

@@ -47,8 +47,10 @@ def test_status_codes_and_errors():
     assert lib.sk_basis_create(2, 11, ctypes.byref(h)) == _lib.SK_ERR_UNSUPPORTED
     with pytest.raises(sk.UnsupportedStrategyError):
         sk.build_shape_basis(sk.Shape.QUAD, 2)
-    with pytest.raises(sk.UnsupportedStrategyError):
-        sk.build_shape_basis(sk.Shape.HEX, 2, qpoints=(5, 5, 5))
+    with pytest.raises(ValueError):  # below the default counts (shapes.py:532-541)
+        sk.build_shape_basis(sk.Shape.HEX, 2, qpoints=(3, 5, 5))
+    q = (ctypes.c_int * 3)(4, 4, 3)
+    assert lib.sk_basis_create_q(2, 2, q, ctypes.byref(h)) == _lib.SK_ERR_ARG
     b = sk.build_shape_basis(sk.Shape.TET, 3)
     # argument checks happen before any device work
     assert lib.sk_helmholtz_apply(b.handle, 1, 0, 4, 1, 1, None, None, -1.0, None, None) == _lib.SK_ERR_ARG
@@ -87,3 +89,24 @@ def test_native_tables_match_reference(golden_tables, shape, P):
             p += 1
     close(b.ref_weights, g[f"{k}_refw"])
     close(b.gdense, g[f"{k}_G"], 1e-14)
+
+
+
+@pytest.mark.parametrize("shape,P,q", [("hex", 2, (5, 4, 6)), ("prism", 3, (6, 5, 6)), ("pyr", 2, (5, 6, 4)),
+                                       ("tet", 3, (6, 5, 6)), ("tet", 1, (3, 4, 2))])
+def test_quadrature_override_tables(shape, P, q):
+    """A qpoints basis (build_shape_basis override): native rules, weights,
+    collocation matrices and the dense basis matrix of the generic device
+    path equal the oracle's (pinned to the reference's qpoints operators in
+    test_oracle_golden.py)."""
+    import oracle as O
+    import paper_2604_04644_b200 as sk
+
+    b = sk.build_shape_basis(sk.Shape(shape), P, q)
+    el = O.element(shape, P, q)
+    assert b.qcounts == q and b.generic and b.n_points == el.nq
+    for d in range(3):
+        assert np.allclose(b.table(f"z{d}"), el.z[d], rtol=0, atol=1e-14)
+        assert np.allclose(b.table(f"w{d}"), el.w[d], rtol=0, atol=1e-14)
+    assert np.allclose(b.ref_weights, el.refw, rtol=0, atol=1e-14)
+    assert np.allclose(b.table("B").reshape(el.nq, el.nm), el.bmat, rtol=0, atol=1e-13)

@@ -2,6 +2,8 @@
 the reference produced (tests/golden/make_golden.py) must be reproduced by the
 numpy restatement in ``oracle/``."""
 
+import os
+
 import numpy as np
 import pytest
 
@@ -111,3 +113,35 @@ def test_two_dense_routes(shape):
             a = O.dense_helmholtz(el, geom, 1.5)
             b = O.dense_helmholtz_factored(el, geom, 1.5)
             assert np.max(np.abs(a - b)) / np.max(np.abs(a)) <= 1e-12
+
+
+QCASES = [("hex", 2, (5, 4, 6)), ("prism", 3, (6, 5, 6)), ("pyr", 2, (5, 6, 4)), ("tet", 3, (6, 5, 6)), ("tet", 1, (3, 4, 2))]
+
+
+@pytest.fixture(scope="module")
+def golden_q():
+    from conftest import GOLDEN
+
+    return np.load(os.path.join(GOLDEN, "operators_qpoints.npz"))
+
+
+@pytest.mark.parametrize("shape,P,q", QCASES)
+@pytest.mark.parametrize("gname", ["regular", "deformed"])
+def test_oracle_quadrature_override_matches_reference(golden_q, shape, P, q, gname):
+    """The oracle with a qpoints override (element(shape, P, q)) reproduces
+    the reference's operators on the reference's own factors."""
+    k = f"{shape}_P{P}_q{''.join(map(str, q))}_{gname}"
+    g = golden_q
+    el = O.element(shape, P, q)
+    geo = O.Geometry(gname == "deformed", g[f"{k}_dxi"], g[f"{k}_jac"])
+    x, y, v = g[f"{k}_x"], g[f"{k}_y"], g[f"{k}_v"]
+    tol = 1e-13
+    assert O.rel_diff(O.bwd_trans(el, geo, x), g[f"{k}_bwd"]) <= tol
+    assert O.rel_diff(O.mass(el, geo, x), g[f"{k}_mass"]) <= tol
+    for lam in (0.0, 1.0):
+        assert O.rel_diff(O.helmholtz_coll(el, geo, x, lam), g[f"{k}_helm_{lam}"]) <= tol
+    assert O.rel_diff(O.helmholtz_noncoll(el, geo, x, 1.0), g[f"{k}_helmnc_1.0"]) <= tol
+    assert O.rel_diff(O.iproduct_wrt_base(el, geo, y), g[f"{k}_iprod"]) <= tol
+    assert O.rel_diff(O.phys_deriv(el, geo, y), g[f"{k}_dphys"]) <= tol
+    assert O.rel_diff(O.iproduct_wrt_deriv_base(el, geo, v), g[f"{k}_ipderiv"]) <= tol
+    assert O.rel_diff(O.synthetic_geometry(el, gname == "deformed", 2, seed=5).jac, g[f"{k}_jac"]) <= 1e-13

@@ -410,3 +410,58 @@ def test_dense_dmma_regular_helmholtz(sk, monkeypatch, shape, P):
             got = sk.helmholtz_apply(blk, lam).get_elements()
             for c in range(2):
                 assert _err(got[c], O.helmholtz_coll(el, geo, x[c], lam)) <= TOL, (width, lam, c)
+
+
+QCASES = [("hex", 2, (5, 4, 6)), ("prism", 3, (6, 5, 6)), ("pyr", 2, (5, 6, 4)), ("tet", 3, (6, 5, 6)), ("tet", 1, (3, 4, 2))]
+
+
+@pytest.mark.parametrize("shape,P,q", QCASES)
+@pytest.mark.parametrize("gname", ["regular", "deformed"])
+def test_quadrature_override_against_reference(sk, shape, P, q, gname):
+    """build_shape_basis(shape, P, qpoints) above the default counts (the
+    run-time-size device path): every operator against the reference's own
+    outputs on the reference's factors (tests/golden/operators_qpoints.npz),
+    and the device geometry builder against the reference's factors."""
+    from conftest import GOLDEN
+    import os
+
+    g = np.load(os.path.join(GOLDEN, "operators_qpoints.npz"))
+    k = f"{shape}_P{P}_q{''.join(map(str, q))}_{gname}"
+    b = sk.build_shape_basis(sk.Shape(shape), P, q)
+    assert b.qcounts == q and b.generic
+    deformed = gname == "deformed"
+    gcls = sk.GeometryClass.DEFORMED if deformed else sk.GeometryClass.REGULAR
+    fac = sk.GeometricFactors(gcls, sk.Shape(shape), 2, dxi_dx=g[f"{k}_dxi"], jac=g[f"{k}_jac"])
+    blk = sk.Block(b, fac, sk.FieldState.COEFF, 1, 2)
+    blk.set_elements(g[f"{k}_x"][None])
+    n0 = sk._lib.launch_count() if hasattr(sk, "_lib") else None
+    for lam in (0.0, 1.0):
+        assert _err(sk.helmholtz_apply(blk, lam).get_elements()[0], g[f"{k}_helm_{lam}"]) <= TOL, lam
+    assert _err(sk.helmholtz_apply_noncoll(blk, 1.0).get_elements()[0], g[f"{k}_helmnc_1.0"]) <= TOL
+    assert _err(sk.mass_apply(blk).get_elements()[0], g[f"{k}_mass"]) <= TOL
+    assert _err(sk.bwd_trans(blk).get_elements()[0], g[f"{k}_bwd"]) <= TOL
+    pb = blk.like(sk.FieldState.PHYS)
+    pb.set_elements(g[f"{k}_y"][None])
+    assert _err(sk.iproduct_wrt_base(pb).get_elements()[0], g[f"{k}_iprod"]) <= TOL
+    assert _err(sk.phys_deriv(pb).get_elements(), g[f"{k}_dphys"]) <= TOL
+    vb = blk.like(sk.FieldState.PHYS, 3)
+    vb.set_elements(g[f"{k}_v"])
+    assert _err(sk.iproduct_wrt_deriv_base(vb).get_elements()[0], g[f"{k}_ipderiv"]) <= TOL
+    if deformed:
+        syn = sk.make_synthetic_factors(b, gcls, 2, seed=5)
+        assert _err(syn.jac, g[f"{k}_jac"]) <= 1e-13
+        # operators on the device-built factors of many elements vs the oracle
+        n = 37
+        el = O.element(shape, P, q)
+        geo = O.synthetic_geometry(el, True, n, seed=7)
+        cb = sk.Block(b, sk.make_synthetic_factors(b, gcls, n, seed=7), sk.FieldState.COEFF, 1, 1)
+        x = np.random.default_rng(3).uniform(-1, 1, (el.nm, n))
+        cb.set_elements(x[None])
+        assert _err(sk.helmholtz_apply(cb, 0.8).get_elements()[0], O.helmholtz_coll(el, geo, x, 0.8)) <= TOL
+    del n0
+
+
+def test_quadrature_override_validation(sk):
+    with pytest.raises(ValueError):
+        sk.build_shape_basis(sk.Shape.TET, 3, (5, 3, 4))  # below the default (5, 4, 4)
+    assert not sk.build_shape_basis(sk.Shape.TET, 3, (5, 4, 4)).generic  # the default itself
