@@ -13,7 +13,8 @@ the reference's public data model:
   ``block._payload_cache`` beside the reference's own payloads
   (field_block.py:309-321);
 * ``list(Shape).index(shape)``, ``basis.order`` and ``basis.qcounts`` -- the
-  basis handle (``sk_basis_create``).
+  basis handle (``sk_basis_create_q``; a qpoints override runs the library's
+  run-time-size path).
 
 It loads nothing but ``libsk200.so`` (device memory through the library's
 own ``sk_device_alloc`` / ``sk_copy_*``; no torch, no cuda-python).  ABI
@@ -67,6 +68,7 @@ def _lib():
                 vp, i, i64, d = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double
                 sig = {
                     "sk_basis_create": [i, i, ctypes.POINTER(vp)],
+                    "sk_basis_create_q": [i, i, ctypes.POINTER(i), ctypes.POINTER(vp)],
                     "sk_basis_counts": [vp, ctypes.POINTER(i64)],
                     "sk_payload_size": [vp, i, i, i64, ctypes.POINTER(i64)],
                     "sk_payload_pack": [vp, i, i, i64, vp, vp, vp, vp],
@@ -130,25 +132,22 @@ _BASES: dict = {}
 
 
 def _basis(block):
-    """libsk200 basis handle for the block's (shape, order); the kernels are
-    specialised for the reference's default quadrature (shapes.py:132-139)."""
-    from speckern.operators import UnsupportedStrategyError
+    """libsk200 basis handle for the block's (shape, order, point counts):
+    the default quadrature (shapes.py:132-139) runs the specialised kernels,
+    a qpoints override (shapes.py:521-541) the library's run-time-size path."""
     from speckern.shapes import Shape
 
     sb = block.basis
-    key = (sb.shape, sb.order)
+    q = tuple(int(v) for v in sb.qcounts)
+    key = (sb.shape, sb.order, q)
     with _LOCK:
         if key not in _BASES:
             h = ctypes.c_void_p()
-            _check(_lib().sk_basis_create(list(Shape).index(sb.shape), sb.order, ctypes.byref(h)), "sk_basis_create")
+            qa = (ctypes.c_int * 3)(*q)
+            _check(_lib().sk_basis_create_q(list(Shape).index(sb.shape), sb.order, qa, ctypes.byref(h)),
+                   "sk_basis_create_q")
             _BASES[key] = h
-        h = _BASES[key]
-    counts = (ctypes.c_int64 * 6)()
-    _check(_lib().sk_basis_counts(h, counts), "sk_basis_counts")
-    if tuple(int(q) for q in sb.qcounts) != tuple(int(counts[i]) for i in range(3)):
-        raise UnsupportedStrategyError(
-            f"sumfac_top kernels use the default quadrature {tuple(counts[:3])}, got qpoints {sb.qcounts}")
-    return h
+        return _BASES[key]
 
 
 def _geo(block) -> int:

@@ -148,9 +148,34 @@ def test_binding_errors_are_reference_types(speckern):
         binding.helmholtz_apply_coll(blk, -1.0, T)
     with pytest.raises(FieldStateError):
         binding.mass_apply(blk, T, out=blk.like(FieldState.PHYS))
-    over = make_field(Shape.HEX, 2, GeometryClass.REGULAR, 3, seed=0, qpoints=(5, 5, 5)).blocks[0]
+    quad = make_field(Shape.QUAD, 2, GeometryClass.REGULAR, 3, seed=0).blocks[0]  # 2D: not on the device path
     with pytest.raises(UnsupportedStrategyError):
-        binding.mass_apply(over, T)
+        binding.mass_apply(quad, T)
+
+
+@pytest.mark.parametrize("gcls", ["REGULAR", "DEFORMED"])
+def test_quadrature_override_blocks_through_binding(speckern, gcls):
+    """speckern blocks built with a qpoints override (shapes.py:521-541) run
+    through the binding on the library's run-time-size path and equal
+    speckern's SUM_FAC output."""
+    import speckern_sk200 as binding
+    from speckern import operators as ref
+    from speckern.field_block import FieldState, make_field
+    from speckern.geometry import GeometryClass
+    from speckern.operators import Strategy
+    from speckern.shapes import Shape
+
+    S, T = Strategy.SUM_FAC, Strategy.SUM_FAC_TOP
+    for shp, P, q in ((Shape.TET, 3, (6, 5, 6)), (Shape.HEX, 2, (5, 4, 6))):
+        blk = make_field(shp, P, GeometryClass[gcls], 11, interleave_width=4, seed=4, qpoints=q).blocks[0]
+        rng = np.random.default_rng(2)
+        blk.set_elements(rng.uniform(-1, 1, (blk.n_data, blk.n_elements)))
+        assert _err(binding.helmholtz_apply_coll(blk, 1.2, T).get_elements(),
+                    ref.helmholtz_apply_coll(blk, 1.2, S).get_elements()) <= TOL
+        assert _err(binding.mass_apply(blk, T).get_elements(), ref.mass_apply(blk, S).get_elements()) <= TOL
+        pb = blk.like(FieldState.PHYS)
+        pb.set_elements(rng.uniform(-1, 1, (pb.n_data, pb.n_elements)))
+        assert _err(binding.phys_deriv(pb).get_elements(), ref.phys_deriv(pb).get_elements()) <= TOL
 
 
 def _launches():
