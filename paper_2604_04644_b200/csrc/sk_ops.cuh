@@ -306,6 +306,46 @@ struct k_helm {
     const long long eg = c.e0 + e;
     const bool live = eg < c.E;
     const int row = ps * S2;  // (i,j) row, ps = i*Q1 + j
+    if constexpr (m2_lowreg(S, P) && LAMW && GEO == GEO_DEFORMED && RING == 0) {
+      // low-register form (bit-identical): u lives only through D2, lam W u
+      // goes straight to the U plane (u_k re-read from it), and the D2^T
+      // accumulator is loaded after the metric loop -- two Q2-long register
+      // lines at any time instead of three plus the geometry chunk
+      double w2[Q2];
+      {
+        double u[Q2];
+#pragma unroll
+        for (int k = 0; k < Q2; ++k) u[k] = sm[L::at(e, UO + row + k)];
+        line_dd<S, P, 2>(A.D, u, w2);
+      }
+      const double* g = A.pay + pay_base<PW>(live ? eg : 0, 7, NQ) + (long long)ps * PW;
+      constexpr int CH = Q2 <= 6 ? Q2 : kGeoChunk;
+#pragma unroll
+      for (int k = 0; k < Q2; ++k) {
+        if (k > 0 && k % CH == 0) asm volatile("" ::: "memory");
+        const double* gk = g + (long long)k * (Q0 * Q1) * PW;
+        const double l00 = live ? __ldcs(gk + 0LL * NQ * PW) : 0.0, l01 = live ? __ldcs(gk + 1LL * NQ * PW) : 0.0,
+                     l02 = live ? __ldcs(gk + 2LL * NQ * PW) : 0.0, l11 = live ? __ldcs(gk + 3LL * NQ * PW) : 0.0,
+                     l12 = live ? __ldcs(gk + 4LL * NQ * PW) : 0.0, l22 = live ? __ldcs(gk + 5LL * NQ * PW) : 0.0;
+        const double v0 = sm[L::at(e, V0O + row + k)], v1 = sm[L::at(e, V1O + row + k)], v2 = w2[k];
+        const double a0 = fma(l02, v2, fma(l01, v1, l00 * v0));
+        const double a1 = fma(l12, v2, fma(l11, v1, l01 * v0));
+        w2[k] = fma(l22, v2, fma(l12, v1, l02 * v0));
+        sm[L::at(e, V0O + row + k)] = a0;
+        sm[L::at(e, V1O + row + k)] = a1;
+        if constexpr (LAMW) {
+          const double wj = live ? __ldcs(gk + 6LL * NQ * PW) : 0.0;
+          sm[L::at(e, UO + row + k)] = (A.lam * wj) * sm[L::at(e, UO + row + k)];
+        }
+      }
+      double z[Q2];
+#pragma unroll
+      for (int k = 0; k < Q2; ++k) z[k] = LAMW ? sm[L::at(e, UO + row + k)] : 0.0;
+      line_ddt_acc<S, P, 2>(A.D, w2, z);
+#pragma unroll
+      for (int k = 0; k < Q2; ++k) sm[L::at(e, UO + row + k)] = z[k];
+      return;
+    }
     double u[Q2], w2[Q2], z[Q2];
 #pragma unroll
     for (int k = 0; k < Q2; ++k) u[k] = sm[L::at(e, UO + row + k)];

@@ -118,6 +118,28 @@ SK_HD constexpr int geo_prefetch(int, int) { return SK_GEO_PF; }
 SK_HD constexpr int geo_prefetch(int S, int P) { return kGeoPF[S][P]; }
 #endif
 
+// Deformed Helmholtz (lam != 0) metric sweep in the low-register form
+// (sk_ops.cuh M2, bit-identical arithmetic: lam W u staged through the U
+// plane instead of keeping u live, the D2^T accumulator loaded after the
+// metric loop).  Measured on B200, two A/B runs against the default form,
+// 1 GB deformed (profiles/r02/m2_lowreg_ab*.jsonl, drift control <= 1.2 %):
+// hex P=10 +27 / +26 %, pyr P=10 +8 / +9 %, prism P=10 +7 / +7 %, prism
+// P=7 +3 / +3 %; other orders within noise or losing (tet -2 .. -11 % in
+// the first run), and stiffness (lam = 0, no u term) gains nowhere, so the
+// form is used for lam != 0 only.  Build-time override for A/B:
+// -DSK_M2_LOWREG=0/1 (every Helmholtz instantiation).
+constexpr bool kM2LowRegT[4][11] = {
+    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1},  // hex
+    {0, 0, 0, 0, 0, 0, 0, 1, 0, 0, 1},  // prism
+    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1},  // pyr
+    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},  // tet
+};
+#ifdef SK_M2_LOWREG
+SK_HD constexpr bool m2_lowreg(int, int) { return SK_M2_LOWREG; }
+#else
+SK_HD constexpr bool m2_lowreg(int S, int P) { return kM2LowRegT[S][P]; }
+#endif
+
 // points per geometry-load chunk in the Helmholtz metric sweep (lines longer
 // than 6 points): 7*CH doubles in flight per thread
 #ifdef SK_GEO_CH

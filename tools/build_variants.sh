@@ -40,6 +40,7 @@ for v in "$@"; do
       ring) extra="$extra -DSK_GEO_RING=$n" ;;
       dminb) extra="$extra -DSK_DENSE_MINB=$n" ;;
       dpf) extra="$extra -DSK_DENSE_PF=$n" ;;
+      lowreg) extra="$extra -DSK_M2_LOWREG=$n" ;;
     esac
   done
   make -j"$(nproc)" BUILD=/tmp/sk200_build_$v LIB=$ROOT/paper_2604_04644_b200/libsk200_$v.so LINEINFO= EXTRA="$extra" > /tmp/sk200_build_$v.log 2>&1 \
