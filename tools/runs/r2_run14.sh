@@ -1,4 +1,2 @@
-# M2 low-register metric sweep A/B (deformed Helmholtz, P=4-10, all shapes)
-timeout 1500 python tools/tune_eb.py --variants op0,op0_lowreg1,op0_lowreg0 --ops helm --orders 4-10 --gbytes 1.0 > gpurun_out/r2run14_lowreg.jsonl 2> gpurun_out/r2run14_lowreg.err; echo "tune rc=$?"
-tail -3 gpurun_out/r2run14_lowreg.err
+SK_MASS_DENSE=0 timeout 1500 python tools/tune_eb.py --variants op1,op1_eb16,op1_eb8,op1_eb4,op1_eb2,op1_nt2,op1_eb8_nt2,op1_eb4_nt2 --ops mass --shapes prism,pyr --orders 2-8 --gbytes 1.0 --reps 10 > gpurun_out/r2run14_mass_tune.jsonl 2>&1
 echo done

@@ -1,6 +1,7 @@
-# confirm the per-order M2 low-register table (op0) against all-off; parity on the new default
-timeout 900 python -m pytest tests/test_parity_gpu.py tests/test_integration_speckern_gpu.py -m gpu -q -x > gpurun_out/r2run15_pytest.log 2>&1; echo "pytest rc=$?"
-tail -2 gpurun_out/r2run15_pytest.log
-timeout 1200 python tools/tune_eb.py --variants op0,op0_lowreg0 --ops helm,stiff --orders 4-10 --gbytes 1.0 > gpurun_out/r2run15_lowreg.jsonl 2> gpurun_out/r2run15_lowreg.err; echo "tune rc=$?"
-tail -3 gpurun_out/r2run15_lowreg.err
+timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/r2run15_pytest.log 2>&1; echo "pytest rc=$?"
+tail -2 gpurun_out/r2run15_pytest.log; grep -E "FAILED" gpurun_out/r2run15_pytest.log | head
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r2run15_smoke.log 2>&1; echo "smoke rc=$?"
+timeout 900 python bench.py --impl reference --steps 20 --warmup 5 > gpurun_out/r2run15_ref.json 2> gpurun_out/r2run15_ref.err; echo "ref rc=$?"
+timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/r2run15_bench.json 2> gpurun_out/r2run15_bench.err; echo "bench rc=$?"
+cut -c 1-1500 gpurun_out/r2run15_bench.json
 echo done
