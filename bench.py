@@ -438,6 +438,9 @@ def _cells(quick: bool, only=None):
     for s in SHAPES:
         for P in orders:
             out.append(("helm_regular", "helm", False, s, P))
+    for s in SHAPES:
+        for P in orders:
+            out.append(("helm_recompute", "helmp", True, s, P))
     for tab, op in (("mass_deformed", "mass"), ("stiff_deformed", "stiff")):
         for s in ("prism", "pyr"):
             for P in (orders if quick else range(2, 9)):
@@ -462,7 +465,7 @@ def run_sweep(args, ws, rank, dist, clk, quick=False):
     peaks, _ = _peaks()
     hbm, fp64 = peaks.get("hbm_gbs", 6650.0), _fp64_peak()
     kinds = {"helm": (sk.OperatorKind.HELMHOLTZ_COLL, 1.0), "stiff": (sk.OperatorKind.HELMHOLTZ_COLL, 0.0),
-             "mass": (sk.OperatorKind.MASS, 1.0)}
+             "mass": (sk.OperatorKind.MASS, 1.0), "helmp": (sk.OperatorKind.HELMHOLTZ_COLL, 1.0)}
     params = synthetic_deformation_params(POOL, SEED)
     verts = {}
     rng = np.random.default_rng(1234 + rank)
@@ -495,6 +498,8 @@ def run_sweep(args, ws, rank, dist, clk, quick=False):
         out = blk.like(sk.FieldState.COEFF)
         if op == "mass":
             fn = lambda: sk.mass_apply(blk, out=out)  # noqa: E731
+        elif op == "helmp":  # metric recomputed per chunk from the 12 parameters per element
+            fn = lambda: sk.helmholtz_apply_params(blk, lam, out=out, check=False)  # noqa: E731
         else:
             fn = lambda: sk.helmholtz_apply(blk, lam, out=out)  # noqa: E731
         fn()
@@ -549,6 +554,8 @@ def run_sweep(args, ws, rank, dist, clk, quick=False):
         shp = sk.Shape(s)
         nm = sk.mode_count(shp, P)
         bel = sk.operator_bytes(kind, shp, P, deformed, lam)
+        if tab == "helm_recompute":
+            bel = 8 * (2 * nm + 12)  # modes in/out + 12 deformation parameters
         fl = sk.operator_flops(kind, shp, P)
         gdof = ws * nm * E / (ms / 1e3) / 1e9
         roof_hbm = ws * hbm * 1e9 / bel * nm / 1e9
@@ -562,7 +569,15 @@ def run_sweep(args, ws, rank, dist, clk, quick=False):
         meta["bound"].add("hbm" if roof_hbm <= roof_fp else "fp64")
         meta["throttle"].update(ck["reasons"] if ck else [])
         meta["max_parity"] = max(meta["max_parity"], err or 0.0)
+    # hex / tet DOF/s per order, streamed and recomputed metric
+    for tab in ("helm_deformed", "helm_recompute"):
+        t = tables.get(tab, {})
+        if "hex" in t and "tet" in t:
+            tet = {r[0]: r[1] for r in t["tet"]}
+            info[tab]["hex_over_tet"] = {str(r[0]): round(r[1] / tet[r[0]], 2) for r in t["hex"] if r[0] in tet}
     for tab, meta in info.items():
+        if "hex_over_tet" in meta:
+            tables[tab]["hex_over_tet"] = meta["hex_over_tet"]
         tables[tab]["bound"] = sorted(meta["bound"])
         tables[tab]["throttle"] = sorted(meta["throttle"])
         tables[tab]["max_parity"] = float(f"{meta['max_parity']:.1e}")
@@ -820,7 +835,8 @@ def run_device(args, ws, rank, local):
             line["per_shape_P"] = {
                 "columns": ["P", "gdof_s", "roofline_frac", "parity_maxrel", "sm_mhz"],
                 "roofline": f"min(HBM {hbm:.0f} GB/s x N_P / bytes_el, FP64 {fp64:.1f} TF x N_P / flops_el), "
-                            "bytes_el = 8(2N_P + 7N_Q) (6N_Q stiffness, N_Q mass; 7 / 6 / 1 regular), "
+                            "bytes_el = 8(2N_P + 7N_Q) (6N_Q stiffness, N_Q mass; 7 / 6 / 1 regular; "
+                            "helm_recompute 8(2N_P + 12): metric rebuilt per chunk from 12 parameters), "
                             "flops_el = reference operator_flops",
                 "parity": "6 sampled elements per cell vs CPU oracle, max-normalised (speckern bench.py:192-194)",
                 "cells": f"deformed: max({POOL}, {args.sweep_gb:.1f} GB / bytes_el) elements per apply; regular: "

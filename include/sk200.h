@@ -137,6 +137,22 @@ int sk_helmholtz_apply_staged(const sk_basis* b, int geo_class, int64_t E, int W
                               const double* hpay, double lam, double* out, double* work, int64_t chunk,
                               void* stream);
 
+/* Collocated Helmholtz on deformed elements with the metric recomputed on the
+ * device instead of streamed (SURVEY H3 option (c)): per element chunk, the
+ * geometry kernel builds the chunk's HELMHOLTZ payload from the 12
+ * deformation parameters per element (as sk_payload_from_params,
+ * geometry.py:275-300 -> 161-212) into `work`, then the fused Helmholtz kernel
+ * consumes it while it is L2-resident.  HBM traffic per element 8(2 NP + 12)
+ * bytes instead of 8(2 NP + 7 NQ); results identical to
+ * sk_payload_from_params + sk_helmholtz_apply(SK_FORM_COLL).  work: device
+ * buffer of the payload size of `chunk` elements (sk_payload_size);
+ * chunk: positive multiple of lcm(16, W).  n_bad (optional; NULL skips the
+ * check and its stream synchronisation) receives the number of points with
+ * det J <= 0 (geometry.py:203-209). */
+int sk_helmholtz_apply_params(const sk_basis* b, int64_t E, int W, int ncomp, const double* uhat,
+                              const double* params, double lam, double* out, double* work, int64_t chunk,
+                              int64_t* n_bad, void* stream);
+
 /* ---- host-buffer applies with transfer/compute overlap ----------------------
  * The reference's callers hold their blocks in host memory (field_block.py:
  * 67-149 MemoryRegion HOST space).  sk_apply_streamed runs a coefficient ->

@@ -47,6 +47,7 @@ SIGNATURES = {
     "sk_mass_apply": (_I, [_P, _I, _L, _I, _I, _P, _P, _P, _P]),
     "sk_helmholtz_apply": (_I, [_P, _I, _I, _L, _I, _I, _P, _P, _D, _P, _P]),
     "sk_helmholtz_apply_staged": (_I, [_P, _I, _L, _I, _I, _P, _P, _D, _P, _P, _L, _P]),
+    "sk_helmholtz_apply_params": (_I, [_P, _L, _I, _I, _P, _P, _D, _P, _P, _L, _P, _P]),
     "sk_apply_streamed": (_I, [_P, _I, _I, _L, _I, _I, _P, _P, _P, _D, _P, _P, _L, _P]),
     "sk_c0_gather": (_I, [_I, _I, _I, _L, _P, _I, _P, _P]),
     "sk_c0_scatter": (_I, [_I, _I, _I, _L, _P, _I, _P, _P]),

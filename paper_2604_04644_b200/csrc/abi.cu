@@ -622,6 +622,57 @@ int sk_helmholtz_apply_staged(const sk_basis* b, int geo, int64_t E, int W, int 
   return SK_OK;
 }
 
+int sk_helmholtz_apply_params(const sk_basis* b, int64_t E, int W, int ncomp, const double* uhat,
+                              const double* params, double lam, double* out, double* work, int64_t chunk,
+                              int64_t* n_bad, void* stream) {
+  if (!b || (E > 0 && (!uhat || !params || !out || !work))) return fail(SK_ERR_ARG, "null argument");
+  if (b->generic) return fail(SK_ERR_UNSUPPORTED, "the recomputed-metric variant needs the default quadrature");
+  if (!(lam >= 0.0)) return fail(SK_ERR_ARG, "reaction coefficient must be nonnegative");
+  if (int st = check_layout(E, W, ncomp)) return st;
+  long long unit = 16;
+  while (unit % W) unit += 16;
+  if (chunk < unit || chunk % unit) return fail(SK_ERR_ARG, "chunk must be a positive multiple of lcm(16, W)");
+  if (n_bad) *n_bad = 0;
+  const long long Epad = padded(E, W);
+  if (Epad == 0) return SK_OK;
+  int st = SK_OK;
+  sk_basis* bb = const_cast<sk_basis*>(b);
+  const double* g = device_gtab(bb, &st);
+  if (st) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  unsigned long long* d_bad = nullptr;
+  cudaError_t ce = cudaMallocAsync(&d_bad, sizeof(unsigned long long), s);
+  if (ce == cudaSuccess) ce = cudaMemsetAsync(d_bad, 0, sizeof(unsigned long long), s);
+  if (ce != cudaSuccess) return cuda_status(ce, "geometry scratch");
+  const long long nm = b->hb.nm;
+  int r = 0;
+  for (long long e0 = 0; e0 < Epad && r == 0; e0 += chunk) {
+    const long long e1 = std::min<long long>(Epad, e0 + chunk);
+    const long long ne = std::max<long long>(0, std::min<long long>(E, e1) - e0);
+    // metric payload of this chunk from its 12 deformation parameters per
+    // element: into the L2-resident work buffer (chunks start on a payload
+    // lane group, so the chunk's payload is the work buffer's prefix)
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    r = b->ops->geometry(1, ne, params + e0 * 12, nullptr, nullptr, SK_PAYLOAD_HELMHOLTZ, work, d_bad, g, stream);
+    if (r) {
+      r = cuda_status(r, "geometry kernel");
+      break;
+    }
+    for (int c = 0; c < ncomp && r == 0; ++c)
+      r = run(bb, sk::OP_HELM, SK_GEO_DEFORMED, ne, W, 1, uhat + c * Epad * nm + e0 * nm, out + c * Epad * nm + e0 * nm,
+              work, lam, nm, nm, stream, nullptr);
+  }
+  unsigned long long h_bad = 0;
+  if (r == 0 && n_bad) {
+    ce = cudaMemcpyAsync(&h_bad, d_bad, sizeof(h_bad), cudaMemcpyDeviceToHost, s);
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(s);
+    if (ce != cudaSuccess) r = cuda_status(ce, "geometry check");
+    *n_bad = (int64_t)h_bad;
+  }
+  cudaFreeAsync(d_bad, s);
+  return r;
+}
+
 namespace {
 long long gcd_ll(long long a, long long b) { return b ? gcd_ll(b, a % b) : a; }
 

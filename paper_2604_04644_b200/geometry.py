@@ -143,6 +143,15 @@ class GeometricFactors:
         j = self._jac
         return j if isinstance(j, np.ndarray) else j.cpu().numpy()
 
+    def device_params(self, device):
+        """Deformation parameters (E x 12, as doubles) on ``device``, cached:
+        the input of the recomputed-metric Helmholtz variant."""
+        torch = _torch()
+        key = ("params", str(device))
+        if key not in self._payloads:
+            self._payloads[key] = torch.as_tensor(self.params, dtype=torch.float64, device=device).contiguous()
+        return self._payloads[key]
+
     def payload(self, basis: ShapeBasis, kind: int):
         """Device payload for operator family ``kind`` (built once, cached):
         replaces Block.payload (field_block.py:309-363)."""

@@ -35,6 +35,7 @@ __all__ = [
     "helmholtz_apply_coll",
     "helmholtz_apply",
     "helmholtz_apply_staged",
+    "helmholtz_apply_params",
     "stiffness_apply",
     "apply_operator",
     "apply_to_field",
@@ -291,6 +292,59 @@ def helmholtz_apply_staged(block: Block, lam: float, out: Block | None = None, c
         ),
         "sk_helmholtz_apply_staged",
     )
+    return out
+
+
+#: L2 budget of the recomputed-metric variant's per-chunk payload (bytes)
+PARAMS_WORK_BYTES = 48 << 20
+
+
+def helmholtz_apply_params(block: Block, lam: float, out: Block | None = None, chunk_elements: int = 0,
+                           check: bool = True) -> Block:
+    """Collocated Helmholtz (Alg. 6) with the metric recomputed on the device
+    per element chunk from the block's deformation parameters
+    (sk_helmholtz_apply_params; SURVEY H3 option (c)): HBM traffic 8(2 NP +
+    12) bytes per element instead of 8(2 NP + 7 NQ).  Same result as
+    ``helmholtz_apply_coll`` on the same factors.  Needs a deformed block
+    whose factors are held as parameters (``make_synthetic_factors``);
+    ``check`` counts degenerate points (one stream synchronisation)."""
+    import torch
+
+    from paper_2604_04644_b200.geometry import DegenerateElementError
+
+    _require_state(block, FieldState.COEFF, "helmholtz_apply_params")
+    if lam < 0.0:
+        raise ValueError(f"reaction coefficient must be nonnegative, got {lam}")
+    f = block.factors
+    if not f.deformed or f.params is None:
+        raise UnsupportedStrategyError("helmholtz_apply_params needs deformed factors held as deformation parameters")
+    out = _out_block(block, out, FieldState.COEFF, block.n_components)
+    W = block.interleave_width
+    unit = 16
+    while unit % W:
+        unit += 16
+    lib = _lib.load()
+    per = ctypes.c_int64()
+    _lib.check(lib.sk_payload_size(block.basis.handle, _lib.SK_GEO_DEFORMED, _lib.SK_PAYLOAD_HELMHOLTZ, unit,
+                                   ctypes.byref(per)), "sk_payload_size")
+    per_el = per.value // unit
+    chunk = chunk_elements or max(unit, PARAMS_WORK_BYTES // (8 * per_el) // unit * unit)
+    chunk = min(chunk, -(-block.padded_elements // unit) * unit)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    work = torch.empty(chunk * per_el, dtype=torch.float64, device=dev)
+    prm = f.device_params(dev)
+    xin = block.device(AccessQualifier.READ_ONLY)
+    xout = out.device(AccessQualifier.WRITE_ONLY)
+    bad = ctypes.c_int64()
+    _lib.check(
+        lib.sk_helmholtz_apply_params(
+            block.basis.handle, block.n_elements, W, block.n_components, _p(xin), _p(prm), float(lam), _p(xout),
+            _p(work), chunk, ctypes.byref(bad) if check else None, _stream(),
+        ),
+        "sk_helmholtz_apply_params",
+    )
+    if bad.value:
+        raise DegenerateElementError(f"{bad.value} quadrature points with nonpositive Jacobian")
     return out
 
 

@@ -465,3 +465,39 @@ def test_quadrature_override_validation(sk):
     with pytest.raises(ValueError):
         sk.build_shape_basis(sk.Shape.TET, 3, (5, 3, 4))  # below the default (5, 4, 4)
     assert not sk.build_shape_basis(sk.Shape.TET, 3, (5, 4, 4)).generic  # the default itself
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+@pytest.mark.parametrize("P", [1, 3, 6, 10])
+def test_recomputed_metric_helmholtz(sk, shape, P):
+    """Helmholtz with the metric recomputed per chunk from the deformation
+    parameters (sk_helmholtz_apply_params) against the oracle on the same
+    seeded deformed geometry, and bitwise against the streamed-payload
+    kernel: several chunks, a ragged last chunk, two components, interleave
+    width 8, lam 0 and > 0."""
+    n = 203
+    el = O.element(shape, P)
+    blk = _block(sk, shape, P, True, n, 11, 8, ncomp=2)
+    geo = O.synthetic_geometry(el, True, n, seed=11)
+    x = np.random.default_rng(P).uniform(-1, 1, (2, el.nm, n))
+    blk.set_elements(x)
+    for lam in (0.0, 1.3):
+        got = sk.helmholtz_apply_params(blk, lam, chunk_elements=48).get_elements()
+        streamed = sk.helmholtz_apply(blk, lam).get_elements()
+        assert np.array_equal(got, streamed), lam
+        for c in range(2):
+            assert _err(got[c], O.helmholtz_coll(el, geo, x[c], lam)) <= TOL, (lam, c)
+    blk_default_chunk = sk.helmholtz_apply_params(blk, 0.5).get_elements()
+    assert np.array_equal(blk_default_chunk, sk.helmholtz_apply(blk, 0.5).get_elements())
+
+
+def test_recomputed_metric_errors(sk):
+    b = sk.build_shape_basis(sk.Shape.TET, 3)
+    reg = sk.Block(b, sk.make_synthetic_factors(b, sk.GeometryClass.REGULAR, 10, seed=0), sk.FieldState.COEFF, 1, 1)
+    with pytest.raises(sk.UnsupportedStrategyError):
+        sk.helmholtz_apply_params(reg, 1.0)
+    blk = _block(sk, "tet", 3, True, 40, 0, 1)
+    with pytest.raises(ValueError):
+        sk.helmholtz_apply_params(blk, -1.0)
+    with pytest.raises(ValueError):
+        sk.helmholtz_apply_params(blk, 1.0, chunk_elements=24)  # not a multiple of 16
