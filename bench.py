@@ -449,6 +449,37 @@ def _cells(quick: bool, only=None):
     return out
 
 
+def _copy_ceiling(h2d: int, d2h: int, ndof: int) -> dict:
+    """PCIe ceiling of the e2e number on this box: the step's H2D and D2H
+    bytes copied between pinned host memory and the device on two streams
+    concurrently (no kernel), best of 3; GDOF/s if transfers were all."""
+    import torch
+
+    hin = torch.empty(h2d // 8, dtype=torch.float64, pin_memory=True)
+    hout = torch.empty(d2h // 8, dtype=torch.float64, pin_memory=True)
+    din = torch.empty(h2d // 8, dtype=torch.float64, device="cuda")
+    dout = torch.empty(d2h // 8, dtype=torch.float64, device="cuda")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    best = {}
+    for mode in ("h2d", "d2h", "both"):
+        ts = []
+        for _ in range(3):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            if mode in ("h2d", "both"):
+                with torch.cuda.stream(s1):
+                    din.copy_(hin, non_blocking=True)
+            if mode in ("d2h", "both"):
+                with torch.cuda.stream(s2):
+                    hout.copy_(dout, non_blocking=True)
+            torch.cuda.synchronize()
+            ts.append(time.perf_counter() - t0)
+        best[mode] = min(ts)
+    del hin, hout, din, dout
+    return {"h2d_gbs": round(h2d / best["h2d"] / 1e9, 1), "d2h_gbs": round(d2h / best["d2h"] / 1e9, 1),
+            "concurrent_ms": round(best["both"] * 1e3, 3), "gdof_s": ndof / best["both"] / 1e9}
+
+
 def run_sweep(args, ws, rank, dist, clk, quick=False):
     """Every cell: a block of >= 1 GB algorithmic traffic per apply built from
     a tiled pool of seeded elements, timed over >= 0.15 s of back-to-back
@@ -745,6 +776,7 @@ def run_device(args, ws, rank, local):
     if dist:
         dist.all_reduce(we, op=dist.ReduceOp.MAX)
     e2e_val = ndof * e2e_steps / float(we.item()) / 1e9
+    copy_bound = _copy_ceiling(h2d, d2h, ndof)
 
     # roofline of the dominant kernel: algorithmic bytes per launch / its
     # average duration (CUDA events on the launching stream)
@@ -821,7 +853,8 @@ def run_device(args, ws, rank, local):
                 "step_frac": step_bytes / (ms / 1e3 / args.steps) / 1e9 / hbm,
             },
             "cpu_baseline": cpu,
-            "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "copy_bound": {**copy_bound, "frac": e2e_val / copy_bound["gdof_s"]}},
             "gpu_launches": launches,
             "clocks": main_clocks,
             "parity": parity,

@@ -726,11 +726,39 @@ int sk_apply_streamed(const sk_basis* b, int op, int geo, int64_t E, int W, int 
   // chunk is a sub-block
   const long long eb = 16;
   const long long unit = (long long)W / gcd_ll(W, eb) * eb;
-  if (chunk <= 0) chunk = (Epad + 15) / 16;
+  // chunk boundaries.  Default: ~Epad/8 chunks with a geometric ramp at both
+  // ends (1/8, 1/4, 1/2 of a chunk), so the exposed first H2D and last
+  // kernel + D2H are short while the count of chunks -- each costs a fixed
+  // overhead on the copy engines (measured, tools/e2e_chunks.py) -- stays low.
+  // chunk > 0: uniform chunks of that many elements.
+  std::vector<long long> bnd{0};
+  auto round_up = [&](long long n) { return std::max(unit, (n + unit - 1) / unit * unit); };
+  const char* ramp_env = std::getenv("SK_STREAM_RAMP");
+  const bool ramp = chunk <= 0 && !(ramp_env && ramp_env[0] == '0');
+  if (chunk <= 0) chunk = ramp ? (Epad + 7) / 8 : (Epad + 15) / 16;
   if (chunk < 4096) chunk = 4096;
-  chunk = (chunk + unit - 1) / unit * unit;
+  chunk = round_up(chunk);
+  if (ramp && Epad >= 4 * chunk) {
+    const long long head[3] = {round_up(chunk / 8), round_up(chunk / 4), round_up(chunk / 2)};
+    long long rem = Epad;
+    for (long long h : head) {
+      bnd.push_back(bnd.back() + h);
+      rem -= h;
+    }
+    const long long tail = head[0] + head[1] + head[2];
+    while (rem - tail > 0) {
+      const long long c = std::min<long long>(chunk, round_up(rem - tail));
+      bnd.push_back(std::min<long long>(Epad, bnd.back() + c));
+      rem = Epad - bnd.back();
+    }
+    for (int t = 2; t >= 0 && bnd.back() < Epad; --t) bnd.push_back(std::min<long long>(Epad, bnd.back() + head[t]));
+    if (bnd.back() < Epad) bnd.push_back(Epad);
+  } else {
+    for (long long e0 = chunk; e0 < Epad; e0 += chunk) bnd.push_back(e0);
+    bnd.push_back(Epad);
+  }
   const long long nm = b->hb.nm, cs = Epad * nm, per_el = b->ops->payload_doubles(kind, geo);
-  const int nchunk = (int)((Epad + chunk - 1) / chunk);
+  const int nchunk = (int)bnd.size() - 1;
   std::vector<cudaEvent_t> ev(2 * nchunk + 2, nullptr);
   cudaError_t e = cudaSuccess;
   for (auto& x : ev)
@@ -766,7 +794,7 @@ int sk_apply_streamed(const sk_basis* b, int op, int geo, int64_t E, int W, int 
     }
   }
   for (int i = 0; i < nchunk && e == cudaSuccess; ++i) {
-    const long long e0 = (long long)i * chunk, e1 = std::min<long long>(Epad, e0 + chunk);
+    const long long e0 = bnd[i], e1 = bnd[i + 1];
     const size_t bytes = sizeof(double) * (size_t)((e1 - e0) * nm);
     for (int c = 0; c < ncomp && e == cudaSuccess; ++c)
       e = cudaMemcpyAsync(dev_in + c * cs + e0 * nm, host_in + c * cs + e0 * nm, bytes, cudaMemcpyHostToDevice, sh);

@@ -279,13 +279,17 @@ def test_every_element_at_scale_by_independent_routes(sk, shape, P, n):
     assert ((ms - md).abs().amax(dim=1) / ms.abs().amax(dim=1)).max().item() <= 1e-12
 
 
+@pytest.mark.parametrize("ramp", ["1", "0"])
 @pytest.mark.parametrize("shape,P,width,ncomp", [("tet", 4, 1, 1), ("hex", 3, 8, 2), ("prism", 5, 3, 1)])
-def test_streamed_host_apply(sk, shape, P, width, ncomp):
+def test_streamed_host_apply(sk, monkeypatch, shape, P, width, ncomp, ramp):
     """Host-resident input >= STREAM_MIN_BYTES: the chunk-pipelined
     H2D / kernel / D2H path (sk_apply_streamed) matches the device-resident
-    path bit for bit, with ragged chunks, interleave widths and components;
-    both regions count one transfer and hold the result in both spaces."""
+    path bit for bit, with ragged chunks, interleave widths and components,
+    ramped (default) and uniform chunk schedules; both regions count one
+    transfer and hold the result in both spaces."""
     from paper_2604_04644_b200 import operators as ops
+
+    monkeypatch.setenv("SK_STREAM_RAMP", ramp)
 
     b = sk.build_shape_basis(sk.Shape(shape), P)
     n = ops.STREAM_MIN_BYTES // (8 * b.n_modes * ncomp) + 777
