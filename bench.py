@@ -9,8 +9,8 @@ collective in the timed region); time = max over ranks of CUDA-event time.
 
 The same JSON line carries ``per_shape_P`` -- the BASELINE metric itself
 ("Helmholtz apply GDOF/s per shape vs P; % of roofline"): every shape at
-P=2..10 (deformed, plus regular), and mass / stiffness on prism and pyr at
-P=2..8 (configs[2]); each cell >= 1 GB of algorithmic traffic per apply,
+P=2..10 (deformed, plus regular, plus the recomputed-metric variant), and
+mass / stiffness on every shape at P=2..8 (configs[2] names prism and pyr); each cell >= 1 GB of algorithmic traffic per apply,
 with its roofline fraction, a sampled-element parity error against the CPU
 oracle and the SM clocks sampled while it ran.
 
@@ -442,7 +442,7 @@ def _cells(quick: bool, only=None):
         for P in orders:
             out.append(("helm_recompute", "helmp", True, s, P))
     for tab, op in (("mass_deformed", "mass"), ("stiff_deformed", "stiff")):
-        for s in ("prism", "pyr"):
+        for s in SHAPES:
             for P in (orders if quick else range(2, 9)):
                 if P <= 8:
                     out.append((tab, op, True, s, P))

@@ -8,6 +8,7 @@
 #include <array>
 #include <cmath>
 #include <vector>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -290,6 +291,40 @@ static int go(const Args& a, const LaunchReq& r, int gy, void* stream) {
   return (int)cudaGetLastError();
 }
 
+// warp-tile mass (k_mass_warp): one resident wave of CTAs, every warp
+// striding over G-element tiles
+inline bool mass_warp_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("SK_MASS_WARP");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+template <int S, int P, int G, int PW, int GEO>
+int launch_mass_warp(const OpArgs<S, P>& a, const LaunchReq& r, void* stream) {
+  using M = MassWarp<S, P, G, kMassWarpWPC, PW, GEO>;
+  auto kern = k_mass_warp<S, P, G, kMassWarpWPC, PW, GEO>;
+  static std::once_flag once;
+  static int per_sm = 1, sms = 148;
+  std::call_once(once, [&] {
+    ensure_smem(kern, M::SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, M::NT, M::SMEM);
+    if (per_sm < 1) per_sm = 1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  });
+  const long long tiles = (r.Epad + G - 1) / G;
+  if (tiles == 0) return 0;
+  const int gy = r.ncomp > 0 ? r.ncomp : 1;
+  const long long resident = (long long)per_sm * sms / gy;
+  const long long need = (tiles + M::WPC - 1) / M::WPC;
+  const long long grid = need < resident ? need : (resident > 0 ? resident : 1);
+  kern<<<dim3((unsigned)grid, (unsigned)gy), M::NT, M::SMEM, static_cast<cudaStream_t>(stream)>>>(a);
+  return (int)cudaGetLastError();
+}
+
 // StdMat mass on DMMA (sk_dense.cuh): persistent warps over 8-element groups
 template <int S, int P, int PW, int GEO>
 int launch_dense_geo(const DenseArgs& a, int ncomp, void* stream) {
@@ -463,6 +498,12 @@ int launch(int op, const LaunchReq& r, void* stream) {
       if (r.dense) {
         if constexpr (P <= kDenseMaxP) return launch_dense<S, P, C::PW>(r, stream);
         return (int)cudaErrorInvalidValue;
+      }
+      if constexpr (mass_warp_g(S, P) > 0) {
+        if (mass_warp_enabled()) {
+          if (def) return launch_mass_warp<S, P, mass_warp_g(S, P), C::PW, GEO_DEFORMED>(a, r, stream);
+          return launch_mass_warp<S, P, mass_warp_g(S, P), C::PW, GEO_REGULAR>(a, r, stream);
+        }
       }
       if (def) return go<S, P, OP_MASS, k_mass<S, P, typename C::L, C::NT, C::PW, GEO_DEFORMED, C::MINB>>(a, r, r.ncomp, stream);
       return go<S, P, OP_MASS, k_mass<S, P, typename C::L, C::NT, C::PW, GEO_REGULAR, C::MINB>>(a, r, r.ncomp, stream);

@@ -257,10 +257,28 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 #endif
 constexpr int kItemsUnroll = SK_ITEMS_UNROLL;
 
+// Thread index within the tile's thread group and the group barrier: a CTA
+// (NT >= 64), or a single warp owning its own tile (NT == 32, the warp-tile
+// kernels: no CTA barrier at all)
+template <int NT>
+__device__ __forceinline__ int tix() {
+  if constexpr (NT == 32)
+    return threadIdx.x & 31;
+  else
+    return threadIdx.x;
+}
+template <int NT>
+__device__ __forceinline__ void csync() {
+  if constexpr (NT == 32)
+    __syncwarp();
+  else
+    __syncthreads();
+}
+
 template <class L, int NPASS, int NT, class F>
 __device__ __forceinline__ void items(F&& f) {
 #pragma unroll kItemsUnroll
-  for (int w = threadIdx.x; w < L::EB * NPASS; w += NT) {
+  for (int w = tix<NT>(); w < L::EB * NPASS; w += NT) {
     const int ps = w / L::EB;
     f(w - ps * L::EB, ps);
   }

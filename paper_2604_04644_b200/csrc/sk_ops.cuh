@@ -675,20 +675,26 @@ struct k_mass {
   }
   static constexpr bool SMT = smem_tables(1, S, P);
   __device__ static void body(const OpArgs<S, P>& A, long long tile, double* sm, long long tnext) {
+    body_t(A, tile, sm, tnext, sm + L::TABOFF);
+  }
+  // stab: the staged ragged tables (SMT); NT == 32: one warp owns the tile
+  // and every barrier is a warp barrier (k_mass_warp)
+  __device__ static void body_t(const OpArgs<S, P>& A, long long tile, double* sm, long long tnext, const double* stab) {
   using Dm = Dims<S, P>;
   constexpr int P1 = Dm::P1, Q0 = Dm::Q0, Q1 = Dm::Q1, Q2 = Dm::Q2, S2 = L::S2, NM = Dm::NM;
   constexpr int PL = L::PLANE, TAo = 0, TBo = PL;
+  constexpr bool WP = NT > 32 && prism_warp_pairs(1, S, P);
   const Ctx c = make_ctx<L::EB>(tile, A.E, A.Epad, A.W);
   const double* src = A.in + blockIdx.y * A.in_cstride;
   double* dst = A.out + blockIdx.y * A.out_cstride;
   double* xs = sm + L::EB * PL;  // plane 1 (TB): staging before F2 and after B2
-  if constexpr (SMT)  // ragged sweep tables staged in shared memory by run()
-    stage_f1<S, P, L, NT, TAo, CoefIn<L, NM>, false, ragged_dispatch(1, S, P), ragged_split(1, S, P), prism_warp_pairs(1, S, P), true>(A.B, sm + L::TABOFF, CoefIn<L, NM>{xs}, sm);
+  if constexpr (SMT)  // ragged sweep tables staged in shared memory
+    stage_f1<S, P, L, NT, TAo, CoefIn<L, NM>, false, ragged_dispatch(1, S, P), ragged_split(1, S, P), WP, true>(A.B, stab, CoefIn<L, NM>{xs}, sm);
   else
-    stage_f1<S, P, L, NT, TAo, CoefIn<L, NM>, false, ragged_dispatch(1, S, P), ragged_split(1, S, P), prism_warp_pairs(1, S, P)>(A.B, A.gtab, CoefIn<L, NM>{xs}, sm);
-  __syncthreads();
+    stage_f1<S, P, L, NT, TAo, CoefIn<L, NM>, false, ragged_dispatch(1, S, P), ragged_split(1, S, P), WP>(A.B, A.gtab, CoefIn<L, NM>{xs}, sm);
+  csync<NT>();
   stage_f2<S, P, L, NT, TAo, TBo>(A.B, A.gtab, sm);
-  __syncthreads();
+  csync<NT>();
   items<L, Q1 * Q2, NT>([&](int e, int ps) {
     const int j = ps / Q2, k = ps - j * Q2;
     const long long eg = c.e0 + e;
@@ -703,18 +709,58 @@ struct k_mass {
 #pragma unroll
     for (int p = 0; p < P1; ++p) sm[L::at(e, TBo + (p * Q1 + j) * S2 + k)] = x[p];
   });
-  __syncthreads();
+  csync<NT>();
   if (tnext >= 0 && threadIdx.x < 32) prefetch_geo(A, tnext);
   stage_b2<S, P, L, NT, TAo, TBo>(A.B, A.gtab, sm);
-  __syncthreads();
+  csync<NT>();
   if constexpr (SMT)
-    stage_b3<S, P, L, NT, TAo, CoefOut<L, NM>, false, ragged_dispatch(1, S, P), ragged_split(1, S, P), prism_warp_pairs(1, S, P), true>(A.B, sm + L::TABOFF, CoefOut<L, NM>{xs}, sm);
+    stage_b3<S, P, L, NT, TAo, CoefOut<L, NM>, false, ragged_dispatch(1, S, P), ragged_split(1, S, P), WP, true>(A.B, stab, CoefOut<L, NM>{xs}, sm);
   else
-    stage_b3<S, P, L, NT, TAo, CoefOut<L, NM>, false, ragged_dispatch(1, S, P), ragged_split(1, S, P), prism_warp_pairs(1, S, P)>(A.B, A.gtab, CoefOut<L, NM>{xs}, sm);
-  __syncthreads();
+    stage_b3<S, P, L, NT, TAo, CoefOut<L, NM>, false, ragged_dispatch(1, S, P), ragged_split(1, S, P), WP>(A.B, A.gtab, CoefOut<L, NM>{xs}, sm);
+  csync<NT>();
   store_tile<L, NM, NT>(dst, c, xs);
   }
 };
+
+// Mass with one warp per tile of G elements (no CTA barriers): WPC warps
+// per CTA each own a private two-plane tile and stride over the tiles
+// independently, so one warp's global-load latency overlaps the others'
+// sweeps without the CTA-wide barrier stalls of k_mass.
+// The ragged tables (kSmemTab) are staged once per CTA after the tiles.
+template <int S, int P, int G, int WPC_, int PW, int GEO>
+struct MassWarp {
+  using L = Lay<S, P, 2, G>;
+  using K = k_mass<S, P, L, 32, PW, GEO, 1>;
+  // warps per CTA: as asked, or as many as fit 200 KB of tiles
+  static constexpr int WPC = WPC_ * L::SMEM_DOUBLES * 8 <= 200 * 1024 ? WPC_
+                             : (200 * 1024) / (L::SMEM_DOUBLES * 8) > 0 ? (200 * 1024) / (L::SMEM_DOUBLES * 8) : 1;
+  static constexpr int NT = WPC * 32;
+  static constexpr int TABOFF = (WPC * L::SMEM_DOUBLES + 1) / 2 * 2;
+  static constexpr int SMEM = (K::SMT ? TABOFF + GLayout<S, P>::RAGGED : WPC * L::SMEM_DOUBLES) * 8;
+};
+
+template <int S, int P, int G, int WPC_, int PW, int GEO>
+__global__ void __launch_bounds__(MassWarp<S, P, G, WPC_, PW, GEO>::NT, kMassWarpMinB) k_mass_warp(const __grid_constant__ OpArgs<S, P> A) {
+  using M = MassWarp<S, P, G, WPC_, PW, GEO>;
+  constexpr int WPC = M::WPC;
+  using L = typename M::L;
+  using K = typename M::K;
+  extern __shared__ double sm[];
+  if constexpr (K::SMT) {
+    for (int t = threadIdx.x; t < GLayout<S, P>::RAGGED; t += M::NT) sm[M::TABOFF + t] = __ldg(A.gtab + t);
+    __syncthreads();
+  }
+  const int warp = threadIdx.x >> 5;
+  double* ws = sm + warp * L::SMEM_DOUBLES;
+  const long long ntiles = (A.Epad + G - 1) / G;
+  for (long long t = (long long)blockIdx.x * WPC + warp; t < ntiles; t += (long long)gridDim.x * WPC) {
+    const Ctx c = make_ctx<G>(t, A.E, A.Epad, A.W);
+    load_tile<L, Dims<S, P>::NM, 32>(A.in + blockIdx.y * A.in_cstride, c, ws + G * L::PLANE);
+    __syncwarp();
+    K::body_t(A, t, ws, -1, sm + M::TABOFF);
+    __syncwarp();  // the store has read the staging area before the next load
+  }
+}
 
 // ---------------------------------------------------------------------------
 // BwdTrans: coefficients -> quadrature values

@@ -45,6 +45,7 @@ constexpr int kPrismUniformMaxP = 8;
 template <int P, class L, int NT, class F>
 __device__ __forceinline__ void prism_slice_pairs(F&& f) {
   constexpr int P1 = P + 1, NPP = (P1 + 1) / 2, LN = L::EB * P1, WPG = (LN + 31) / 32;
+  static_assert(NT >= 64, "warp-uniform slice pairs need a CTA-wide thread group");
   for (int sl = threadIdx.x; sl < NPP * WPG * 32; sl += NT) {
     const int g = sl / (WPG * 32), l = sl - g * (WPG * 32);
     if (l < LN) {
@@ -97,12 +98,12 @@ __device__ __forceinline__ void load_tile(const double* __restrict__ src, const 
     const double* base = src + c.e0 * N;
     const long long lim = (c.E - c.e0) * N;  // loads past the last element read 0
 #pragma unroll 4
-    for (int g = threadIdx.x; g < EB * N; g += NT) {
+    for (int g = tix<NT>(); g < EB * N; g += NT) {
       const int e = g / N, m = g - e * N;
       xs[m * XS + e] = g < lim ? __ldg(base + g) : 0.0;
     }
   } else {
-    for (int g = threadIdx.x; g < EB * N; g += NT) {
+    for (int g = tix<NT>(); g < EB * N; g += NT) {
       const int m = g / EB, e = g - m * EB;
       const long long eg = c.e0 + e;
       xs[m * XS + e] = eg < c.E ? __ldg(src + lane_base(eg, N, c.W) + (long long)m * c.W) : 0.0;
@@ -117,12 +118,12 @@ __device__ __forceinline__ void store_tile(double* __restrict__ dst, const Ctx& 
     double* base = dst + c.e0 * N;
     const long long lim = (c.Epad - c.e0) * N;
 #pragma unroll 4
-    for (int g = threadIdx.x; g < EB * N; g += NT) {
+    for (int g = tix<NT>(); g < EB * N; g += NT) {
       const int e = g / N, m = g - e * N;
       if (g < lim) base[g] = xs[m * XS + e];
     }
   } else {
-    for (int g = threadIdx.x; g < EB * N; g += NT) {
+    for (int g = tix<NT>(); g < EB * N; g += NT) {
       const int m = g / EB, e = g - m * EB;
       const long long eg = c.e0 + e;
       if (eg < c.Epad) dst[lane_base(eg, N, c.W) + (long long)m * c.W] = xs[m * XS + e];
@@ -144,13 +145,13 @@ struct TileRegs {
       const long long lim = (c.E - c.e0) * N;
 #pragma unroll
       for (int i = 0; i < CPT; ++i) {
-        const int g = threadIdx.x + i * NT;
+        const int g = tix<NT>() + i * NT;
         v[i] = (g < EB * N && g < lim) ? __ldg(base + g) : 0.0;
       }
     } else {
 #pragma unroll
       for (int i = 0; i < CPT; ++i) {
-        const int g = threadIdx.x + i * NT;
+        const int g = tix<NT>() + i * NT;
         const int m = g / EB, e = g - m * EB;
         const long long eg = c.e0 + e;
         v[i] = (g < EB * N && eg < c.E) ? __ldg(src + lane_base(eg, N, c.W) + (long long)m * c.W) : 0.0;
@@ -160,7 +161,7 @@ struct TileRegs {
   __device__ __forceinline__ void put(int W, double* xs) const {
 #pragma unroll
     for (int i = 0; i < CPT; ++i) {
-      const int g = threadIdx.x + i * NT;
+      const int g = tix<NT>() + i * NT;
       if (g < EB * N) {
         int e, m;
         if (W == 1) {

@@ -209,6 +209,33 @@ SK_HD constexpr int geo_ring(int, int) { return SK_GEO_RING; }
 SK_HD constexpr int geo_ring(int S, int P) { return kGeoRing[S][P]; }
 #endif
 
+// Sum-factorised mass with one warp per tile (sk_ops.cuh k_mass_warp, no CTA
+// barriers) instead of the CTA-tile k_mass: elements per warp tile G and
+// warps per CTA, per shape x order (G = 0: CTA tiles).  Build-time
+// overrides for A/B: -DSK_MASS_WARP_G=<G> (every order), -DSK_MASS_WARP_WPC.
+// Run-time override: SK_MASS_WARP=0 (never).
+constexpr int kMassWarpG[4][11] = {
+    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},  // hex
+    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},  // prism
+    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},  // pyr
+    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},  // tet
+};
+#ifdef SK_MASS_WARP_G
+SK_HD constexpr int mass_warp_g(int, int) { return SK_MASS_WARP_G; }
+#else
+SK_HD constexpr int mass_warp_g(int S, int P) { return kMassWarpG[S][P]; }
+#endif
+#ifdef SK_MASS_WARP_WPC
+constexpr int kMassWarpWPC = SK_MASS_WARP_WPC;
+#else
+constexpr int kMassWarpWPC = 8;
+#endif
+#ifdef SK_MASS_WARP_MINB
+constexpr int kMassWarpMinB = SK_MASS_WARP_MINB;
+#else
+constexpr int kMassWarpMinB = 1;
+#endif
+
 // Mass by the StdMat strategy on the FP64 tensor cores (sk_dense.cuh)
 // instead of sum factorisation, per geometry class (0 regular, 1 deformed)
 // x shape x order; instantiated up to kDenseMaxP.  Run-time override:
