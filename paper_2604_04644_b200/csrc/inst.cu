@@ -291,6 +291,41 @@ static int go(const Args& a, const LaunchReq& r, int gy, void* stream) {
   return (int)cudaGetLastError();
 }
 
+// TMA-fed deformed mass (k_mass_tma): one resident wave of persistent CTAs
+inline bool mass_tma_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("SK_MASS_TMA");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+template <int S, int P>
+int launch_mass_tma(const OpArgs<S, P>& a, const LaunchReq& r, void* stream) {
+  using C = Cfg<S, P, OP_MASS>;
+  constexpr int SM0 = MassTma<S, P, typename C::L, C::NT, C::PW, 1>::SMEM;
+  constexpr int MINB = tuned_minb(1, S, P) ? cmax(1, cmin(cmin(tuned_minb_cap(1, S, P), (220 * 1024) / (SM0 + 1024)), 2048 / C::NT)) : 1;
+  using M = MassTma<S, P, typename C::L, C::NT, C::PW, MINB>;
+  auto kern = k_mass_tma<S, P, typename C::L, C::NT, C::PW, MINB>;
+  static std::once_flag once;
+  static int per_sm = 1, sms = 148;
+  std::call_once(once, [&] {
+    ensure_smem(kern, M::SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::NT, M::SMEM);
+    if (per_sm < 1) per_sm = 1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  });
+  const long long tiles = (r.Epad + C::EB - 1) / C::EB;
+  if (tiles == 0) return 0;
+  const int gy = r.ncomp > 0 ? r.ncomp : 1;
+  const long long wave = (long long)per_sm * sms / gy;
+  const long long grid = tiles < wave ? tiles : (wave > 0 ? wave : 1);
+  kern<<<dim3((unsigned)grid, (unsigned)gy), C::NT, M::SMEM, static_cast<cudaStream_t>(stream)>>>(a);
+  return (int)cudaGetLastError();
+}
+
 // warp-tile mass (k_mass_warp): one resident wave of CTAs, every warp
 // striding over G-element tiles
 inline bool mass_warp_enabled() {
@@ -498,6 +533,9 @@ int launch(int op, const LaunchReq& r, void* stream) {
       if (r.dense) {
         if constexpr (P <= kDenseMaxP) return launch_dense<S, P, C::PW>(r, stream);
         return (int)cudaErrorInvalidValue;
+      }
+      if constexpr (mass_tma(S, P) && (C::EB * Dims<S, P>::NM) % 2 == 0 && (Dims<S, P>::NQ * C::PW) % 2 == 0) {
+        if (def && mass_tma_enabled()) return launch_mass_tma<S, P>(a, r, stream);
       }
       if constexpr (mass_warp_g(S, P) > 0) {
         if (mass_warp_enabled()) {

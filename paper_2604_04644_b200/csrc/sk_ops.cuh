@@ -680,6 +680,19 @@ struct k_mass {
   // stab: the staged ragged tables (SMT); NT == 32: one warp owns the tile
   // and every barrier is a warp barrier (k_mass_warp)
   __device__ static void body_t(const OpArgs<S, P>& A, long long tile, double* sm, long long tnext, const double* stab) {
+    body_w(
+        A, tile, sm, stab, [&](long long eg, bool live, int l, int) { return w_at<S, P, PW, GEO>(A, eg, live, l); },
+        [] {},
+        [&] {
+          if (tnext >= 0 && threadIdx.x < 32) prefetch_geo(A, tnext);
+        });
+  }
+  // wf(eg, live, point, tile element): the diagonal W entry; pre(): runs
+  // before the W sweep; hook(): once every thread is past it (next-tile
+  // prefetch / copy issue)
+  template <class WF, class PRE, class HOOK>
+  __device__ static void body_w(const OpArgs<S, P>& A, long long tile, double* sm, const double* stab, const WF& wf,
+                                const PRE& pre, const HOOK& hook) {
   using Dm = Dims<S, P>;
   constexpr int P1 = Dm::P1, Q0 = Dm::Q0, Q1 = Dm::Q1, Q2 = Dm::Q2, S2 = L::S2, NM = Dm::NM;
   constexpr int PL = L::PLANE, TAo = 0, TBo = PL;
@@ -695,6 +708,7 @@ struct k_mass {
   csync<NT>();
   stage_f2<S, P, L, NT, TAo, TBo>(A.B, A.gtab, sm);
   csync<NT>();
+  pre();
   items<L, Q1 * Q2, NT>([&](int e, int ps) {
     const int j = ps / Q2, k = ps - j * Q2;
     const long long eg = c.e0 + e;
@@ -704,13 +718,13 @@ struct k_mass {
     for (int p = 0; p < P1; ++p) x[p] = sm[L::at(e, TBo + (p * Q1 + j) * S2 + k)];
     line_a0_eo<S, P>(A.B, x, u);
 #pragma unroll
-    for (int i = 0; i < Q0; ++i) u[i] *= w_at<S, P, PW, GEO>(A, eg, live, (i * Q1 + j) * Q2 + k);
+    for (int i = 0; i < Q0; ++i) u[i] *= wf(eg, live, (i * Q1 + j) * Q2 + k, e);
     line_a0t_eo<S, P>(A.B, u, x);
 #pragma unroll
     for (int p = 0; p < P1; ++p) sm[L::at(e, TBo + (p * Q1 + j) * S2 + k)] = x[p];
   });
   csync<NT>();
-  if (tnext >= 0 && threadIdx.x < 32) prefetch_geo(A, tnext);
+  hook();
   stage_b2<S, P, L, NT, TAo, TBo>(A.B, A.gtab, sm);
   csync<NT>();
   if constexpr (SMT)
@@ -721,6 +735,101 @@ struct k_mass {
   store_tile<L, NM, NT>(dst, c, xs);
   }
 };
+
+// Mass, deformed, with the tile inputs moved by TMA bulk copies (SASS
+// UBLKCP): a persistent CTA strides over its tiles; thread 0 issues the
+// next tile's coefficient block (W = 1 layout: one contiguous range, double
+// buffered) at the top of the current tile and the next tile's W payload
+// (one contiguous PW-lane group) as soon as the current tile's W sweep is
+// done, each completing on an mbarrier, so the global latency of both lands
+// under the sum-factorisation sweeps instead of stalling the first barrier
+// and the W sweep (ncu: 20 % + 14 % of samples in k_mass at tet P=4).
+// Ragged last tiles and unaligned component offsets take the register path.
+template <int S, int P, class L, int NT_, int PW, int MINB_>
+struct MassTma {
+  using K = k_mass<S, P, L, NT_, PW, GEO_DEFORMED, MINB_>;
+  using Dm = Dims<S, P>;
+  static constexpr int NT = NT_, EB = L::EB, NQ = Dm::NQ, NM = Dm::NM;
+  static_assert(EB == PW, "one tile = one payload lane group");
+  static constexpr int TAB = K::SMT ? GLayout<S, P>::RAGGED : 0;
+  static constexpr int PBUF = (L::TABOFF + TAB + 1) / 2 * 2;         // NQ * PW doubles
+  static constexpr int CBUF = PBUF + NQ * PW;                         // 2 x EB * NM doubles
+  static constexpr int MBAR = (CBUF + 2 * EB * NM + 1) / 2 * 2;       // 3 mbarriers
+  static constexpr int SMEM = MBAR * 8 + 3 * 8;
+};
+
+template <int S, int P, class L, int NT_, int PW, int MINB_>
+__global__ void __launch_bounds__(NT_, MINB_) k_mass_tma(const __grid_constant__ OpArgs<S, P> A) {
+  using M = MassTma<S, P, L, NT_, PW, MINB_>;
+  using K = typename M::K;
+  constexpr int EB = M::EB, NM = M::NM, NQ = M::NQ, NT = NT_;
+  extern __shared__ double sm[];
+  double* pbuf = sm + M::PBUF;
+  double* cbuf = sm + M::CBUF;
+  unsigned long long* mb = reinterpret_cast<unsigned long long*>(sm + M::MBAR);  // [0,1] coefficients, [2] W
+  const long long ntiles = (A.Epad + EB - 1) / EB;
+  const long long stride = gridDim.x;
+  const double* src = A.in + blockIdx.y * A.in_cstride;
+  // a tile's coefficients come by TMA when it is whole and its range is
+  // 16-byte aligned (W = 1: element-major, EB * NM contiguous doubles)
+  auto coef_tma = [&](long long t) {
+    const long long e0 = t * EB;
+    return A.W == 1 && e0 + EB <= A.E && ((reinterpret_cast<unsigned long long>(src + e0 * NM) & 15) == 0);
+  };
+  constexpr unsigned CBYTES = EB * NM * 8, PBYTES = NQ * PW * 8;
+  static_assert(CBYTES % 16 == 0 && PBYTES % 16 == 0, "bulk copies move multiples of 16 bytes");
+  long long t = blockIdx.x;
+  if (threadIdx.x == 0) {
+    mbar_init(&mb[0], 1);
+    mbar_init(&mb[1], 1);
+    mbar_init(&mb[2], 1);
+    mbar_fence_init();
+    if (t < ntiles) {
+      if (coef_tma(t)) {
+        mbar_expect_tx(&mb[0], CBYTES);
+        bulk_g2s(cbuf, src + t * EB * NM, CBYTES, &mb[0]);
+      }
+      mbar_expect_tx(&mb[2], PBYTES);
+      bulk_g2s(pbuf, A.pay + t * EB * NQ, PBYTES, &mb[2]);
+    }
+  }
+  if constexpr (K::SMT) stage_tables<S, P, NT>(A.gtab, sm + L::TABOFF);
+  __syncthreads();
+  double* xs = sm + EB * L::PLANE;  // plane 1: coefficient staging
+  for (int i = 0; t < ntiles; t += stride, ++i) {
+    const int b = i & 1;
+    // next tile's coefficients into the other buffer (last read by tile i-1's
+    // staging copy, before this tile's first barrier... and the one below)
+    if (threadIdx.x == 0 && t + stride < ntiles && coef_tma(t + stride)) {
+      mbar_expect_tx(&mb[b ^ 1], CBYTES);
+      bulk_g2s(cbuf + (b ^ 1) * EB * NM, src + (t + stride) * EB * NM, CBYTES, &mb[b ^ 1]);
+    }
+    const Ctx c = make_ctx<EB>(t, A.E, A.Epad, A.W);
+    if (coef_tma(t)) {
+      mbar_wait(&mb[b], (i >> 1) & 1);
+      const double* cb = cbuf + b * EB * NM;
+      for (int g = threadIdx.x; g < EB * NM; g += NT) {
+        const int e = g / NM, m = g - e * NM;
+        xs[m * L::XSTR + e] = cb[g];
+      }
+    } else {
+      load_tile<L, NM, NT>(src, c, xs);
+    }
+    __syncthreads();
+    K::body_w(
+        A, t, sm, sm + L::TABOFF,
+        [&](long long, bool live, int l, int e) {
+          return live ? pbuf[l * PW + e] : 0.0;
+        },
+        [&] { mbar_wait(&mb[2], i & 1); },
+        [&] {  // every thread is done with pbuf: the next tile's W
+          if (threadIdx.x == 0 && t + stride < ntiles) {
+            mbar_expect_tx(&mb[2], PBYTES);
+            bulk_g2s(pbuf, A.pay + (t + stride) * EB * NQ, PBYTES, &mb[2]);
+          }
+        });
+  }
+}
 
 // Mass with one warp per tile of G elements (no CTA barriers): WPC warps
 // per CTA each own a private two-plane tile and stride over the tiles

@@ -209,6 +209,30 @@ SK_HD constexpr int geo_ring(int, int) { return SK_GEO_RING; }
 SK_HD constexpr int geo_ring(int S, int P) { return kGeoRing[S][P]; }
 #endif
 
+// Deformed sum-factorised mass with TMA-moved tile inputs (sk_ops.cuh
+// k_mass_tma) instead of k_mass, per shape x order.  Measured on B200, two
+// A/B runs (profiles/r02/mass_tma_ab.jsonl, mass_tma_grid.jsonl; roofline
+// fraction k_mass -> k_mass_tma): pyr P=3 0.45 -> 0.61, P=4 0.51 -> 0.54,
+// P=5 0.44 -> 0.48, P=6 0.46 -> 0.49; prism P=2 0.59 -> 0.66, P=3 0.59 ->
+// 0.72; tet P=4 0.43 -> 0.50, P=5 0.40 -> 0.43; hex P=6 0.69 -> 0.74.  It
+// loses at tet P=3, prism P>=4, hex P=3..5 and P>=7 (one resident wave with
+// the larger footprint), and the DMMA StdMat kernel stays ahead at P=1 and
+// pyr / tet P=2; tile widths 4 / 8 and halved thread counts were no better.
+// Build-time override for A/B: -DSK_MASS_TMA=0/1 (every order); run-time:
+// SK_MASS_TMA=0.
+constexpr bool kMassTma[4][11] = {
+    // P: 0  1  2  3  4  5  6  7  8  9 10
+    {0, 0, 0, 0, 0, 0, 1, 0, 0, 0, 0},  // hex
+    {0, 0, 1, 1, 0, 0, 0, 0, 0, 0, 0},  // prism
+    {0, 0, 0, 1, 1, 1, 1, 0, 0, 0, 0},  // pyr
+    {0, 0, 0, 0, 1, 1, 0, 0, 0, 0, 0},  // tet
+};
+#ifdef SK_MASS_TMA
+SK_HD constexpr bool mass_tma(int, int) { return SK_MASS_TMA; }
+#else
+SK_HD constexpr bool mass_tma(int S, int P) { return kMassTma[S][P]; }
+#endif
+
 // Sum-factorised mass with one warp per tile (sk_ops.cuh k_mass_warp, no CTA
 // barriers) instead of the CTA-tile k_mass: elements per warp tile G and
 // warps per CTA, per shape x order (G = 0: CTA tiles).  Build-time

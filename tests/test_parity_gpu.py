@@ -505,3 +505,22 @@ def test_recomputed_metric_errors(sk):
         sk.helmholtz_apply_params(blk, -1.0)
     with pytest.raises(ValueError):
         sk.helmholtz_apply_params(blk, 1.0, chunk_elements=24)  # not a multiple of 16
+
+
+@pytest.mark.parametrize("shape,P,n", [("tet", 4, 50021), ("pyr", 3, 40003), ("prism", 5, 30011), ("hex", 3, 30001)])
+def test_mass_at_scale(sk, shape, P, n):
+    """Deformed mass over several waves of persistent CTAs (every CTA
+    strides over many tiles: the TMA-fed kernel's double-buffered
+    coefficient blocks and per-tile W copies, kMassTma), two components
+    (the second one's offset is not 16-byte aligned for odd n * n_modes:
+    register path for it), interleave width 1, ragged last tile; compared
+    with the oracle on every element."""
+    el = O.element(shape, P)
+    geo = O.synthetic_geometry(el, True, n, seed=21)
+    blk = _block_from(sk, shape, P, geo, 1, ncomp=2)
+    x = np.random.default_rng(7).uniform(-1, 1, (2, el.nm, n))
+    blk.set_elements(x)
+    blk.device()
+    got = sk.mass_apply(blk).get_elements()
+    for c in range(2):
+        assert _err(got[c], O.mass(el, geo, x[c])) <= TOL, c
