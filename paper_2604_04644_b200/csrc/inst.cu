@@ -360,6 +360,38 @@ int launch_mass_warp(const OpArgs<S, P>& a, const LaunchReq& r, void* stream) {
   return (int)cudaGetLastError();
 }
 
+// persistent TMA-staged driver (k_persist_tma): one resident wave
+inline bool helm_tma_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("SK_HELM_TMA");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+template <int S, int P, int OP, class Op, class C = Cfg<S, P, OP>, class Args>
+static int go_tma(const Args& a, const LaunchReq& r, int gy, void* stream) {
+  using T = PersistTma<Op, Args, Dims<S, P>::NM, C::SMEM>;
+  auto kern = k_persist_tma<Op, Args, Dims<S, P>::NM, C::SMEM>;
+  static std::once_flag once;
+  static int per_sm = 1, sms = 148;
+  std::call_once(once, [&] {
+    ensure_smem(kern, T::SMEM);
+    int dev = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Op::NT, T::SMEM);
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (per_sm < 1) per_sm = 1;
+  });
+  const long long tiles = (r.Epad + C::EB - 1) / C::EB;
+  if (tiles == 0) return 0;
+  const int g = gy > 0 ? gy : 1;
+  const long long wave = (long long)per_sm * sms / g;
+  const long long grid = tiles < wave ? tiles : (wave > 0 ? wave : 1);
+  kern<<<dim3((unsigned)grid, (unsigned)g), Op::NT, T::SMEM, static_cast<cudaStream_t>(stream)>>>(a);
+  return (int)cudaGetLastError();
+}
+
 // StdMat mass on DMMA (sk_dense.cuh): persistent warps over 8-element groups
 template <int S, int P, int PW, int GEO>
 int launch_dense_geo(const DenseArgs& a, int ncomp, void* stream) {
@@ -513,6 +545,12 @@ int launch(int op, const LaunchReq& r, void* stream) {
             return go<S, P, OP_HELM, k_helm<S, P, typename C::L, C::NT, C::PW, GEO_DEFORMED, true, C::MINB, true>>(a, r, 1, stream);
         }
         return (int)cudaErrorInvalidValue;
+      }
+      if constexpr (helm_tma(S, P) && C::RING == 0) {
+        if (def && helm_tma_enabled()) {
+          if (r.lam != 0.0) return go_tma<S, P, OP_HELM, k_helm<S, P, typename C::L, C::NT, C::PW, GEO_DEFORMED, true, C::MINB>>(a, r, r.ncomp, stream);
+          return go_tma<S, P, OP_HELM, k_helm<S, P, typename C::L, C::NT, C::PW, GEO_DEFORMED, false, C::MINB>>(a, r, r.ncomp, stream);
+        }
       }
       if (def) {
         if (r.lam != 0.0) return go<S, P, OP_HELM, k_helm<S, P, typename C::L, C::NT, C::PW, GEO_DEFORMED, true, C::MINB, false, C::RING>>(a, r, r.ncomp, stream);

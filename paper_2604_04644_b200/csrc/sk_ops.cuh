@@ -201,6 +201,87 @@ __device__ __forceinline__ void stage_tables(const double* __restrict__ gtab, do
   for (int t = threadIdx.x; t < GLayout<S, P>::RAGGED; t += NT) st[t] = __ldg(gtab + t);
 }
 
+// Persistent driver with TMA-staged coefficient tiles: the next tile's
+// coefficient block (interleave width 1: EB x NM contiguous doubles) is
+// bulk-copied (SASS UBLKCP) into a double buffer behind the Op's shared
+// memory while the current tile runs, completing on an mbarrier, then
+// transposed smem-to-smem into the staging area (plane 1) -- no registers
+// held across the tile (unlike k_persist's register-staged next tile) and
+// no exposed load latency at the tile's first barrier (unlike k_tile).
+// Ragged last tiles, other interleave widths and unaligned component
+// offsets take load_tile.  The ragged tables (SMT) are staged once.
+template <class Op, class Args, int NM, int SMEM0>
+struct PersistTma {
+  static constexpr int CB = Op::EB * NM + 2;  // one buffer: the block plus 16-byte rounding
+  static constexpr int CBUF = (SMEM0 / 8 + 1) / 2 * 2;
+  static constexpr int MBAR = CBUF + 2 * ((CB + 1) / 2 * 2);
+  static constexpr int SMEM = MBAR * 8 + 2 * 8;
+};
+
+template <class Op, class Args, int NM, int SMEM0>
+__global__ void __launch_bounds__(Op::NT, Op::MINB) k_persist_tma(const __grid_constant__ Args A) {
+  using T = PersistTma<Op, Args, NM, SMEM0>;
+  using L = typename Op::LayT;
+  constexpr int EB = Op::EB, NT = Op::NT, CBS = (T::CB + 1) / 2 * 2;
+  extern __shared__ double sm[];
+  double* cbuf = sm + T::CBUF;
+  unsigned long long* mb = reinterpret_cast<unsigned long long*>(sm + T::MBAR);
+  double* xs = sm + EB * L::PLANE;
+  const long long ntiles = (A.Epad + EB - 1) / EB;
+  const long long stride = gridDim.x;
+  const double* src = A.in + blockIdx.y * A.in_cstride;
+  // a whole tile's block (interleave width 1: EB * NM contiguous doubles)
+  // moves as the 16-byte-aligned range covering it; not when that range
+  // would end past the component's last element
+  auto span = [&](long long t, unsigned long long& a0, unsigned& bytes, int& off) {
+    const long long e0 = t * EB;
+    const unsigned long long a = reinterpret_cast<unsigned long long>(src + e0 * NM);
+    const unsigned long long end = a + (unsigned long long)EB * NM * 8;
+    a0 = a & ~15ULL;
+    off = (int)((a - a0) / 8);
+    bytes = (unsigned)(((end + 15) & ~15ULL) - a0);
+    return A.W == 1 && e0 + EB <= A.E && (e0 + EB < A.E || (end & 15) == 0);
+  };
+  auto issue = [&](long long tt, int buf) {
+    unsigned long long a0;
+    unsigned bytes;
+    int off;
+    if (span(tt, a0, bytes, off)) {
+      mbar_expect_tx(&mb[buf], bytes);
+      bulk_g2s(cbuf + buf * CBS, reinterpret_cast<const void*>(a0), bytes, &mb[buf]);
+    }
+  };
+  long long t = blockIdx.x;
+  if (threadIdx.x == 0) {
+    mbar_init(&mb[0], 1);
+    mbar_init(&mb[1], 1);
+    mbar_fence_init();
+    if (t < ntiles) issue(t, 0);
+  }
+  if constexpr (Op::SMT) stage_tables<Op::S_, Op::P_, NT>(A.gtab, sm + L::TABOFF);
+  if (threadIdx.x < 32 && t < ntiles) Op::prefetch_geo(A, t);
+  for (int i = 0; t < ntiles; t += stride, ++i) {
+    const int b = i & 1;
+    if (threadIdx.x == 0 && t + stride < ntiles) issue(t + stride, b ^ 1);
+    __syncthreads();  // the previous tile's store has read the staging area
+    unsigned long long a0;
+    unsigned bytes;
+    int off;
+    if (span(t, a0, bytes, off)) {
+      mbar_wait(&mb[b], (i >> 1) & 1);
+      const double* cb = cbuf + b * CBS + off;
+      for (int g = threadIdx.x; g < EB * NM; g += NT) {
+        const int e = g / NM, m = g - e * NM;
+        xs[m * L::XSTR + e] = cb[g];
+      }
+    } else {
+      load_tile<L, NM, NT>(src, make_ctx<EB>(t, A.E, A.Epad, A.W), xs);
+    }
+    __syncthreads();
+    Op::body(A, t, sm, t + stride < ntiles ? t + stride : -1);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Helmholtz, collocated: 9 sweeps + coefficient tile staging, 10 CTA barriers
 template <int S, int P, class L, int NT_, int PW, int GEO, bool LAMW, int MINB_, bool C0 = false, int RING = 0>
@@ -208,6 +289,8 @@ struct k_helm {
   static constexpr int NT = NT_;
   static constexpr int EB = L::EB;
   static constexpr int MINB = MINB_;
+  static constexpr int S_ = S, P_ = P;
+  using LayT = L;
   // TMA geometry ring (RING > 0 slots, sk_tune.h kGeoRing): slot s holds one
   // k-slice [C][Q0*Q1][PW] of the tile's payload, after the work planes
   // (and staged tables); then RING "full" and RING "empty" mbarriers

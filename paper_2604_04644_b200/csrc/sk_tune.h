@@ -233,6 +233,29 @@ SK_HD constexpr bool mass_tma(int, int) { return SK_MASS_TMA; }
 SK_HD constexpr bool mass_tma(int S, int P) { return kMassTma[S][P]; }
 #endif
 
+// Deformed Helmholtz / stiffness through the persistent TMA-staged driver
+// (sk_ops.cuh k_persist_tma) instead of k_tile / k_persist, per shape x
+// order.  Measured on B200 (profiles/r02/helm_tma_ab*.jsonl, roofline
+// fraction Helmholtz / stiffness, default -> TMA): hex P=6 0.86 -> 0.92 /
+// 0.81 -> 0.85, P=7 0.65 -> 0.72, P=8 0.65 -> 0.68 / 0.64 -> 0.67, P=9
+// 0.70 -> 0.77; prism P=2 0.90 -> 0.94; pyr P=2 0.88 -> 0.92 / 0.80 -> 0.84,
+// P=3 stiffness 0.69 -> 0.74, P=5 0.65 -> 0.72.  It loses at prism / pyr /
+// tet P>=6 and hex P<=5, P=10: one resident wave, the register-capped tile
+// spills a little.  Build-time override for A/B: -DSK_HELM_TMA=0/1;
+// run-time: SK_HELM_TMA=0.
+constexpr bool kHelmTma[4][11] = {
+    // P: 0  1  2  3  4  5  6  7  8  9 10
+    {0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 0},  // hex
+    {0, 0, 1, 0, 0, 0, 0, 0, 0, 0, 0},  // prism
+    {0, 0, 1, 1, 0, 1, 0, 0, 0, 0, 0},  // pyr
+    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},  // tet
+};
+#ifdef SK_HELM_TMA
+SK_HD constexpr bool helm_tma(int, int) { return SK_HELM_TMA; }
+#else
+SK_HD constexpr bool helm_tma(int S, int P) { return kHelmTma[S][P]; }
+#endif
+
 // Sum-factorised mass with one warp per tile (sk_ops.cuh k_mass_warp, no CTA
 // barriers) instead of the CTA-tile k_mass: elements per warp tile G and
 // warps per CTA, per shape x order (G = 0: CTA tiles).  Build-time
