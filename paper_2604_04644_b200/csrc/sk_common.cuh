@@ -111,6 +111,10 @@ __host__ __device__ constexpr bool use_eo(int S, int P) {
   return P >= (S == HEX ? 6 : S == TET ? 4 : 3);
 }
 #endif
+// the mass kernels' sweeps (measured separately: hex P=5 mass 0.53 -> 0.65 of
+// its roofline with even-odd, while the Helmholtz kernel loses 5 % there;
+// profiles/r02/eo_hex5.jsonl)
+__host__ __device__ constexpr bool use_eo_mass(int S, int P) { return use_eo(S, P) || (S == HEX && P == 5); }
 
 template <int S, int P>
 struct FwdTab {

@@ -780,16 +780,17 @@ struct k_mass {
   constexpr int P1 = Dm::P1, Q0 = Dm::Q0, Q1 = Dm::Q1, Q2 = Dm::Q2, S2 = L::S2, NM = Dm::NM;
   constexpr int PL = L::PLANE, TAo = 0, TBo = PL;
   constexpr bool WP = NT > 32 && prism_warp_pairs(1, S, P);
+  constexpr bool EO = use_eo_mass(S, P);
   const Ctx c = make_ctx<L::EB>(tile, A.E, A.Epad, A.W);
   const double* src = A.in + blockIdx.y * A.in_cstride;
   double* dst = A.out + blockIdx.y * A.out_cstride;
   double* xs = sm + L::EB * PL;  // plane 1 (TB): staging before F2 and after B2
   if constexpr (SMT)  // ragged sweep tables staged in shared memory
-    stage_f1<S, P, L, NT, TAo, CoefIn<L, NM>, false, ragged_dispatch(1, S, P), ragged_split(1, S, P), WP, true>(A.B, stab, CoefIn<L, NM>{xs}, sm);
+    stage_f1<S, P, L, NT, TAo, CoefIn<L, NM>, false, ragged_dispatch(1, S, P), ragged_split(1, S, P), WP, true, EO>(A.B, stab, CoefIn<L, NM>{xs}, sm);
   else
-    stage_f1<S, P, L, NT, TAo, CoefIn<L, NM>, false, ragged_dispatch(1, S, P), ragged_split(1, S, P), WP>(A.B, A.gtab, CoefIn<L, NM>{xs}, sm);
+    stage_f1<S, P, L, NT, TAo, CoefIn<L, NM>, false, ragged_dispatch(1, S, P), ragged_split(1, S, P), WP, false, EO>(A.B, A.gtab, CoefIn<L, NM>{xs}, sm);
   csync<NT>();
-  stage_f2<S, P, L, NT, TAo, TBo>(A.B, A.gtab, sm);
+  stage_f2<S, P, L, NT, TAo, TBo, false, EO>(A.B, A.gtab, sm);
   csync<NT>();
   pre();
   items<L, Q1 * Q2, NT>([&](int e, int ps) {
@@ -799,21 +800,21 @@ struct k_mass {
     double x[P1], u[Q0];
 #pragma unroll
     for (int p = 0; p < P1; ++p) x[p] = sm[L::at(e, TBo + (p * Q1 + j) * S2 + k)];
-    line_a0_eo<S, P>(A.B, x, u);
+    line_a0_eo<S, P, EO>(A.B, x, u);
 #pragma unroll
     for (int i = 0; i < Q0; ++i) u[i] *= wf(eg, live, (i * Q1 + j) * Q2 + k, e);
-    line_a0t_eo<S, P>(A.B, u, x);
+    line_a0t_eo<S, P, EO>(A.B, u, x);
 #pragma unroll
     for (int p = 0; p < P1; ++p) sm[L::at(e, TBo + (p * Q1 + j) * S2 + k)] = x[p];
   });
   csync<NT>();
   hook();
-  stage_b2<S, P, L, NT, TAo, TBo>(A.B, A.gtab, sm);
+  stage_b2<S, P, L, NT, TAo, TBo, false, false, EO>(A.B, A.gtab, sm);
   csync<NT>();
   if constexpr (SMT)
-    stage_b3<S, P, L, NT, TAo, CoefOut<L, NM>, false, ragged_dispatch(1, S, P), ragged_split(1, S, P), WP, true>(A.B, stab, CoefOut<L, NM>{xs}, sm);
+    stage_b3<S, P, L, NT, TAo, CoefOut<L, NM>, false, ragged_dispatch(1, S, P), ragged_split(1, S, P), WP, true, EO>(A.B, stab, CoefOut<L, NM>{xs}, sm);
   else
-    stage_b3<S, P, L, NT, TAo, CoefOut<L, NM>, false, ragged_dispatch(1, S, P), ragged_split(1, S, P), WP>(A.B, A.gtab, CoefOut<L, NM>{xs}, sm);
+    stage_b3<S, P, L, NT, TAo, CoefOut<L, NM>, false, ragged_dispatch(1, S, P), ragged_split(1, S, P), WP, false, EO>(A.B, A.gtab, CoefOut<L, NM>{xs}, sm);
   csync<NT>();
   store_tile<L, NM, NT>(dst, c, xs);
   }

@@ -376,17 +376,17 @@ __device__ __forceinline__ void line_ddt_acc(const DTab<S, P>& D, const double (
 }
 
 // dir-0 value contractions in even-odd form (value tables only)
-template <int S, int P>
+template <int S, int P, bool EO = use_eo(S, P)>
 __device__ __forceinline__ void line_a0_eo(const FwdTab<S, P>& B, const double (&x)[P + 1], double (&u)[Dims<S, P>::Q0]) {
-  if constexpr (use_eo(S, P))
+  if constexpr (EO)
     line_b_eo<Dims<S, P>::Q0, P + 1>(B.a0, B.a0p, B.a0m, x, u);
   else
     line_a0<S, P>(B, x, u);
 }
 
-template <int S, int P>
+template <int S, int P, bool EO = use_eo(S, P)>
 __device__ __forceinline__ void line_a0t_eo(const FwdTab<S, P>& B, const double (&r)[Dims<S, P>::Q0], double (&t)[P + 1]) {
-  if constexpr (use_eo(S, P))
+  if constexpr (EO)
     line_bt_eo<Dims<S, P>::Q0, P + 1>(B.a0, B.a0p, B.a0m, r, t);
   else
     line_a0t<S, P>(B, r, t);
@@ -397,7 +397,7 @@ __device__ __forceinline__ void line_a0t_eo(const FwdTab<S, P>& B, const double 
 // caller passes the derivative FwdTab for hex/prism, the device buffer's DC2
 // slices are used for pyr/tet)
 template <int S, int P, class L, int NT, int TAo, class In, bool DER2 = false, bool RD = false, bool SPL = false,
-          bool WP = false, bool SMT = false>
+          bool WP = false, bool SMT = false, bool EO = use_eo(S, P)>
 __device__ __forceinline__ void stage_f1(const FwdTab<S, P>& B, const double* __restrict__ gtab, const In& xin,
                                          double* sm) {
   using Dm = Dims<S, P>;
@@ -407,7 +407,7 @@ __device__ __forceinline__ void stage_f1(const FwdTab<S, P>& B, const double* __
       double x[P1];
 #pragma unroll
       for (int r = 0; r < P1; ++r) x[r] = xin(e, ps * P1 + r);
-      if constexpr (!DER2 && use_eo(S, P)) {
+      if constexpr (!DER2 && EO) {
         double u[Q2];
         line_b_eo<Q2, P1>(B.a2, B.a2p, B.a2m, x, u);
 #pragma unroll
@@ -587,7 +587,7 @@ __device__ __forceinline__ void stage_f1(const FwdTab<S, P>& B, const double* __
 // DER1: the dir-1 family is the derivative one (reference dmode == 1): the
 // caller passes the derivative FwdTab and the apex share's constant eta_2
 // factor differentiates to zero ("ones2", operators.py:233-235)
-template <int S, int P, class L, int NT, int TAo, int TBo, bool DER1 = false>
+template <int S, int P, class L, int NT, int TAo, int TBo, bool DER1 = false, bool EO = use_eo(S, P)>
 __device__ __forceinline__ void stage_f2(const FwdTab<S, P>& B, const double* __restrict__ gtab, double* sm) {
   using Dm = Dims<S, P>;
   constexpr int P1 = Dm::P1, Q1 = Dm::Q1, Q2 = Dm::Q2, S2 = L::S2;
@@ -599,7 +599,7 @@ __device__ __forceinline__ void stage_f2(const FwdTab<S, P>& B, const double* __
       for (int q = 0; q < P1; ++q) x[q] = sm[L::at(e, TAo + (p * P1 + q) * S2 + k)];
       double y = 0.0;
       if constexpr (S == PYR) y = sm[L::at(e, TAo + P1 * P1 * S2 + k)];
-      if constexpr (!DER1 && use_eo(S, P)) {
+      if constexpr (!DER1 && EO) {
         // apex shares (operators.py:335-349): a1[j][1] y into p = 0, y into p = 1
         if constexpr (S == PYR) {
           if (p == 0) x[1] += y;
@@ -718,7 +718,7 @@ __device__ __forceinline__ void stage_f2(const FwdTab<S, P>& B, const double* __
 // ---- B2: j -> q.  TA[p][q][k] = sum_j B_p[j][q] TB[p][j][k] ---------------
 // DER1: derivative dir-1 family (transposed dmode == 1, apex "ones" share
 // vanishes); ACC: add into TA and the spare rows instead of overwriting
-template <int S, int P, class L, int NT, int TAo, int TBo, bool DER1 = false, bool ACC = false>
+template <int S, int P, class L, int NT, int TAo, int TBo, bool DER1 = false, bool ACC = false, bool EO = use_eo(S, P)>
 __device__ __forceinline__ void stage_b2(const FwdTab<S, P>& B, const double* __restrict__ gtab, double* sm) {
   using Dm = Dims<S, P>;
   constexpr int P1 = Dm::P1, Q1 = Dm::Q1, Q2 = Dm::Q2, S2 = L::S2;
@@ -728,7 +728,7 @@ __device__ __forceinline__ void stage_b2(const FwdTab<S, P>& B, const double* __
       double x[Q1];
 #pragma unroll
       for (int j = 0; j < Q1; ++j) x[j] = sm[L::at(e, TBo + (p * Q1 + j) * S2 + k)];
-      if constexpr (!DER1 && use_eo(S, P)) {
+      if constexpr (!DER1 && EO) {
         double t[P1];
         line_bt_eo<Q1, P1>(B.a1, B.a1p, B.a1m, x, t);
 #pragma unroll
@@ -847,7 +847,7 @@ __device__ __forceinline__ void stage_b2(const FwdTab<S, P>& B, const double* __
 // DER2: derivative dir-2 family (transposed dmode == 2); accumulation into
 // the output is the Out functor's business
 template <int S, int P, class L, int NT, int TAo, class Out, bool DER2 = false, bool RD = false, bool SPL = false,
-          bool WP = false, bool SMT = false>
+          bool WP = false, bool SMT = false, bool EO = use_eo(S, P)>
 __device__ __forceinline__ void stage_b3(const FwdTab<S, P>& B, const double* __restrict__ gtab, const Out& out,
                                          const double* sm) {
   using Dm = Dims<S, P>;
@@ -857,7 +857,7 @@ __device__ __forceinline__ void stage_b3(const FwdTab<S, P>& B, const double* __
       double x[Q2];
 #pragma unroll
       for (int k = 0; k < Q2; ++k) x[k] = sm[L::at(e, TAo + ps * S2 + k)];
-      if constexpr (!DER2 && use_eo(S, P)) {
+      if constexpr (!DER2 && EO) {
         double t[P1];
         line_bt_eo<Q2, P1>(B.a2, B.a2p, B.a2m, x, t);
 #pragma unroll
