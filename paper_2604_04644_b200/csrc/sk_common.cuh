@@ -111,10 +111,13 @@ __host__ __device__ constexpr bool use_eo(int S, int P) {
   return P >= (S == HEX ? 6 : S == TET ? 4 : 3);
 }
 #endif
-// the mass kernels' sweeps (measured separately: hex P=5 mass 0.53 -> 0.65 of
-// its roofline with even-odd, while the Helmholtz kernel loses 5 % there;
-// profiles/r02/eo_hex5.jsonl)
-__host__ __device__ constexpr bool use_eo_mass(int S, int P) { return use_eo(S, P) || (S == HEX && P == 5); }
+// the mass kernels' sweeps, measured separately (roofline fraction plain ->
+// even-odd): hex P=5 0.53 -> 0.65 (the Helmholtz kernel loses 5 % there),
+// hex P=4 0.69 -> 0.73, prism P=2 0.66 -> 0.70; neutral at hex P=2-3, pyr /
+// tet P=2-3 (profiles/r02/eo_hex5*.jsonl, eo_mass_low.jsonl)
+__host__ __device__ constexpr bool use_eo_mass(int S, int P) {
+  return use_eo(S, P) || (S == HEX && P >= 4) || (S == PRISM && P >= 2);
+}
 
 template <int S, int P>
 struct FwdTab {
