@@ -59,7 +59,7 @@ struct Cfg {
                                     cmax(Dm::NPAIR, Dm::P1 * Dm::Q2));
   using L = Lay<S, P, planes, EB>;
   static constexpr int CLS = (OP == OP_HELM || OP == OP_QP) ? 0 : OP == OP_MASS ? 1 : 2;
-  static constexpr int NT0 = ((EB * items / (REG ? tuned_nt_div_regular(S, P) : tuned_nt_div(CLS, S, P)) + 31) / 32) * 32;
+  static constexpr int NT0 = ((EB * items / (REG ? tuned_nt_div_regular(S, P) : nt_div_op(OP, CLS, S, P)) + 31) / 32) * 32;
   static constexpr int NT = NT0 > 512 ? 512 : (NT0 < 64 ? 64 : NT0);
   // deformed Helmholtz: TMA geometry ring after the planes (sk_tune.h kGeoRing)
   static constexpr int RING = (OP == OP_HELM && !REG && geo_ring(S, P) > 0 && EB * Dm::Q0 * Dm::Q1 <= NT &&
@@ -70,7 +70,7 @@ struct Cfg {
   static constexpr int SMEM = RING ? (SMEM0 + 15) / 16 * 16 + RING * (7 * Dm::Q0 * Dm::Q1 * EB * 8 + 16) : SMEM0;
   // __launch_bounds__ min blocks: 1, or the CTAs per SM that shared memory
   // allows (forces ptxas to fit the registers; tuned, as it can spill)
-  static constexpr int MINB = tuned_minb(CLS, S, P) ? cmax(1, cmin(cmin(tuned_minb_cap(CLS, S, P), (220 * 1024) / (SMEM + 1024)), 2048 / NT))
+  static constexpr int MINB = minb_op(OP, CLS, S, P) ? cmax(1, cmin(cmin(tuned_minb_cap(CLS, S, P), (220 * 1024) / (SMEM + 1024)), 2048 / NT))
                                                : 1;
 };
 

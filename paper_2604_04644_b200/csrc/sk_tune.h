@@ -358,6 +358,76 @@ SK_HD constexpr int tuned_minb_cap(int, int, int) { return SK_MINB_CAP; }
 #else
 SK_HD constexpr int tuned_minb_cap(int cls, int S, int P) { return kMinBCap[cls][S][P]; }
 #endif
+// Per-operator overrides of the class-2 launch tables for bwd_trans,
+// iproduct_wrt_base, phys_deriv, iproduct_wrt_deriv_base and the
+// non-collocated Helmholtz (they share kTunedNTDiv[2] / kTunedMinB[2]):
+// thread divisor (0 = the class table) and min-blocks rule (-1 = the class
+// table, 0 = none), shape x order.  From a deformed grid over divisors
+// 1/2/4 and min-blocks off (profiles/r02/other_ops_grid.jsonl), adopted
+// where >= 8 % faster than the class setting: e.g. iproduct_wrt_deriv_base
+// pyr P=5 0.32 -> 0.59, prism P=4 0.21 -> 0.42; non-collocated Helmholtz
+// hex P=3 0.44 -> 0.61, tet P=3 0.38 -> 0.52; bwd_trans pyr P=3 0.44 ->
+// 0.58; iproduct_wrt_base hex P=5 0.68 -> 0.86.
+constexpr int kOpNTDiv[5][4][11] = {
+    {{ 0,  0,  0,  4,  4,  0,  0,  0,  0,  0,  0},
+     { 0,  0,  0,  4,  0,  4,  0,  0,  0,  0,  0},
+     { 0,  0,  0,  4,  0,  0,  0,  0,  0,  2,  0},
+     { 0,  1,  0,  4,  0,  0,  0,  0,  4,  4,  0}},  // bwd
+    {{ 0,  1,  0,  0,  4,  0,  0,  2,  0,  0,  0},
+     { 0,  0,  0,  2,  0,  0,  0,  0,  0,  0,  0},
+     { 0,  0,  0,  0,  0,  0,  0,  2,  0,  0,  0},
+     { 0,  1,  0,  0,  0,  0,  0,  0,  0,  0,  0}},  // iprod
+    {{ 0,  1,  0,  0,  0,  0,  0,  0,  0,  2,  0},
+     { 0,  1,  1,  0,  0,  0,  0,  0,  0,  2,  0},
+     { 0,  1,  1,  0,  0,  0,  0,  0,  2,  2,  0},
+     { 0,  1,  1,  0,  0,  0,  0,  0,  0,  0,  0}},  // pderiv
+    {{ 0,  0,  0,  0,  2,  0,  0,  2,  0,  0,  0},
+     { 0,  0,  0,  2,  0,  0,  0,  0,  0,  0,  0},
+     { 0,  0,  0,  0,  0,  0,  0,  2,  0,  0,  0},
+     { 0,  0,  0,  0,  0,  0,  0,  0,  2,  0,  0}},  // ipderiv
+    {{ 0,  0,  0,  4,  0,  0,  0,  0,  0,  0,  0},
+     { 0,  0,  4,  4,  4,  4,  2,  4,  0,  0,  0},
+     { 0,  0,  0,  4,  0,  4,  2,  0,  0,  0,  4},
+     { 0,  0,  0,  4,  4,  0,  0,  0,  0,  0,  0}},  // helmnc
+};
+constexpr int kOpMinB[5][4][11] = {
+    {{-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1},
+     {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1},
+     {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1},
+     {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1}},  // bwd
+    {{-1, -1, -1, -1, -1,  0, -1, -1, -1, -1, -1},
+     {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1},
+     {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1},
+     {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1}},  // iprod
+    {{-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1},
+     {-1, -1, -1,  0, -1,  0, -1, -1, -1, -1, -1},
+     {-1, -1, -1,  0, -1, -1, -1, -1, -1, -1, -1},
+     {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1}},  // pderiv
+    {{-1, -1, -1, -1, -1,  0, -1, -1, -1, -1, -1},
+     {-1, -1, -1, -1,  0, -1, -1,  0, -1, -1, -1},
+     {-1, -1, -1, -1,  0,  0, -1, -1, -1, -1, -1},
+     {-1, -1, -1, -1,  0, -1, -1, -1, -1, -1, -1}},  // ipderiv
+    {{-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1},
+     {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1},
+     {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1},
+     {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1}},  // helmnc
+};
+SK_HD constexpr int op_slot(int op) { return op >= 2 && op <= 6 ? op - 2 : -1; }  // OP_BWD .. OP_HELM_NC
+#if defined(SK_NT_DIV)
+SK_HD constexpr int nt_div_op(int op, int cls, int S, int P) { return tuned_nt_div(cls, S, P); }
+#else
+SK_HD constexpr int nt_div_op(int op, int cls, int S, int P) {
+  return op_slot(op) >= 0 && kOpNTDiv[op_slot(op)][S][P] > 0 ? kOpNTDiv[op_slot(op)][S][P] : tuned_nt_div(cls, S, P);
+}
+#endif
+#if defined(SK_MINB)
+SK_HD constexpr int minb_op(int op, int cls, int S, int P) { return tuned_minb(cls, S, P); }
+#else
+SK_HD constexpr int minb_op(int op, int cls, int S, int P) {
+  return op_slot(op) >= 0 && kOpMinB[op_slot(op)][S][P] >= 0 ? kOpMinB[op_slot(op)][S][P] : tuned_minb(cls, S, P);
+}
+#endif
+
 #ifdef SK_PERSIST
 constexpr bool tuned_persist(int, int, int) { return SK_PERSIST; }
 #else

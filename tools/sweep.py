@@ -55,7 +55,9 @@ def main():
     deformed = a.geo == "deformed"
     kinds = {"helm": (sk.OperatorKind.HELMHOLTZ_COLL, 1.0), "stiff": (sk.OperatorKind.HELMHOLTZ_COLL, 0.0),
              "mass": (sk.OperatorKind.MASS, 1.0), "helmnc": (sk.OperatorKind.HELMHOLTZ_NONCOLL, 1.0),
-             "helmstaged": (sk.OperatorKind.HELMHOLTZ_COLL, 1.0), "stiffstaged": (sk.OperatorKind.HELMHOLTZ_COLL, 0.0)}
+             "helmstaged": (sk.OperatorKind.HELMHOLTZ_COLL, 1.0), "stiffstaged": (sk.OperatorKind.HELMHOLTZ_COLL, 0.0),
+             "bwd": (sk.OperatorKind.BWD_TRANS, 0.0), "iprod": (sk.OperatorKind.IPRODUCT_WRT_BASE, 0.0),
+             "pderiv": (sk.OperatorKind.PHYS_DERIV, 0.0), "ipderiv": (sk.OperatorKind.IPRODUCT_WRT_DERIV_BASE, 0.0)}
     cases = []
     emax = 1
     for op in a.ops.split(","):
@@ -73,10 +75,22 @@ def main():
             fac = sk.GeometricFactors(sk.GeometryClass.DEFORMED, b.shape, E, params=params[:E], basis=b)
         else:
             fac = sk.make_synthetic_factors(b, sk.GeometryClass.REGULAR, E, seed=0)
-        blk = sk.Block(b, fac, sk.FieldState.COEFF, 1, 1)
-        blk.set_elements(np.random.default_rng(P).uniform(-1, 1, (1, b.n_modes, E)))
-        out = blk.like(sk.FieldState.COEFF)
-        if op == "mass":
+        # input state / components per operator (GDOF/s counts coefficient DOFs throughout)
+        st, nc = {"iprod": (sk.FieldState.PHYS, 1), "pderiv": (sk.FieldState.PHYS, 1),
+                  "ipderiv": (sk.FieldState.PHYS, 3)}.get(op, (sk.FieldState.COEFF, 1))
+        blk = sk.Block(b, fac, st, nc, 1)
+        blk.device(sk.AccessQualifier.WRITE_ONLY).uniform_(-1.0, 1.0)
+        out = {"bwd": lambda: blk.like(sk.FieldState.PHYS, 1), "pderiv": lambda: blk.like(sk.FieldState.PHYS, 3),
+               "ipderiv": lambda: blk.like(sk.FieldState.COEFF, 1)}.get(op, lambda: blk.like(sk.FieldState.COEFF))()
+        if op == "bwd":
+            fn = lambda: sk.bwd_trans(blk, out=out)  # noqa: E731
+        elif op == "iprod":
+            fn = lambda: sk.iproduct_wrt_base(blk, out=out)  # noqa: E731
+        elif op == "pderiv":
+            fn = lambda: sk.phys_deriv(blk, out=out)  # noqa: E731
+        elif op == "ipderiv":
+            fn = lambda: sk.iproduct_wrt_deriv_base(blk, out=out)  # noqa: E731
+        elif op == "mass":
             fn = lambda: sk.mass_apply(blk, out=out)  # noqa: E731
         elif op == "helmnc":
             fn = lambda: sk.helmholtz_apply_noncoll(blk, lam, out=out)  # noqa: E731
@@ -96,7 +110,8 @@ def main():
         sec = t0.elapsed_time(t1) / 1e3 / a.reps
         gdof = b.n_modes * E / sec / 1e9
         flops = sk.operator_flops(kind, sk.Shape(s), P) * E
-        cfg = b.launch_config({"mass": 1, "helmnc": 6, "helmstaged": 7, "stiffstaged": 7}.get(op, 0), deformed)
+        cfg = b.launch_config({"mass": 1, "helmnc": 6, "helmstaged": 7, "stiffstaged": 7, "bwd": 2, "iprod": 3, "pderiv": 4,
+                               "ipderiv": 5}.get(op, 0), deformed)
         rec = {
             "op": op, "shape": s, "P": P, "geo": a.geo, "elements": E, "ms": sec * 1e3, "gdof_s": gdof,
             "hbm_gbs": bel * E / sec / 1e9, "hbm_frac": bel * E / sec / 1e9 / hbm,
