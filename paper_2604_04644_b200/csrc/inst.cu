@@ -46,7 +46,11 @@ struct Mode {
   // regular-geometry collocated Helmholtz tile width (its payload lane
   // width is kRegPW, independent of the tile)
   static constexpr int EBHR = tuned_eb_regular(S, P) > 0 ? fit(tuned_eb_regular(S, P), 200 * 1024) : EBH;
-  SK_HD static constexpr int eb(int op) { return (op == OP_HELM || op == OP_HELM_NC || op == OP_PDERIV || op == OP_QP) ? EBH : EBW; }
+  // bwd_trans reads no payload: its own tile width (kTunedEBBwd, 0 = EBW)
+  static constexpr int EBB = tuned_eb_bwd(S, P) > 0 ? fit(tuned_eb_bwd(S, P), 200 * 1024) : EBW;
+  SK_HD static constexpr int eb(int op) {
+    return (op == OP_HELM || op == OP_HELM_NC || op == OP_PDERIV || op == OP_QP) ? EBH : op == OP_BWD ? EBB : EBW;
+  }
 };
 
 template <int S, int P, int OP, bool REG = false>

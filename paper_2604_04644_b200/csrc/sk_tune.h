@@ -333,6 +333,21 @@ SK_HD constexpr int tuned_eb(int, int, int) { return SK_EB_FIXED; }
 #else
 SK_HD constexpr int tuned_eb(int fam, int S, int P) { return kTunedEB[fam][S][P]; }
 #endif
+// bwd_trans tile width (it reads no payload, so it need not match the W
+// family's lane width); 0 = the W family's.  From a tile-width grid
+// (profiles/r02/bwd_eb_grid.jsonl), adopted where >= 8 % faster: e.g. hex
+// P=4 0.45 -> 0.69, tet P=3 0.27 -> 0.41, prism P=3 0.51 -> 0.66.
+constexpr int kTunedEBBwd[4][11] = {
+    { 0,  0,  8,  8,  4,  0,  0,  1,  0,  0,  0},  // hex
+    { 0,  0,  8,  8,  4,  4,  2,  0,  0,  1,  0},  // prism
+    { 0,  0,  8,  0,  4,  0,  2,  4,  0,  0,  0},  // pyr
+    { 0,  0,  0,  8,  4,  0,  0,  4,  0,  0,  0}  // tet
+};
+#ifdef SK_EB_FIXED
+SK_HD constexpr int tuned_eb_bwd(int, int) { return SK_EB_FIXED; }
+#else
+SK_HD constexpr int tuned_eb_bwd(int S, int P) { return kTunedEBBwd[S][P]; }
+#endif
 #ifdef SK_EB_FIXED
 SK_HD constexpr int tuned_eb_regular(int, int) { return SK_EB_FIXED; }
 #else
