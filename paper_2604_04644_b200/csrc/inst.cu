@@ -36,20 +36,26 @@ struct Mode {
   static constexpr int fit(int eb, int budget) {
     return (eb <= 1 || smem_bytes(eb) <= budget) ? eb : fit(eb / 2, budget);
   }
+  // the non-collocated Helmholtz keeps five planes
+  static constexpr int fit5(int eb, int budget) {
+    return (eb <= 1 || smem_bytes(eb) / 3 * 5 <= budget) ? eb : fit5(eb / 2, budget);
+  }
   // Helmholtz family (Helmholtz / stiffness / non-collocated / phys_deriv;
   // payload kinds 0, 2, 3) and W family (mass / iproduct / iproduct-deriv /
   // bwd_trans; payload kind 1): independent tile widths
   static constexpr int EBH = tuned_eb(0, S, P) > 0 ? fit(tuned_eb(0, S, P), 200 * 1024) : fit(16, 100 * 1024);
   static constexpr int EBW = tuned_eb(1, S, P) > 0 ? fit(tuned_eb(1, S, P), 200 * 1024) : fit(16, 100 * 1024);
   // payload lane width of each payload kind = tile width of its consumers
-  SK_HD static constexpr int pw(int kind) { return kind == 1 ? EBW : EBH; }
+  // non-collocated Helmholtz (payload kind 3): its own tile / lane width
+  static constexpr int EBN = tuned_eb_nc(S, P) > 0 ? fit5(tuned_eb_nc(S, P), 200 * 1024) : EBH;
+  SK_HD static constexpr int pw(int kind) { return kind == 1 ? EBW : kind == 3 ? EBN : EBH; }
   // regular-geometry collocated Helmholtz tile width (its payload lane
   // width is kRegPW, independent of the tile)
   static constexpr int EBHR = tuned_eb_regular(S, P) > 0 ? fit(tuned_eb_regular(S, P), 200 * 1024) : EBH;
   // bwd_trans reads no payload: its own tile width (kTunedEBBwd, 0 = EBW)
   static constexpr int EBB = tuned_eb_bwd(S, P) > 0 ? fit(tuned_eb_bwd(S, P), 200 * 1024) : EBW;
   SK_HD static constexpr int eb(int op) {
-    return (op == OP_HELM || op == OP_HELM_NC || op == OP_PDERIV || op == OP_QP) ? EBH : op == OP_BWD ? EBB : EBW;
+    return (op == OP_HELM || op == OP_PDERIV || op == OP_QP) ? EBH : op == OP_HELM_NC ? EBN : op == OP_BWD ? EBB : EBW;
   }
 };
 
@@ -674,7 +680,7 @@ template <int S, int P>
 __device__ __forceinline__ void put_point(int kind, long long e, int l, const double (&dxi)[3][3], double wjac,
                                           double* __restrict__ pay, const double* __restrict__ gtab) {
   using Dm = Dims<S, P>;
-  constexpr int NQ = Dm::NQ, PW = Mode<S, P>::pw(0), PWW = Mode<S, P>::pw(1);
+  constexpr int NQ = Dm::NQ, PW0 = Mode<S, P>::pw(0), PW3 = Mode<S, P>::pw(3), PWW = Mode<S, P>::pw(1);
   const int k = l % Dm::Q2, ij = l / Dm::Q2;
   const long long km = k * Dm::Q0 * Dm::Q1 + ij;
   if (kind == 1) {
@@ -704,7 +710,8 @@ __device__ __forceinline__ void put_point(int kind, long long e, int l, const do
 #pragma unroll
       for (int n = 0; n < 3; ++n) T[a][n] = L[a][0] * G[0][n] + L[a][1] * G[1][n] + L[a][2] * G[2][n];
     const int mi[6] = {0, 0, 0, 1, 1, 2}, ni[6] = {0, 1, 2, 1, 2, 2};
-    double* o = pay + pay_base<PW>(e, 7, NQ) + (kind == 3 ? (long long)l : km) * PW;
+    const int PW = kind == 3 ? PW3 : PW0;
+    double* o = pay + (kind == 3 ? pay_base<PW3>(e, 7, NQ) + (long long)l * PW3 : pay_base<PW0>(e, 7, NQ) + km * PW0);
 #pragma unroll
     for (int c = 0; c < 6; ++c) {
       const int m = mi[c], n = ni[c];
@@ -714,6 +721,7 @@ __device__ __forceinline__ void put_point(int kind, long long e, int l, const do
     return;
   }
   // DERIV: T[m][j] = sum_a G[a][m] dxi[a][j]
+  constexpr int PW = PW0;
   double* o = pay + pay_base<PW>(e, 9, NQ) + km * PW;
 #pragma unroll
   for (int m = 0; m < 3; ++m)
@@ -742,13 +750,13 @@ __global__ void k_pack_deformed(int kind, long long E, const double* __restrict_
 template <int S, int P>
 __global__ void k_pack_regular(int kind, long long E, const double* __restrict__ dxi, const double* __restrict__ jac,
                                double* __restrict__ pay) {
-  constexpr int PW = Mode<S, P>::pw(0), PWW = Mode<S, P>::pw(1);
+  constexpr int PW = Mode<S, P>::pw(0), PW3 = Mode<S, P>::pw(3), PWW = Mode<S, P>::pw(1);
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < E; e += (long long)gridDim.x * blockDim.x) {
     const double* d = dxi + e * 9;
     if (kind == 0 || kind == 3) {
       // kind 0 (collocated Helmholtz) uses the fixed regular lane width
-      const int W0 = kind == 0 ? kRegPW : PW;
-      double* o = pay + (kind == 0 ? pay_base<kRegPW>(e, 8, 1) : pay_base<PW>(e, 8, 1));
+      const int W0 = kind == 0 ? kRegPW : PW3;
+      double* o = pay + (kind == 0 ? pay_base<kRegPW>(e, 8, 1) : pay_base<PW3>(e, 8, 1));
       const int mi[6] = {0, 0, 0, 1, 1, 2}, ni[6] = {0, 1, 2, 1, 2, 2};
       for (int c = 0; c < 6; ++c) {
         const int a = mi[c], b = ni[c];

@@ -343,6 +343,21 @@ constexpr int kTunedEBBwd[4][11] = {
     { 0,  0,  8,  0,  4,  0,  2,  4,  0,  0,  0},  // pyr
     { 0,  0,  0,  8,  4,  0,  0,  4,  0,  0,  0}  // tet
 };
+// non-collocated Helmholtz tile width = its payload's lane width (kind 3);
+// 0 = the Helmholtz family's.  From a tile-width grid with the five-plane
+// fit (profiles/r02/nc_eb_grid*.jsonl), adopted where >= 8 % faster: e.g.
+// pyr P=4 0.33 -> 0.44, tet P=6 0.25 -> 0.36, prism P=8 0.21 -> 0.32.
+constexpr int kTunedEBNc[4][11] = {
+    { 0,  0,  0,  0,  2, 16,  0,  4,  0,  0,  0},  // hex
+    { 0,  0,  0,  0,  0,  0,  0,  0, 16,  0,  4},  // prism
+    { 0,  0, 16,  0, 16,  0,  0,  4,  4,  0,  0},  // pyr
+    { 0,  0,  0,  0,  0,  0,  8,  0,  0,  0,  0},  // tet
+};
+#ifdef SK_EB_FIXED
+SK_HD constexpr int tuned_eb_nc(int, int) { return SK_EB_FIXED; }
+#else
+SK_HD constexpr int tuned_eb_nc(int S, int P) { return kTunedEBNc[S][P]; }
+#endif
 #ifdef SK_EB_FIXED
 SK_HD constexpr int tuned_eb_bwd(int, int) { return SK_EB_FIXED; }
 #else
