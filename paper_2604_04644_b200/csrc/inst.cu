@@ -48,14 +48,16 @@ struct Mode {
   // payload lane width of each payload kind = tile width of its consumers
   // non-collocated Helmholtz (payload kind 3): its own tile / lane width
   static constexpr int EBN = tuned_eb_nc(S, P) > 0 ? fit5(tuned_eb_nc(S, P), 200 * 1024) : EBH;
-  SK_HD static constexpr int pw(int kind) { return kind == 1 ? EBW : kind == 3 ? EBN : EBH; }
+  // phys_deriv (payload kind 2): its own tile / lane width
+  static constexpr int EBD = tuned_eb_pderiv(S, P) > 0 ? fit(tuned_eb_pderiv(S, P), 200 * 1024) : EBH;
+  SK_HD static constexpr int pw(int kind) { return kind == 1 ? EBW : kind == 3 ? EBN : kind == 2 ? EBD : EBH; }
   // regular-geometry collocated Helmholtz tile width (its payload lane
   // width is kRegPW, independent of the tile)
   static constexpr int EBHR = tuned_eb_regular(S, P) > 0 ? fit(tuned_eb_regular(S, P), 200 * 1024) : EBH;
   // bwd_trans reads no payload: its own tile width (kTunedEBBwd, 0 = EBW)
   static constexpr int EBB = tuned_eb_bwd(S, P) > 0 ? fit(tuned_eb_bwd(S, P), 200 * 1024) : EBW;
   SK_HD static constexpr int eb(int op) {
-    return (op == OP_HELM || op == OP_PDERIV || op == OP_QP) ? EBH : op == OP_HELM_NC ? EBN : op == OP_BWD ? EBB : EBW;
+    return (op == OP_HELM || op == OP_QP) ? EBH : op == OP_PDERIV ? EBD : op == OP_HELM_NC ? EBN : op == OP_BWD ? EBB : EBW;
   }
 };
 
@@ -615,11 +617,15 @@ int launch(int op, const LaunchReq& r, void* stream) {
       using C = Cfg<S, P, OP_BT>;
       return go<S, P, OP_BT, k_iprod<S, P, typename C::L, C::NT, C::PW, GEO_UNIT, C::MINB>>(a, r, r.ncomp, stream);
     }
+#endif
+#if !defined(SK_ONLY_OP) || SK_ONLY_OP == 4
     case OP_PDERIV: {
       using C = Cfg<S, P, OP_PDERIV>;
       if (def) return go<S, P, OP_PDERIV, k_pderiv<S, P, typename C::L, C::NT, C::PW, GEO_DEFORMED, C::MINB>>(a, r, 1, stream);
       return go<S, P, OP_PDERIV, k_pderiv<S, P, typename C::L, C::NT, C::PW, GEO_REGULAR, C::MINB>>(a, r, 1, stream);
     }
+#endif
+#if !defined(SK_ONLY_OP)
     case OP_IPDERIV: {
       using C = Cfg<S, P, OP_IPDERIV>;
       if (def) return go<S, P, OP_IPDERIV, k_ipderiv<S, P, typename C::L, C::NT, C::PW, GEO_DEFORMED, C::MINB>>(a, r, 1, stream);
@@ -721,7 +727,7 @@ __device__ __forceinline__ void put_point(int kind, long long e, int l, const do
     return;
   }
   // DERIV: T[m][j] = sum_a G[a][m] dxi[a][j]
-  constexpr int PW = PW0;
+  constexpr int PW = Mode<S, P>::pw(2);
   double* o = pay + pay_base<PW>(e, 9, NQ) + km * PW;
 #pragma unroll
   for (int m = 0; m < 3; ++m)
@@ -768,8 +774,9 @@ __global__ void k_pack_regular(int kind, long long E, const double* __restrict__
     } else if (kind == 1) {
       pay[pay_base<PWW>(e, 1, 1)] = jac[e];
     } else {
-      double* o = pay + pay_base<PW>(e, 9, 1);
-      for (int a = 0; a < 9; ++a) o[a * PW] = d[a];
+      constexpr int PW2 = Mode<S, P>::pw(2);
+      double* o = pay + pay_base<PW2>(e, 9, 1);
+      for (int a = 0; a < 9; ++a) o[a * PW2] = d[a];
     }
   }
 }

@@ -353,6 +353,21 @@ constexpr int kTunedEBNc[4][11] = {
     { 0,  0, 16,  0, 16,  0,  0,  4,  4,  0,  0},  // pyr
     { 0,  0,  0,  0,  0,  0,  8,  0,  0,  0,  0},  // tet
 };
+// phys_deriv tile width = its payload's lane width (kind 2); 0 = the
+// Helmholtz family's.  From a tile-width grid (profiles/r02/pderiv_eb_grid.jsonl),
+// adopted where >= 8 % faster: e.g. prism P=2 0.59 -> 0.86, hex P=3 0.48 ->
+// 0.66, tet P=2 0.64 -> 0.77.
+constexpr int kTunedEBPderiv[4][11] = {
+    { 0,  4,  2,  1,  1,  1,  0,  2,  0,  0,  0},  // hex
+    { 0,  4,  2,  1,  0,  1,  0,  0,  0,  0,  0},  // prism
+    { 0,  4,  2,  1,  1,  0,  0,  2,  0,  0,  0},  // pyr
+    { 0,  8,  4,  0,  1,  1,  0,  0,  0,  0,  0},  // tet
+};
+#ifdef SK_EB_FIXED
+SK_HD constexpr int tuned_eb_pderiv(int, int) { return SK_EB_FIXED; }
+#else
+SK_HD constexpr int tuned_eb_pderiv(int S, int P) { return kTunedEBPderiv[S][P]; }
+#endif
 #ifdef SK_EB_FIXED
 SK_HD constexpr int tuned_eb_nc(int, int) { return SK_EB_FIXED; }
 #else
