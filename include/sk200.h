@@ -170,6 +170,14 @@ enum { SK_STREAM_HELMHOLTZ = 0, SK_STREAM_HELMHOLTZ_NC = 1, SK_STREAM_MASS = 2 }
 int sk_apply_streamed(const sk_basis* b, int op, int geo_class, int64_t E, int W, int ncomp,
                       const double* host_in, double* dev_in, const double* pay, double lam, double* dev_out,
                       double* host_out, int64_t chunk_elements, void* stream);
+/* Same with flags.  SK_STREAM_DIRECT_OUT: the kernels store each chunk's
+ * result straight into host_out (pinned, mapped: the PCIe writes overlap the
+ * next chunks' H2D copies and kernels, no D2H stage); dev_out is not written
+ * and may be NULL.  Fails with SK_ERR_ARG when host_out is not mapped. */
+enum { SK_STREAM_DIRECT_OUT = 1 };
+int sk_apply_streamed_ex(const sk_basis* b, int op, int geo_class, int64_t E, int W, int ncomp,
+                         const double* host_in, double* dev_in, const double* pay, double lam, double* dev_out,
+                         double* host_out, int64_t chunk_elements, int flags, void* stream);
 
 /* ---- assembled C0 variant (hex, conforming, axis-aligned) --------
  * No reference counterpart (global assembly is outside speckern, SPEC.md:8,

@@ -20,6 +20,7 @@ SK_GEO_REGULAR, SK_GEO_DEFORMED = 0, 1
 SK_PAYLOAD_HELMHOLTZ, SK_PAYLOAD_W, SK_PAYLOAD_DERIV, SK_PAYLOAD_HELMHOLTZ_NC = 0, 1, 2, 3
 SK_FORM_COLL, SK_FORM_NONCOLL = 0, 1
 SK_STREAM_HELMHOLTZ, SK_STREAM_HELMHOLTZ_NC, SK_STREAM_MASS = 0, 1, 2
+SK_STREAM_DIRECT_OUT = 1
 
 #: every exported symbol and its (restype, argtypes)
 _P = ctypes.c_void_p
@@ -49,6 +50,7 @@ SIGNATURES = {
     "sk_helmholtz_apply_staged": (_I, [_P, _I, _L, _I, _I, _P, _P, _D, _P, _P, _L, _P]),
     "sk_helmholtz_apply_params": (_I, [_P, _L, _I, _I, _P, _P, _D, _P, _P, _L, _P, _P]),
     "sk_apply_streamed": (_I, [_P, _I, _I, _L, _I, _I, _P, _P, _P, _D, _P, _P, _L, _P]),
+    "sk_apply_streamed_ex": (_I, [_P, _I, _I, _L, _I, _I, _P, _P, _P, _D, _P, _P, _L, _I, _P]),
     "sk_c0_gather": (_I, [_I, _I, _I, _L, _P, _I, _P, _P]),
     "sk_c0_scatter": (_I, [_I, _I, _I, _L, _P, _I, _P, _P]),
     "sk_c0_gather_map": (_I, [_L, _I, _P, _P, _P, _I, _P, _P]),

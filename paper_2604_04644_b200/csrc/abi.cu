@@ -704,7 +704,27 @@ int copy_streams(cudaStream_t* h2d, cudaStream_t* d2h) {
 int sk_apply_streamed(const sk_basis* b, int op, int geo, int64_t E, int W, int ncomp, const double* host_in,
                       double* dev_in, const double* pay, double lam, double* dev_out, double* host_out,
                       int64_t chunk, void* stream) {
-  if (!b || (E > 0 && (!host_in || !dev_in || !pay || !dev_out || !host_out))) return fail(SK_ERR_ARG, "null argument");
+  return sk_apply_streamed_ex(b, op, geo, E, W, ncomp, host_in, dev_in, pay, lam, dev_out, host_out, chunk, 0, stream);
+}
+
+int sk_apply_streamed_ex(const sk_basis* b, int op, int geo, int64_t E, int W, int ncomp, const double* host_in,
+                         double* dev_in, const double* pay, double lam, double* dev_out, double* host_out,
+                         int64_t chunk, int flags, void* stream) {
+  if (flags & ~SK_STREAM_DIRECT_OUT) return fail(SK_ERR_ARG, "unknown streamed-apply flag");
+  // direct output: the kernels store the result straight into the (mapped)
+  // pinned host buffer; no device copy of the output, no D2H stage
+  double* hout_dev = nullptr;
+  if ((flags & SK_STREAM_DIRECT_OUT) && host_out) {
+    void* p = nullptr;
+    if (cudaHostGetDevicePointer(&p, host_out, 0) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(SK_ERR_ARG, "direct output needs mapped pinned host memory");
+    }
+    hout_dev = static_cast<double*>(p);
+  }
+  const bool direct = hout_dev != nullptr;
+  if (!b || (E > 0 && (!host_in || !dev_in || !pay || (!dev_out && !direct) || !host_out)))
+    return fail(SK_ERR_ARG, "null argument");
   if (geo != SK_GEO_REGULAR && geo != SK_GEO_DEFORMED) return fail(SK_ERR_ARG, "bad geometry class");
   if (op != SK_STREAM_HELMHOLTZ && op != SK_STREAM_HELMHOLTZ_NC && op != SK_STREAM_MASS)
     return fail(SK_ERR_ARG, "unknown streamed operator");
@@ -802,20 +822,24 @@ int sk_apply_streamed(const sk_basis* b, int op, int geo, int64_t E, int W, int 
     if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ev[2 * i], 0);
     if (e != cudaSuccess) break;
     r.in = dev_in + e0 * nm;
-    r.out = dev_out + e0 * nm;
+    r.out = (direct ? hout_dev : dev_out) + e0 * nm;
     r.pay = pay + e0 * per_el;  // chunks start on a payload lane group
     r.E = std::max<long long>(0, std::min<long long>(E, e1) - e0);
     r.Epad = e1 - e0;
     g_launches.fetch_add(1, std::memory_order_relaxed);
     e = static_cast<cudaError_t>(b->ops->launch(kop, r, stream));
+    if (direct) continue;
     if (e == cudaSuccess) e = cudaEventRecord(ev[2 * i + 1], s);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(sd, ev[2 * i + 1], 0);
     for (int c = 0; c < ncomp && e == cudaSuccess; ++c)
       e = cudaMemcpyAsync(host_out + c * cs + e0 * nm, dev_out + c * cs + e0 * nm, bytes, cudaMemcpyDeviceToHost, sd);
   }
   // the caller's stream resumes once every chunk is back on the host
-  if (e == cudaSuccess) e = cudaEventRecord(ev[2 * nchunk + 1], sd);
-  if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ev[2 * nchunk + 1], 0);
+  // (direct output: once the last kernel on it has stored its chunk)
+  if (!direct) {
+    if (e == cudaSuccess) e = cudaEventRecord(ev[2 * nchunk + 1], sd);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ev[2 * nchunk + 1], 0);
+  }
   cleanup();
   return cuda_status(e, "streamed apply");
 }

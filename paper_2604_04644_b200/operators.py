@@ -15,6 +15,7 @@ from __future__ import annotations
 
 import ctypes
 import enum
+import os
 
 from paper_2604_04644_b200 import _lib
 from paper_2604_04644_b200.field_block import AccessQualifier, Block, Field, FieldState
@@ -115,8 +116,14 @@ def _geo(block: Block) -> int:
 #: applied chunk-pipelined (H2D / kernel / D2H overlapped, sk_apply_streamed);
 #: smaller ones take the plain transfer-then-apply path
 STREAM_MIN_BYTES = 32 << 20
-#: elements per streamed chunk (0: the library default, ~16 chunks)
+#: elements per streamed chunk (0: the library default, a ramped schedule)
 STREAM_CHUNK_ELEMENTS = 0
+#: SK_STREAM_DIRECT=1: the kernels store the result straight into the pinned
+#: host buffer (SK_STREAM_DIRECT_OUT) and the output stays host-only; off by
+#: default -- it measured within 1 % of the D2H stage on B200 (the two PCIe
+#: directions do not overlap fully there) and the D2H stage
+#: leaves the result live on both sides
+STREAM_DIRECT_OUT = os.environ.get("SK_STREAM_DIRECT", "0") == "1"
 
 
 def _streamed(block: Block, out: Block, op: int, pay, lam: float) -> bool:
@@ -130,17 +137,21 @@ def _streamed(block: Block, out: Block, op: int, pay, lam: float) -> bool:
 
     h_in, d_in = reg.buffers()
     h_out, d_out = out.region.buffers()
+    flags = _lib.SK_STREAM_DIRECT_OUT if STREAM_DIRECT_OUT else 0
     _lib.check(
-        _lib.load().sk_apply_streamed(
+        _lib.load().sk_apply_streamed_ex(
             block.basis.handle, op, _geo(block), block.n_elements, block.interleave_width, block.n_components,
-            _p(h_in), _p(d_in), _p(pay), float(lam), _p(d_out), _p(h_out), STREAM_CHUNK_ELEMENTS, _stream(),
+            _p(h_in), _p(d_in), _p(pay), float(lam), _p(d_out), _p(h_out), STREAM_CHUNK_ELEMENTS, flags, _stream(),
         ),
-        "sk_apply_streamed",
+        "sk_apply_streamed_ex",
     )
     ev = torch.cuda.Event()
     ev.record()
     reg.mark_streamed(ev, wrote_host=False)
-    out.region.mark_streamed(ev, wrote_host=True)
+    if flags:
+        out.region.mark_host_written(ev)
+    else:
+        out.region.mark_streamed(ev, wrote_host=True)
     return True
 
 

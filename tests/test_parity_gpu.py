@@ -279,17 +279,23 @@ def test_every_element_at_scale_by_independent_routes(sk, shape, P, n):
     assert ((ms - md).abs().amax(dim=1) / ms.abs().amax(dim=1)).max().item() <= 1e-12
 
 
+@pytest.mark.parametrize("direct", [True, False])
 @pytest.mark.parametrize("ramp", ["1", "0"])
 @pytest.mark.parametrize("shape,P,width,ncomp", [("tet", 4, 1, 1), ("hex", 3, 8, 2), ("prism", 5, 3, 1)])
-def test_streamed_host_apply(sk, monkeypatch, shape, P, width, ncomp, ramp):
+def test_streamed_host_apply(sk, monkeypatch, shape, P, width, ncomp, ramp, direct):
     """Host-resident input >= STREAM_MIN_BYTES: the chunk-pipelined
-    H2D / kernel / D2H path (sk_apply_streamed) matches the device-resident
-    path bit for bit, with ragged chunks, interleave widths and components,
-    ramped (default) and uniform chunk schedules; both regions count one
-    transfer and hold the result in both spaces."""
+    H2D / kernel / D2H path (sk_apply_streamed_ex) matches the
+    device-resident path bit for bit, with ragged chunks, interleave widths
+    and components, ramped (default) and uniform chunk schedules, and with
+    the kernels storing straight into the pinned host buffer (direct output)
+    or through a D2H stage; both regions count one transfer; with a D2H
+    stage the output is live in both spaces, with direct output on the host
+    only (the device copy comes from one more transfer)."""
     from paper_2604_04644_b200 import operators as ops
+    from paper_2604_04644_b200.field_block import MemorySpace
 
     monkeypatch.setenv("SK_STREAM_RAMP", ramp)
+    monkeypatch.setattr(ops, "STREAM_DIRECT_OUT", direct)
 
     b = sk.build_shape_basis(sk.Shape(shape), P)
     n = ops.STREAM_MIN_BYTES // (8 * b.n_modes * ncomp) + 777
@@ -311,8 +317,10 @@ def test_streamed_host_apply(sk, monkeypatch, shape, P, width, ncomp, ramp):
         got = out.get_elements()
         assert out.region.transfer_count == 1
         assert np.array_equal(got, want), kind
-        # the device copy of the streamed output is live and identical
+        assert out.region.valid(MemorySpace.DEVICE) is (not direct)
+        # the device copy of the streamed output is (or becomes) identical
         assert np.array_equal(out.device().cpu().numpy(), out.host().reshape(-1))
+        assert out.region.transfer_count == (2 if direct else 1)
 
 
 @pytest.mark.parametrize("shape,P,n,width", [("hex", 9, 2500, 1), ("pyr", 3, 40001, 1), ("pyr", 3, 30011, 3)])

@@ -23,10 +23,12 @@ out = blk.like(sk.FieldState.COEFF)
 sk.helmholtz_apply(blk, 1.0, out=out)
 torch.cuda.synchronize()
 ndof = b.n_modes * E
-for nch in (0, -1, 8, 12, 16):
-    # 0: default ramped schedule; -1: default with the ramp off (SK_STREAM_RAMP=0)
+for nch, direct in ((0, True), (0, False), (-1, True), (8, True), (16, True), (32, True)):
+    # 0: default ramped schedule; -1: default with the ramp off (SK_STREAM_RAMP=0);
+    # direct: kernels store straight into the pinned host output (no D2H stage)
     os.environ["SK_STREAM_RAMP"] = "0" if nch == -1 else "1"
     ops.STREAM_CHUNK_ELEMENTS = -(-E // nch) if nch > 0 else 0
+    ops.STREAM_DIRECT_OUT = direct
     for _ in range(2):
         blk.host(sk.AccessQualifier.READ_WRITE)
         sk.helmholtz_apply(blk, 1.0, out=out).host()
@@ -40,11 +42,13 @@ for nch in (0, -1, 8, 12, 16):
             out.host()
         torch.cuda.synchronize()
         best = min(best, (time.perf_counter() - t0) / 8)
-    print(json.dumps({"chunks": nch, "ms_per_step": best * 1e3, "e2e_gdof_s": ndof / best / 1e9}), flush=True)
+    print(json.dumps({"chunks": nch, "direct_out": direct, "ms_per_step": best * 1e3, "e2e_gdof_s": ndof / best / 1e9}),
+          flush=True)
 
 # where the step time goes (default schedule): host time inside the apply
 # call, device time of the apply (events on the current stream), wall
 ops.STREAM_CHUNK_ELEMENTS = 0
+ops.STREAM_DIRECT_OUT = True
 os.environ["SK_STREAM_RAMP"] = "1"
 ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 for _ in range(3):
