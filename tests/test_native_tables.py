@@ -56,6 +56,14 @@ def test_status_codes_and_errors():
     assert lib.sk_helmholtz_apply(b.handle, 1, 0, 4, 1, 1, None, None, -1.0, None, None) == _lib.SK_ERR_ARG
     assert lib.sk_mass_apply(b.handle, 1, -1, 1, 1, None, None, None, None) == _lib.SK_ERR_ARG
     assert lib.sk_bwd_trans(b.handle, 4, 0, 1, None, None, None) == _lib.SK_ERR_ARG
+    # recomputed-metric Helmholtz and the streamed entry point validate before any device work
+    dummy = ctypes.c_void_p(16)
+    assert lib.sk_helmholtz_apply_params(b.handle, 4, 1, 1, None, None, 1.0, None, None, 16, None, None) == _lib.SK_ERR_ARG
+    assert lib.sk_helmholtz_apply_params(b.handle, 4, 1, 1, dummy, dummy, -1.0, dummy, dummy, 16, None, None) == _lib.SK_ERR_ARG
+    assert lib.sk_helmholtz_apply_params(b.handle, 40, 1, 1, dummy, dummy, 1.0, dummy, dummy, 24, None, None) == _lib.SK_ERR_ARG
+    bq = sk.build_shape_basis(sk.Shape.TET, 3, qpoints=(6, 5, 6))
+    assert lib.sk_helmholtz_apply_params(bq.handle, 4, 1, 1, dummy, dummy, 1.0, dummy, dummy, 16, None, None) == _lib.SK_ERR_UNSUPPORTED
+    assert lib.sk_apply_streamed_ex(b.handle, 0, 1, 4, 1, 1, dummy, dummy, dummy, 1.0, dummy, dummy, 0, 4, None) == _lib.SK_ERR_ARG
 
 
 @pytest.mark.parametrize("shape", SHAPES)
