@@ -573,6 +573,12 @@ int launch(int op, const LaunchReq& r, void* stream) {
         return (int)cudaErrorInvalidValue;
       }
       using CR = Cfg<S, P, OP_HELM, true>;  // regular geometry: own tile width
+      if constexpr (helm_tma_reg(S, P)) {
+        if (helm_tma_enabled()) {
+          if (r.lam != 0.0) return go_tma<S, P, OP_HELM, k_helm<S, P, typename CR::L, CR::NT, CR::PW, GEO_REGULAR, true, CR::MINB>, CR>(a, r, r.ncomp, stream);
+          return go_tma<S, P, OP_HELM, k_helm<S, P, typename CR::L, CR::NT, CR::PW, GEO_REGULAR, false, CR::MINB>, CR>(a, r, r.ncomp, stream);
+        }
+      }
       if (r.lam != 0.0) return go<S, P, OP_HELM, k_helm<S, P, typename CR::L, CR::NT, CR::PW, GEO_REGULAR, true, CR::MINB>, CR>(a, r, r.ncomp, stream);
       return go<S, P, OP_HELM, k_helm<S, P, typename CR::L, CR::NT, CR::PW, GEO_REGULAR, false, CR::MINB>, CR>(a, r, r.ncomp, stream);
     }

@@ -250,6 +250,23 @@ constexpr bool kHelmTma[4][11] = {
     {0, 0, 1, 1, 0, 1, 0, 0, 0, 0, 0},  // pyr
     {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},  // tet
 };
+// the same driver for regular-geometry Helmholtz / stiffness (sum-factorised
+// orders; the StdMat kernels take the low orders).  Measured
+// (profiles/r02/helm_tma_regular.jsonl, FP64 roofline fraction Helmholtz /
+// stiffness): tet P=9 0.30 -> 0.40 / 0.34 -> 0.35, prism P=5 0.42 -> 0.44 /
+// 0.43 -> 0.48; it loses at most other orders (hex P=6-8 -15-30 %).
+constexpr bool kHelmTmaReg[4][11] = {
+    // P: 0  1  2  3  4  5  6  7  8  9 10
+    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},  // hex
+    {0, 0, 0, 0, 0, 1, 0, 0, 0, 0, 0},  // prism
+    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},  // pyr
+    {0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 0},  // tet
+};
+#ifdef SK_HELM_TMA_REG
+SK_HD constexpr bool helm_tma_reg(int, int) { return SK_HELM_TMA_REG; }
+#else
+SK_HD constexpr bool helm_tma_reg(int S, int P) { return kHelmTmaReg[S][P]; }
+#endif
 #ifdef SK_HELM_TMA
 SK_HD constexpr bool helm_tma(int, int) { return SK_HELM_TMA; }
 #else

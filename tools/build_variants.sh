@@ -46,6 +46,7 @@ for v in "$@"; do
       mwb) extra="$extra -DSK_MASS_WARP_MINB=$n" ;;
       mtma) extra="$extra -DSK_MASS_TMA=$n" ;;
       htma) extra="$extra -DSK_HELM_TMA=$n" ;;
+      htmar) extra="$extra -DSK_HELM_TMA_REG=$n" ;;
     esac
   done
   make -j"$(nproc)" BUILD=/tmp/sk200_build_$v LIB=$ROOT/paper_2604_04644_b200/libsk200_$v.so LINEINFO= EXTRA="$extra" > /tmp/sk200_build_$v.log 2>&1 \
