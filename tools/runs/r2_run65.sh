@@ -1,0 +1,7 @@
+# driver-equivalent final validation: GPU suite, smoke, reference arm, default bench
+timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/r2run65_pytest.log 2>&1; echo "pytest rc=$?"
+tail -1 gpurun_out/r2run65_pytest.log; grep FAILED gpurun_out/r2run65_pytest.log | head
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r2run65_smoke.log 2>&1; echo "smoke rc=$?"
+tail -4 gpurun_out/r2run65_smoke.log
+timeout 900 python bench.py --impl reference > gpurun_out/r2run65_ref.json 2> gpurun_out/r2run65_ref.err; echo "ref rc=$?"
+timeout 900 python bench.py > gpurun_out/r2run65_bench.json 2> gpurun_out/r2run65_bench.err; echo "bench rc=$?"
