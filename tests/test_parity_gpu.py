@@ -532,3 +532,28 @@ def test_mass_at_scale(sk, shape, P, n):
     got = sk.mass_apply(blk).get_elements()
     for c in range(2):
         assert _err(got[c], O.mass(el, geo, x[c])) <= TOL, c
+
+
+@pytest.mark.parametrize("n", [1, 3, 17, 130])
+@pytest.mark.parametrize("width", [1, 4])
+def test_tma_paths_small_and_ragged(sk, n, width):
+    """The TMA-fed kernels at the cells they are on for (mass pyr P=3, tet
+    P=4; Helmholtz hex P=6, pyr P=5; regular tet P=9): a handful of
+    elements (fewer tiles than CTAs, a ragged last tile, the register path
+    for interleave width 4 and for an unaligned second component) against
+    the oracle."""
+    for shape, P, op, deformed in (("pyr", 3, "mass", True), ("tet", 4, "mass", True), ("hex", 6, "helm", True),
+                                   ("pyr", 5, "helm", True), ("tet", 9, "helm", False)):
+        el = O.element(shape, P)
+        geo = O.synthetic_geometry(el, deformed, n, seed=n)
+        blk = _block_from(sk, shape, P, geo, width, ncomp=2)
+        x = np.random.default_rng(n).uniform(-1, 1, (2, el.nm, n))
+        blk.set_elements(x)
+        if op == "mass":
+            got = sk.mass_apply(blk).get_elements()
+            want = [O.mass(el, geo, x[c]) for c in range(2)]
+        else:
+            got = sk.helmholtz_apply(blk, 0.8).get_elements()
+            want = [O.helmholtz_coll(el, geo, x[c], 0.8) for c in range(2)]
+        for c in range(2):
+            assert _err(got[c], want[c]) <= TOL, (shape, P, op, c)
