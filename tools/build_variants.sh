@@ -1,9 +1,14 @@
 #!/bin/bash
 # Build tuning variants of libsk200 restricted to one operator class:
 #   tools/build_variants.sh op0_eb8_nt1_mb1_cap4 op1_eb16_nt2_mb1_cap8_rd9 ...
-# keys: op (0 Helmholtz/stiffness, 1 mass), eb (tile elements), nt (thread
+# keys: op (SK_ONLY_OP: 0 Helmholtz/stiffness, 1 mass, 2 bwd_trans only,
+# 4 phys_deriv, 6 non-collocated Helmholtz), eb (tile elements), nt (thread
 # divisor), mb (min-blocks rule on/off), cap (CTAs/SM cap), rd (ragged
-# dispatch max order); omitted keys keep the sk_tune.h tables.
+# dispatch max order), lowreg (low-register metric sweep), mtma / htma /
+# htmar (TMA pipelines: mass, deformed / regular Helmholtz), mwg / mwc /
+# mwb (warp-tile mass), eo (even-odd from order), td (tet slice dispatch),
+# s (row stride), iu (items unroll), ps (persistent), ring, ch, pf, ...
+# (see the case list below); omitted keys keep the sk_tune.h tables.
 # -> paper_2604_04644_b200/libsk200_<name>.so, used by tools/tune_eb.py.
 set -e
 ROOT=$(cd "$(dirname "$0")/.." && pwd)
