@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "../../include/sk200.h"
 
@@ -90,6 +91,48 @@ __global__ void k_c0_scatter(int P, int nx, int ny, long long nzl, const double*
   }
 }
 
+// The same scatter over 32 x 32 (gx, gz) tiles of one gy plane: a warp reads
+// a run of 32 consecutive gz -- contiguous modes r of an element column in
+// the element-major local array -- and the sums leave through a transposed
+// shared-memory tile as 32 consecutive gx, so both the local reads and the
+// y writes are coalesced (the one-DOF-per-thread form reads local with the
+// (P+1)^2 stride of the x modes).  Same summation order per DOF.
+__global__ void __launch_bounds__(256) k_c0_scatter_t(int P, int nx, int ny, long long nzl,
+                                                     const double* __restrict__ local, int W, double* __restrict__ y) {
+  __shared__ double tile[32][33];
+  const int P1 = P + 1, NM = P1 * P1 * P1;
+  const long long Nx = (long long)nx * P + 1, Ny = (long long)ny * P + 1, Nz = nzl * P + 1;
+  const long long gx0 = (long long)blockIdx.x * 32, gz0 = (long long)blockIdx.z * 32;
+  const long long gy = blockIdx.y;
+  const int lane = threadIdx.x, warp = threadIdx.y;
+  long long ey[2], ez[2];
+  int py[2], pz[2];
+  const int nyo = dof_owners(gy, P, ny, ey, py);
+  const long long gz = gz0 + lane;
+  const int nzo = gz < Nz ? dof_owners(gz, P, nzl, ez, pz) : 0;
+  for (int i = 0; i < 4; ++i) {
+    const long long gx = gx0 + warp + 8 * i;
+    if (gx >= Nx || gz >= Nz) continue;
+    long long ex[2];
+    int px[2];
+    const int nxo = dof_owners(gx, P, nx, ex, px);
+    double s = 0.0;
+    for (int c = 0; c < nzo; ++c)
+      for (int b = 0; b < nyo; ++b)
+        for (int a = 0; a < nxo; ++a) {
+          const long long e = (ez[c] * ny + ey[b]) * nx + ex[a];
+          const int m = (px[a] * P1 + py[b]) * P1 + pz[c];
+          s += local[lane_idx(e, m, NM, W)];
+        }
+    tile[warp + 8 * i][lane] = s;
+  }
+  __syncthreads();
+  for (int i = 0; i < 4; ++i) {
+    const long long gzw = gz0 + warp + 8 * i, gx = gx0 + lane;
+    if (gx < Nx && gzw < Nz) y[(gzw * Ny + gy) * Nx + gx] = tile[lane][warp + 8 * i];
+  }
+}
+
 // ---- generic signed maps (any shape): gather through l2g / sign, scatter as
 // a gather over each global dof's CSR list of (element, mode) contributions
 __global__ void k_c0_gather_map(long long E, int nm, const long long* __restrict__ l2g,
@@ -140,9 +183,19 @@ int sk_c0_scatter(int order, int nx, int ny, int64_t nz_local, const double* loc
   if (order < 1 || order > 10 || nx < 1 || ny < 1 || nz_local < 0 || W < 1) return SK_ERR_ARG;
   if (nz_local == 0) return SK_OK;
   if (!y || !local) return SK_ERR_ARG;
-  const long long N = ((long long)nx * order + 1) * ((long long)ny * order + 1) * (nz_local * order + 1);
+  const long long Nx = (long long)nx * order + 1, Ny = (long long)ny * order + 1, Nz = nz_local * order + 1;
+  const long long N = Nx * Ny * Nz;
   sk::count_launch();
-  k_c0_scatter<<<grid_for(N), 256, 0, static_cast<cudaStream_t>(stream)>>>(order, nx, ny, nz_local, local, W, y);
+  static const bool tiled = [] {
+    const char* e = std::getenv("SK_C0_SCATTER_TILED");
+    return !(e && e[0] == '0');
+  }();
+  if (tiled && Ny <= 65535 && (Nz + 31) / 32 <= 65535) {
+    const dim3 grid((unsigned)((Nx + 31) / 32), (unsigned)Ny, (unsigned)((Nz + 31) / 32));
+    k_c0_scatter_t<<<grid, dim3(32, 8), 0, static_cast<cudaStream_t>(stream)>>>(order, nx, ny, nz_local, local, W, y);
+  } else {
+    k_c0_scatter<<<grid_for(N), 256, 0, static_cast<cudaStream_t>(stream)>>>(order, nx, ny, nz_local, local, W, y);
+  }
   return cudaGetLastError() == cudaSuccess ? SK_OK : SK_ERR_CUDA;
 }
 
