@@ -19,6 +19,7 @@ elemental operator.
 from __future__ import annotations
 
 import ctypes
+import os
 
 import numpy as np
 
@@ -226,6 +227,17 @@ class _MappedC0Mesh:
             sg = sgn.reshape(-1)
             self._sgn = torch.as_tensor(sg, device=dev)
             self._csgn = torch.as_tensor(sg[order_], device=dev)
+        # compact int32 maps ((index << 1) | negative sign): a third of the map
+        # traffic (sk_c0_gather_map32 / sk_c0_scatter_map32); the int64 / double
+        # maps stay for meshes beyond their index range
+        self._map32 = None
+        nm = self.basis.n_modes
+        if self.n_dofs < (1 << 30) and flat.size < (1 << 31) and os.environ.get("SK_C0_MAP32", "1") != "0":
+            neg = np.zeros(flat.size, dtype=np.int64) if sgn is None else (sgn.reshape(-1) < 0).astype(np.int64)
+            l2gs = ((flat.astype(np.int64) << 1) | neg).astype(np.int32)
+            locs = ((order_.astype(np.int64) << 1) | neg[order_]).astype(np.int32)
+            self._map32 = (torch.as_tensor(l2gs, device=dev), torch.as_tensor(ptr.astype(np.int32), device=dev),
+                           torch.as_tensor(locs, device=dev))
         self.factors = deformed_factors_from_coords(self.basis, coords, either_orientation=either_orientation)
         self.block = Block(self.basis, self.factors, FieldState.COEFF, 1, 1)
         self.out = self.block.like(FieldState.COEFF)
@@ -249,13 +261,21 @@ class _MappedC0Mesh:
         vp = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
         nm = self.basis.n_modes
         local = self.block.device(AccessQualifier.WRITE_ONLY)
-        _lib.check(lib.sk_c0_gather_map(self.E, nm, vp(self._l2g), vp(self._sgn), vp(x), 1, vp(local), s),
-                   "sk_c0_gather_map")
+        m32 = self._map32
+        if m32 is not None:
+            _lib.check(lib.sk_c0_gather_map32(self.E, nm, vp(m32[0]), vp(x), 1, vp(local), s), "sk_c0_gather_map32")
+        else:
+            _lib.check(lib.sk_c0_gather_map(self.E, nm, vp(self._l2g), vp(self._sgn), vp(x), 1, vp(local), s),
+                       "sk_c0_gather_map")
         helmholtz_apply(self.block, lam, out=self.out)
         y = torch.empty(self.n_dofs, dtype=torch.float64, device=x.device)
         loc = self.out.device(AccessQualifier.READ_ONLY)
-        _lib.check(lib.sk_c0_scatter_map(self.n_dofs, nm, vp(self._ptr), vp(self._loc), vp(self._csgn), vp(loc), 1,
-                                         vp(y), s), "sk_c0_scatter_map")
+        if m32 is not None:
+            _lib.check(lib.sk_c0_scatter_map32(self.n_dofs, nm, vp(m32[1]), vp(m32[2]), vp(loc), 1, vp(y), s),
+                       "sk_c0_scatter_map32")
+        else:
+            _lib.check(lib.sk_c0_scatter_map(self.n_dofs, nm, vp(self._ptr), vp(self._loc), vp(self._csgn), vp(loc),
+                                             1, vp(y), s), "sk_c0_scatter_map")
         exchange_interfaces(y, self.layer, group)
         return y
 

@@ -158,6 +158,33 @@ __global__ void k_c0_scatter_map(long long n, int nm, const long long* __restric
   }
 }
 
+// Compact maps: one int32 per entry, (index << 1) | (sign < 0), index < 2^30
+// -- a third of the map bytes of the int64 index + double sign form; the
+// signs are +-1, so negating is bitwise the same as multiplying by them
+__global__ void k_c0_gather_map32(long long E, int nm, const int* __restrict__ l2gs, const double* __restrict__ x,
+                                  int W, double* __restrict__ local) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < E * nm; t += (long long)gridDim.x * blockDim.x) {
+    const long long e = t / nm;
+    const int v = __ldg(l2gs + t);
+    const double xv = __ldg(x + (v >> 1));
+    local[lane_idx(e, (int)(t - e * nm), nm, W)] = (v & 1) ? -xv : xv;
+  }
+}
+
+__global__ void k_c0_scatter_map32(long long n, int nm, const int* __restrict__ ptr, const int* __restrict__ locs,
+                                   const double* __restrict__ local, int W, double* __restrict__ y) {
+  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < n; g += (long long)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int k = __ldg(ptr + g), k1 = __ldg(ptr + g + 1); k < k1; ++k) {
+      const int v = __ldg(locs + k);
+      const long long t = v >> 1, e = t / nm;
+      const double lv = local[lane_idx(e, (int)(t - e * nm), nm, W)];
+      s = fma((v & 1) ? -1.0 : 1.0, lv, s);
+    }
+    y[g] = s;
+  }
+}
+
 unsigned grid_for(long long n) {
   long long g = (n + 255) / 256;
   if (g > 148LL * 32) g = 148LL * 32;
@@ -219,6 +246,28 @@ int sk_c0_scatter_map(int64_t n_dofs, int n_modes, const int64_t* ptr, const int
   k_c0_scatter_map<<<grid_for(n_dofs), 256, 0, static_cast<cudaStream_t>(stream)>>>(
       n_dofs, n_modes, reinterpret_cast<const long long*>(ptr), reinterpret_cast<const long long*>(loc), sgn, local, W,
       y);
+  return cudaGetLastError() == cudaSuccess ? SK_OK : SK_ERR_CUDA;
+}
+
+int sk_c0_gather_map32(int64_t E, int n_modes, const int32_t* l2gs, const double* x, int W, double* local,
+                       void* stream) {
+  if (E < 0 || n_modes < 1 || W < 1 || E * (int64_t)n_modes >= (int64_t(1) << 31)) return SK_ERR_ARG;
+  if (E == 0) return SK_OK;
+  if (!l2gs || !x || !local) return SK_ERR_ARG;
+  sk::count_launch();
+  k_c0_gather_map32<<<grid_for(E * n_modes), 256, 0, static_cast<cudaStream_t>(stream)>>>(E, n_modes, l2gs, x, W,
+                                                                                          local);
+  return cudaGetLastError() == cudaSuccess ? SK_OK : SK_ERR_CUDA;
+}
+
+int sk_c0_scatter_map32(int64_t n_dofs, int n_modes, const int32_t* ptr, const int32_t* locs, const double* local,
+                        int W, double* y, void* stream) {
+  if (n_dofs < 0 || n_modes < 1 || W < 1 || n_dofs >= (int64_t(1) << 30)) return SK_ERR_ARG;
+  if (n_dofs == 0) return SK_OK;
+  if (!ptr || !locs || !local || !y) return SK_ERR_ARG;
+  sk::count_launch();
+  k_c0_scatter_map32<<<grid_for(n_dofs), 256, 0, static_cast<cudaStream_t>(stream)>>>(n_dofs, n_modes, ptr, locs, local,
+                                                                                      W, y);
   return cudaGetLastError() == cudaSuccess ? SK_OK : SK_ERR_CUDA;
 }
 

@@ -151,3 +151,22 @@ def test_assembled_pyr_matches_oracle(torch, P):
     for lam in (0.0, 1.0):
         y = mesh.helmholtz(torch.from_numpy(x).cuda(), lam).cpu().numpy()
         assert O.rel_diff(y, A.assembled_helmholtz_pyr(nx, ny, nz, P, x, lam)) <= 1e-12, lam
+
+
+@pytest.mark.parametrize("kind", ["prism", "tet", "pyr"])
+def test_compact_maps_bitwise(torch, monkeypatch, kind):
+    """The compact int32 maps (sk_c0_gather_map32 / sk_c0_scatter_map32,
+    sign folded into the index) give bitwise the results of the int64 index
+    + double sign maps, on meshes with signed (prism) and unsigned maps."""
+    from paper_2604_04644_b200 import assembly as M
+
+    cls, dims = {"prism": (M.C0PrismMesh, (5, 4, 3)), "tet": (M.C0TetMesh, (3, 2, 3)),
+                 "pyr": (M.C0PyrMesh, (3, 2, 3))}[kind]
+    ys = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("SK_C0_MAP32", flag)
+        mesh = cls(*dims, 4)
+        assert (mesh._map32 is None) == (flag == "0")
+        x = np.random.default_rng(3).standard_normal(mesh.n_dofs)
+        ys.append(mesh.helmholtz(torch.from_numpy(x).cuda(), 0.9).cpu().numpy())
+    assert np.array_equal(ys[0], ys[1])
