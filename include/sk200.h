@@ -197,6 +197,12 @@ int sk_c0_scatter(int order, int nx, int ny, int64_t nz_local, const double* loc
  * A x.  Deformed geometry, lam > 0, hex bases only. */
 int sk_helmholtz_apply_c0(const sk_basis* b, int geo_class, int nx, int ny, int64_t nz_local, const double* x,
                           const double* hpay, double lam, double* out, void* stream);
+/* Elemental Helmholtz of a mapped C0 mesh (prism / pyramid / tet) with the
+ * gather fused into the kernel's tile load: out (element-major, W = 1) =
+ * H_e (A x) with A from the compact map l2gs (E x n_modes, as
+ * sk_c0_gather_map32).  Deformed geometry, lam >= 0, E * n_modes < 2^31. */
+int sk_helmholtz_apply_c0_mapped(const sk_basis* b, int geo_class, int64_t E, const int32_t* l2gs, const double* x,
+                                 const double* hpay, double lam, double* out, void* stream);
 
 /* Generic signed assembly maps (any shape; the prism C0 variant): gather
  * local(e, m) = sgn[e*n_modes+m] * x[l2g[e*n_modes+m]] into the lane-major

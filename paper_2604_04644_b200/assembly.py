@@ -260,14 +260,23 @@ class _MappedC0Mesh:
         s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
         vp = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
         nm = self.basis.n_modes
-        local = self.block.device(AccessQualifier.WRITE_ONLY)
         m32 = self._map32
-        if m32 is not None:
-            _lib.check(lib.sk_c0_gather_map32(self.E, nm, vp(m32[0]), vp(x), 1, vp(local), s), "sk_c0_gather_map32")
+        if m32 is not None and os.environ.get("SK_C0_FUSED", "1") != "0":
+            # gather fused into the elemental kernel's tile load
+            pay = self.block.payload(_lib.SK_PAYLOAD_HELMHOLTZ)
+            dout = self.out.device(AccessQualifier.WRITE_ONLY)
+            _lib.check(lib.sk_helmholtz_apply_c0_mapped(self.basis.handle, _lib.SK_GEO_DEFORMED, self.E, vp(m32[0]),
+                                                        vp(x), vp(pay), float(lam), vp(dout), s),
+                       "sk_helmholtz_apply_c0_mapped")
         else:
-            _lib.check(lib.sk_c0_gather_map(self.E, nm, vp(self._l2g), vp(self._sgn), vp(x), 1, vp(local), s),
-                       "sk_c0_gather_map")
-        helmholtz_apply(self.block, lam, out=self.out)
+            local = self.block.device(AccessQualifier.WRITE_ONLY)
+            if m32 is not None:
+                _lib.check(lib.sk_c0_gather_map32(self.E, nm, vp(m32[0]), vp(x), 1, vp(local), s),
+                           "sk_c0_gather_map32")
+            else:
+                _lib.check(lib.sk_c0_gather_map(self.E, nm, vp(self._l2g), vp(self._sgn), vp(x), 1, vp(local), s),
+                           "sk_c0_gather_map")
+            helmholtz_apply(self.block, lam, out=self.out)
         y = torch.empty(self.n_dofs, dtype=torch.float64, device=x.device)
         loc = self.out.device(AccessQualifier.READ_ONLY)
         if m32 is not None:

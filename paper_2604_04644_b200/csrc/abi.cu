@@ -844,6 +844,40 @@ int sk_apply_streamed_ex(const sk_basis* b, int op, int geo, int64_t E, int W, i
   return cuda_status(e, "streamed apply");
 }
 
+int sk_helmholtz_apply_c0_mapped(const sk_basis* b, int geo, int64_t E, const int32_t* l2gs, const double* x,
+                                 const double* hpay, double lam, double* out, void* stream) {
+  if (b && b->generic) return fail(SK_ERR_UNSUPPORTED, "the C0 variant needs the default quadrature");
+  if (!b || E < 0) return fail(SK_ERR_ARG, "bad C0 mesh");
+  if (b->ops->S == sk::HEX) return fail(SK_ERR_UNSUPPORTED, "mapped C0 gather: prism / pyramid / tet bases");
+  if (geo != SK_GEO_DEFORMED) return fail(SK_ERR_UNSUPPORTED, "fused C0 gather: deformed geometry");
+  if (!(lam >= 0.0)) return fail(SK_ERR_ARG, "reaction coefficient must be nonnegative");
+  if (E * (int64_t)b->hb.nm >= (int64_t(1) << 31)) return fail(SK_ERR_ARG, "compact map index range exceeded");
+  if (E > 0 && (!l2gs || !x || !hpay || !out)) return fail(SK_ERR_ARG, "null argument");
+  if (E == 0) return SK_OK;
+  int st = SK_OK;
+  const double* g = device_gtab(const_cast<sk_basis*>(b), &st);
+  if (st) return st;
+  sk::LaunchReq r;
+  r.fwd = b->fwd_vals.data();
+  r.fwd_d = b->fwd_ders.data();
+  r.dtab = b->dtab.data();
+  r.in = x;
+  r.out = out;
+  r.pay = hpay;
+  r.gtab = g;
+  r.E = E;
+  r.Epad = E;
+  r.in_cs = 0;
+  r.out_cs = E * b->hb.nm;
+  r.W = 1;
+  r.ncomp = 1;
+  r.geo = geo;
+  r.lam = lam;
+  r.c0map = l2gs;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cuda_status(b->ops->launch(sk::OP_HELM, r, stream), "mapped C0 kernel launch");
+}
+
 int sk_helmholtz_apply_c0(const sk_basis* b, int geo, int nx, int ny, int64_t nz_local, const double* x,
                           const double* hpay, double lam, double* out, void* stream) {
   if (b && b->generic) return fail(SK_ERR_UNSUPPORTED, "the C0 variant needs the default quadrature");

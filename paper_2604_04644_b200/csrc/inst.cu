@@ -540,6 +540,7 @@ int launch(int op, const LaunchReq& r, void* stream) {
   a.c0_ny = r.c0_ny;
   a.pad_ = 0;
   a.lam = r.lam;
+  a.c0map = reinterpret_cast<const int*>(r.c0map);
   const bool def = r.geo == GEO_DEFORMED;
   using namespace std;
   switch (op) {
@@ -550,6 +551,16 @@ int launch(int op, const LaunchReq& r, void* stream) {
 #if !defined(SK_ONLY_OP) || SK_ONLY_OP == 0
     case OP_HELM: {
       using C = Cfg<S, P, OP_HELM>;
+      if (r.c0map) {  // assembled C0, mapped mesh: gather fused into the tile load (deformed)
+        if constexpr (S != HEX) {
+          if (def) {
+            if (r.lam != 0.0)
+              return go<S, P, OP_HELM, k_helm<S, P, typename C::L, C::NT, C::PW, GEO_DEFORMED, true, C::MINB, 2>>(a, r, 1, stream);
+            return go<S, P, OP_HELM, k_helm<S, P, typename C::L, C::NT, C::PW, GEO_DEFORMED, false, C::MINB, 2>>(a, r, 1, stream);
+          }
+        }
+        return (int)cudaErrorInvalidValue;
+      }
       if (r.c0_nx > 0) {
         // assembled C0 hex: gather fused into the tile load (deformed, lam > 0)
         if constexpr (S == HEX) {

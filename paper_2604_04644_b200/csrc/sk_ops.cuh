@@ -42,6 +42,7 @@ struct OpArgs {
   int c0_nx, c0_ny;  // assembled C0 hex slab (fused gather from the global DOF vector)
   int pad_;
   double lam;
+  const int* __restrict__ c0map;  // assembled C0, mapped meshes: compact l2g (fused gather)
 };
 
 // Assembled C0 hex slab: the coefficient tile gathered straight from the
@@ -63,6 +64,29 @@ __device__ __forceinline__ void load_tile_c0(const double* __restrict__ x, const
       const int r = m % P1, q = (m / P1) % P1, p = m / (P1 * P1);
       const long long ex = eg % nx, ey = (eg / nx) % ny, ez = eg / ((long long)nx * ny);
       v = __ldg(x + (md(ez, r) * Ny + md(ey, q)) * Nx + md(ex, p));
+    }
+    xs[m * XS + e] = v;
+  }
+}
+
+// Assembled C0 on a mapped mesh (prism / tet / pyramid): the coefficient
+// tile gathered straight from the global DOF vector x through the compact
+// map (l2gs[e * NM + m] = (global index << 1) | negative sign, as
+// sk_c0_gather_map32), fusing the gather into the Helmholtz load.  Threads
+// walk the map element-major (coalesced map reads; x is L2-resident).
+template <class L, int NM, int NT>
+__device__ __forceinline__ void load_tile_mapped(const double* __restrict__ x, const Ctx& c,
+                                                 const int* __restrict__ l2gs, double* xs) {
+  constexpr int EB = L::EB, XS = L::XSTR;
+  const long long lim = (c.E - c.e0) * NM;
+  const int* mp = l2gs + c.e0 * NM;
+  for (int g = threadIdx.x; g < EB * NM; g += NT) {
+    const int e = g / NM, m = g - e * NM;
+    double v = 0.0;
+    if (g < lim) {
+      const int t = __ldg(mp + g);
+      const double xv = __ldg(x + (t >> 1));
+      v = (t & 1) ? -xv : xv;
     }
     xs[m * XS + e] = v;
   }
@@ -284,7 +308,7 @@ __global__ void __launch_bounds__(Op::NT, Op::MINB) k_persist_tma(const __grid_c
 
 // ---------------------------------------------------------------------------
 // Helmholtz, collocated: 9 sweeps + coefficient tile staging, 10 CTA barriers
-template <int S, int P, class L, int NT_, int PW, int GEO, bool LAMW, int MINB_, bool C0 = false, int RING = 0>
+template <int S, int P, class L, int NT_, int PW, int GEO, bool LAMW, int MINB_, int C0 = 0, int RING = 0>
 struct k_helm {
   static constexpr int NT = NT_;
   static constexpr int EB = L::EB;
@@ -355,7 +379,9 @@ struct k_helm {
           for (int s = 0; s < RING && s < Dims<S, P>::Q2; ++s) ring_issue(A, tile, s, s, sm);
       }
     }
-    if constexpr (C0)
+    if constexpr (C0 == 2)  // mapped mesh: compact l2g
+      load_tile_mapped<L, Dm::NM, NT>(A.in, c, A.c0map, sm + L::EB * L::PLANE);
+    else if constexpr (C0)  // structured hex slab
       load_tile_c0<L, P, NT>(A.in, c, A.c0_nx, A.c0_ny, sm + L::EB * L::PLANE);
     else
       load_tile<L, Dm::NM, NT>(A.in + blockIdx.y * A.in_cstride, c, sm + L::EB * L::PLANE);

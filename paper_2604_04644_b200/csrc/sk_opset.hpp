@@ -26,6 +26,7 @@ struct LaunchReq {
   int W, ncomp, geo;
   double lam;
   int c0_nx = 0, c0_ny = 0;  // > 0: assembled C0 hex slab, `in` is the global DOF vector
+  const int* c0map = nullptr;  // assembled C0 on a mapped mesh: compact l2g, `in` is the global DOF vector
   const double* dense = nullptr;  // mass only: DMMA StdMat fragments (sk_dense.cuh) -> dense kernel
 };
 

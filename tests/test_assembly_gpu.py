@@ -156,17 +156,23 @@ def test_assembled_pyr_matches_oracle(torch, P):
 @pytest.mark.parametrize("kind", ["prism", "tet", "pyr"])
 def test_compact_maps_bitwise(torch, monkeypatch, kind):
     """The compact int32 maps (sk_c0_gather_map32 / sk_c0_scatter_map32,
-    sign folded into the index) give bitwise the results of the int64 index
-    + double sign maps, on meshes with signed (prism) and unsigned maps."""
+    sign folded into the index) and the gather fused into the elemental
+    kernel (sk_helmholtz_apply_c0_mapped) give bitwise the results of the
+    int64 index + double sign maps, on meshes with signed (prism) and
+    unsigned maps, Helmholtz and stiffness."""
     from paper_2604_04644_b200 import assembly as M
 
     cls, dims = {"prism": (M.C0PrismMesh, (5, 4, 3)), "tet": (M.C0TetMesh, (3, 2, 3)),
                  "pyr": (M.C0PyrMesh, (3, 2, 3))}[kind]
     ys = []
-    for flag in ("0", "1"):
-        monkeypatch.setenv("SK_C0_MAP32", flag)
+    for map32, fused in (("0", "0"), ("1", "0"), ("1", "1")):
+        monkeypatch.setenv("SK_C0_MAP32", map32)
+        monkeypatch.setenv("SK_C0_FUSED", fused)
         mesh = cls(*dims, 4)
-        assert (mesh._map32 is None) == (flag == "0")
+        assert (mesh._map32 is None) == (map32 == "0")
         x = np.random.default_rng(3).standard_normal(mesh.n_dofs)
-        ys.append(mesh.helmholtz(torch.from_numpy(x).cuda(), 0.9).cpu().numpy())
-    assert np.array_equal(ys[0], ys[1])
+        for lam in (0.9, 0.0):
+            ys.append(mesh.helmholtz(torch.from_numpy(x).cuda(), lam).cpu().numpy())
+    # wide maps, compact maps, compact maps with the gather fused into the kernel
+    assert np.array_equal(ys[0], ys[2]) and np.array_equal(ys[0], ys[4])
+    assert np.array_equal(ys[1], ys[3]) and np.array_equal(ys[1], ys[5])
