@@ -197,6 +197,11 @@ int sk_c0_scatter(int order, int nx, int ny, int64_t nz_local, const double* loc
  * A x.  Deformed geometry, lam > 0, hex bases only. */
 int sk_helmholtz_apply_c0(const sk_basis* b, int geo_class, int nx, int ny, int64_t nz_local, const double* x,
                           const double* hpay, double lam, double* out, void* stream);
+/* Same with the output in the lane-major layout of width out_W (out_W
+ * divides the slab's element count; out_W = E is mode-major [mode][element],
+ * which the scatter reads coalesced along x). */
+int sk_helmholtz_apply_c0_w(const sk_basis* b, int geo_class, int nx, int ny, int64_t nz_local, const double* x,
+                            const double* hpay, double lam, double* out, int64_t out_W, void* stream);
 /* Elemental Helmholtz of a mapped C0 mesh (prism / pyramid / tet) with the
  * gather fused into the kernel's tile load: out (element-major, W = 1) =
  * H_e (A x) with A from the compact map l2gs (E x n_modes, as

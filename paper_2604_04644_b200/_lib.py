@@ -58,6 +58,7 @@ SIGNATURES = {
     "sk_c0_gather_map32": (_I, [_L, _I, _P, _P, _I, _P, _P]),
     "sk_c0_scatter_map32": (_I, [_L, _I, _P, _P, _P, _I, _P, _P]),
     "sk_helmholtz_apply_c0": (_I, [_P, _I, _I, _I, _L, _P, _P, _D, _P, _P]),
+    "sk_helmholtz_apply_c0_w": (_I, [_P, _I, _I, _I, _L, _P, _P, _D, _P, _L, _P]),
     "sk_helmholtz_apply_c0_mapped": (_I, [_P, _I, _L, _P, _P, _P, _D, _P, _P]),
     "sk_device_alloc": (_I, [_L, ctypes.POINTER(_P)]),
     "sk_device_free": (_I, [_P]),

@@ -880,6 +880,11 @@ int sk_helmholtz_apply_c0_mapped(const sk_basis* b, int geo, int64_t E, const in
 
 int sk_helmholtz_apply_c0(const sk_basis* b, int geo, int nx, int ny, int64_t nz_local, const double* x,
                           const double* hpay, double lam, double* out, void* stream) {
+  return sk_helmholtz_apply_c0_w(b, geo, nx, ny, nz_local, x, hpay, lam, out, 1, stream);
+}
+
+int sk_helmholtz_apply_c0_w(const sk_basis* b, int geo, int nx, int ny, int64_t nz_local, const double* x,
+                            const double* hpay, double lam, double* out, int64_t out_W, void* stream) {
   if (b && b->generic) return fail(SK_ERR_UNSUPPORTED, "the C0 variant needs the default quadrature");
   if (!b || nx < 1 || ny < 1 || nz_local < 0) return fail(SK_ERR_ARG, "bad C0 slab");
   if (b->ops->S != sk::HEX) return fail(SK_ERR_UNSUPPORTED, "assembled C0 variant is hex only");
@@ -887,6 +892,7 @@ int sk_helmholtz_apply_c0(const sk_basis* b, int geo, int nx, int ny, int64_t nz
   const long long E = (long long)nx * ny * nz_local;
   if (E > 0 && (!x || !hpay || !out)) return fail(SK_ERR_ARG, "null argument");
   if (E == 0) return SK_OK;
+  if (out_W < 1 || out_W > E || E % out_W || out_W > 0x7fffffff) return fail(SK_ERR_ARG, "output lane width must divide the element count");
   int st = SK_OK;
   const double* g = device_gtab(const_cast<sk_basis*>(b), &st);
   if (st) return st;
@@ -902,7 +908,7 @@ int sk_helmholtz_apply_c0(const sk_basis* b, int geo, int nx, int ny, int64_t nz
   r.Epad = E;
   r.in_cs = 0;
   r.out_cs = E * b->hb.nm;
-  r.W = 1;
+  r.W = (int)out_W;  // output layout (the input is the global DOF vector)
   r.ncomp = 1;
   r.geo = geo;
   r.lam = lam;

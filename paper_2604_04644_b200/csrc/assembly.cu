@@ -217,7 +217,7 @@ int sk_c0_scatter(int order, int nx, int ny, int64_t nz_local, const double* loc
     const char* e = std::getenv("SK_C0_SCATTER_TILED");
     return !(e && e[0] == '0');
   }();
-  if (tiled && Ny <= 65535 && (Nz + 31) / 32 <= 65535) {
+  if (tiled && W == 1 && Ny <= 65535 && (Nz + 31) / 32 <= 65535) {
     const dim3 grid((unsigned)((Nx + 31) / 32), (unsigned)Ny, (unsigned)((Nz + 31) / 32));
     k_c0_scatter_t<<<grid, dim3(32, 8), 0, static_cast<cudaStream_t>(stream)>>>(order, nx, ny, nz_local, local, W, y);
   } else {
