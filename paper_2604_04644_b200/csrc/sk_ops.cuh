@@ -54,15 +54,20 @@ struct OpArgs {
 template <class L, int P, int NT>
 __device__ __forceinline__ void load_tile_c0(const double* __restrict__ x, const Ctx& c, int nx, int ny, double* xs) {
   constexpr int P1 = P + 1, NM = P1 * P1 * P1, EB = L::EB, XS = L::XSTR;
+  static_assert(NT % EB == 0, "a thread keeps one tile element");
   const long long Nx = (long long)nx * P + 1, Ny = (long long)ny * P + 1;
   auto md = [](long long el, int k) { return el * P + (k == 0 ? 0 : k == 1 ? P : k - 1); };
-  for (int g = threadIdx.x; g < EB * NM; g += NT) {
-    const int m = g / EB, e = g - m * EB;
-    const long long eg = c.e0 + e;
+  // g = threadIdx.x + k NT walks (m, e) = (g / EB, g % EB): the element is
+  // fixed per thread, so its (ex, ey, ez) -- runtime divisions -- are
+  // computed once instead of per coefficient
+  const int e = threadIdx.x % EB;
+  const long long eg = c.e0 + e;
+  const bool live = eg < c.E;
+  const long long ex = eg % nx, ey = (eg / nx) % ny, ez = eg / ((long long)nx * ny);
+  for (int m = threadIdx.x / EB; m < NM; m += NT / EB) {
     double v = 0.0;
-    if (eg < c.E) {
+    if (live) {
       const int r = m % P1, q = (m / P1) % P1, p = m / (P1 * P1);
-      const long long ex = eg % nx, ey = (eg / nx) % ny, ez = eg / ((long long)nx * ny);
       v = __ldg(x + (md(ez, r) * Ny + md(ey, q)) * Nx + md(ex, p));
     }
     xs[m * XS + e] = v;
