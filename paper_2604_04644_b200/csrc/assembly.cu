@@ -46,6 +46,28 @@ __global__ void k_c0_gather(int P, int nx, int ny, long long nzl, const double* 
   }
 }
 
+// 32-bit form of dof_owners for per-axis indices (< 2^31): the runtime
+// divisions by P are 32-bit
+__device__ __forceinline__ int dof_owners32(int g, int P, int ne, int* el, int* md) {
+  int n = 0;
+  const int e = g / P;
+  const int o = g - e * P;
+  if (o == 0) {
+    if (e >= 1) {
+      el[n] = e - 1;
+      md[n++] = 1;
+    }
+    if (e < ne) {
+      el[n] = e;
+      md[n++] = 0;
+    }
+  } else {
+    el[n] = e;
+    md[n++] = o + 1;
+  }
+  return n;
+}
+
 // contributions of 1D DOF g: (element, mode) pairs, at most two
 __device__ __forceinline__ int dof_owners(long long g, int P, long long ne, long long* el, int* md) {
   int n = 0;
@@ -98,31 +120,31 @@ __global__ void k_c0_scatter(int P, int nx, int ny, long long nzl, const double*
 // y writes are coalesced (the one-DOF-per-thread form reads local with the
 // (P+1)^2 stride of the x modes).  Same summation order per DOF.
 __global__ void __launch_bounds__(256) k_c0_scatter_t(int P, int nx, int ny, long long nzl,
-                                                     const double* __restrict__ local, int W, double* __restrict__ y) {
+                                                     const double* __restrict__ local, double* __restrict__ y) {
   __shared__ double tile[32][33];
   const int P1 = P + 1, NM = P1 * P1 * P1;
   const long long Nx = (long long)nx * P + 1, Ny = (long long)ny * P + 1, Nz = nzl * P + 1;
-  const long long gx0 = (long long)blockIdx.x * 32, gz0 = (long long)blockIdx.z * 32;
-  const long long gy = blockIdx.y;
+  const int gx0 = blockIdx.x * 32, gz0 = blockIdx.z * 32;
+  const int gy = blockIdx.y;
   const int lane = threadIdx.x, warp = threadIdx.y;
-  long long ey[2], ez[2];
+  int ey[2], ez[2];
   int py[2], pz[2];
-  const int nyo = dof_owners(gy, P, ny, ey, py);
-  const long long gz = gz0 + lane;
-  const int nzo = gz < Nz ? dof_owners(gz, P, nzl, ez, pz) : 0;
+  const int nyo = dof_owners32(gy, P, ny, ey, py);
+  const int gz = gz0 + lane;
+  const int nzo = gz < Nz ? dof_owners32(gz, P, (int)nzl, ez, pz) : 0;
   for (int i = 0; i < 4; ++i) {
-    const long long gx = gx0 + warp + 8 * i;
+    const int gx = gx0 + warp + 8 * i;
     if (gx >= Nx || gz >= Nz) continue;
-    long long ex[2];
+    int ex[2];
     int px[2];
-    const int nxo = dof_owners(gx, P, nx, ex, px);
+    const int nxo = dof_owners32(gx, P, nx, ex, px);
     double s = 0.0;
     for (int c = 0; c < nzo; ++c)
       for (int b = 0; b < nyo; ++b)
         for (int a = 0; a < nxo; ++a) {
-          const long long e = (ez[c] * ny + ey[b]) * nx + ex[a];
+          const long long e = ((long long)ez[c] * ny + ey[b]) * nx + ex[a];
           const int m = (px[a] * P1 + py[b]) * P1 + pz[c];
-          s += local[lane_idx(e, m, NM, W)];
+          s += local[e * NM + m];  // interleave width 1: element-major
         }
     tile[warp + 8 * i][lane] = s;
   }
@@ -161,13 +183,19 @@ __global__ void k_c0_scatter_map(long long n, int nm, const long long* __restric
 // Compact maps: one int32 per entry, (index << 1) | (sign < 0), index < 2^30
 // -- a third of the map bytes of the int64 index + double sign form; the
 // signs are +-1, so negating is bitwise the same as multiplying by them
+// (interleave width 1 -- the meshes' only layout -- indexes local by the map
+// entry itself, t = e * nm + m; other widths pay the lane arithmetic)
 __global__ void k_c0_gather_map32(long long E, int nm, const int* __restrict__ l2gs, const double* __restrict__ x,
                                   int W, double* __restrict__ local) {
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < E * nm; t += (long long)gridDim.x * blockDim.x) {
-    const long long e = t / nm;
     const int v = __ldg(l2gs + t);
     const double xv = __ldg(x + (v >> 1));
-    local[lane_idx(e, (int)(t - e * nm), nm, W)] = (v & 1) ? -xv : xv;
+    long long idx = t;
+    if (W != 1) {
+      const long long e = t / nm;
+      idx = lane_idx(e, (int)(t - e * nm), nm, W);
+    }
+    local[idx] = (v & 1) ? -xv : xv;
   }
 }
 
@@ -177,9 +205,13 @@ __global__ void k_c0_scatter_map32(long long n, int nm, const int* __restrict__ 
     double s = 0.0;
     for (int k = __ldg(ptr + g), k1 = __ldg(ptr + g + 1); k < k1; ++k) {
       const int v = __ldg(locs + k);
-      const long long t = v >> 1, e = t / nm;
-      const double lv = local[lane_idx(e, (int)(t - e * nm), nm, W)];
-      s = fma((v & 1) ? -1.0 : 1.0, lv, s);
+      const int t = v >> 1;
+      long long idx = t;
+      if (W != 1) {
+        const int e = t / nm;
+        idx = lane_idx(e, t - e * nm, nm, W);
+      }
+      s = fma((v & 1) ? -1.0 : 1.0, local[idx], s);
     }
     y[g] = s;
   }
@@ -217,9 +249,9 @@ int sk_c0_scatter(int order, int nx, int ny, int64_t nz_local, const double* loc
     const char* e = std::getenv("SK_C0_SCATTER_TILED");
     return !(e && e[0] == '0');
   }();
-  if (tiled && W == 1 && Ny <= 65535 && (Nz + 31) / 32 <= 65535) {
+  if (tiled && W == 1 && Ny <= 65535 && (Nz + 31) / 32 <= 65535 && Nx < (1LL << 31) && Nz < (1LL << 31)) {
     const dim3 grid((unsigned)((Nx + 31) / 32), (unsigned)Ny, (unsigned)((Nz + 31) / 32));
-    k_c0_scatter_t<<<grid, dim3(32, 8), 0, static_cast<cudaStream_t>(stream)>>>(order, nx, ny, nz_local, local, W, y);
+    k_c0_scatter_t<<<grid, dim3(32, 8), 0, static_cast<cudaStream_t>(stream)>>>(order, nx, ny, nz_local, local, y);
   } else {
     k_c0_scatter<<<grid_for(N), 256, 0, static_cast<cudaStream_t>(stream)>>>(order, nx, ny, nz_local, local, W, y);
   }
