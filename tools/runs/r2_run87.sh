@@ -1,0 +1,4 @@
+# driver-equivalent validation after the C0 work: GPU suite, smoke, default bench
+timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/r2run87_pytest.log 2>&1; echo "pytest rc=$?"; tail -1 gpurun_out/r2run87_pytest.log; grep FAILED gpurun_out/r2run87_pytest.log | head
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r2run87_smoke.log 2>&1; echo "smoke rc=$?"; tail -1 gpurun_out/r2run87_smoke.log
+timeout 900 python bench.py > gpurun_out/r2run87_bench.json 2> gpurun_out/r2run87_bench.err; echo "bench rc=$?"
