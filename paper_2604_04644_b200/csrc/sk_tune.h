@@ -308,7 +308,9 @@ constexpr int kDenseMaxP = 6;
 // Measured on B200 (roofline fraction sum-fac -> dense): deformed
 // (profiles/r02/mass_dense_def_*.jsonl) P=1 every shape (hex 0.60 -> 0.70,
 // prism 0.56 -> 0.74, pyr 0.46 -> 0.69, tet 0.41 -> 0.73), pyr / tet P=2
-// (0.46 -> 0.62, 0.48 -> 0.53); regular (|J| M_ref, one GEMM;
+// (0.46 -> 0.62, 0.48 -> 0.53), tet P=3 (0.47 -> 0.54, re-measured with the
+// register-bounded dense kernel, profiles/r02/dense_vs_sumfac_p2to4.txt);
+// regular (|J| M_ref, one GEMM;
 // profiles/r02/dense_mass_regular_*.jsonl) hex P<=2 (0.23/0.35 ->
 // 0.76/0.58), prism P<=4 (0.22-0.38 -> 0.48-0.69), pyr P<=5 (0.17-0.37 ->
 // 0.59-0.89), tet P<=6 (0.19-0.33 -> 0.65-1.16); slower elsewhere.
@@ -322,7 +324,7 @@ constexpr bool kDenseMass[2][4][11] = {
     {{0, 1, 0, 0, 0, 0, 0},
      {0, 1, 0, 0, 0, 0, 0},
      {0, 1, 1, 0, 0, 0, 0},
-     {0, 1, 1, 0, 0, 0, 0}},
+     {0, 1, 1, 1, 0, 0, 0}},
 };
 
 // Regular-geometry collocated Helmholtz / stiffness by StdMat on DMMA
