@@ -316,7 +316,7 @@ constexpr int kDenseMaxP = 6;
 // 0.59-0.89), tet P<=6 (0.19-0.33 -> 0.65-1.16); slower elsewhere.
 constexpr bool kDenseMass[2][4][11] = {
     // regular   P: 0  1  2  3  4  5  6
-    {{0, 1, 1, 0, 0, 0, 0},   // hex
+    {{0, 1, 1, 1, 0, 0, 0},   // hex (P=3: 0.38 -> 0.49, profiles/r02/dense_vs_sumfac_regular.txt)
      {0, 1, 1, 1, 1, 0, 0},   // prism
      {0, 1, 1, 1, 1, 1, 0},   // pyr
      {0, 1, 1, 1, 1, 1, 1}},  // tet
